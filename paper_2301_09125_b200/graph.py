@@ -22,6 +22,7 @@ unit-weight undirected edge list, without the general lexsort.
 
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
@@ -116,6 +117,32 @@ def preprocess(graph: Graph, unit_weights: bool = True, self_loops: bool = True)
 
 
 def undirected_csr(n: int, u, v, weights=None) -> Graph:
+    """Canonical preprocessed graph from an undirected edge list.
+
+    Equivalent to ``preprocess(from_arcs(n, u, v, 1), unit_weights=True)``
+    (with ``weights``: the same graph carrying per-edge weights, max over
+    duplicate pairs).  Unit-weight lists go through the native builder
+    (``lp_csr_build_undirected``, OpenMP); weighted ones through numpy.
+    """
+    if weights is None:
+        from . import _lib
+
+        u = np.ascontiguousarray(u, dtype=np.int64).ravel()
+        v = np.ascontiguousarray(v, dtype=np.int64).ravel()
+        if u.shape != v.shape:
+            raise ValueError("u and v must have equal length")
+        offsets = np.empty(n + 1, dtype=np.int64)
+        nbr = np.empty(2 * u.size + n, dtype=np.int64)
+        m = C.c_int64(0)
+        _lib.check(_lib.lib().lp_csr_build_undirected(n, u.size, u, v, offsets, nbr, C.byref(m)))
+        nbr = nbr[: m.value].copy()
+        wts = np.ones(m.value, dtype=np.float64)
+        total = float(m.value + n)
+        return Graph(n, int(m.value), _ro(offsets), _ro(nbr), _ro(wts), total)
+    return undirected_csr_numpy(n, u, v, weights)
+
+
+def undirected_csr_numpy(n: int, u, v, weights=None) -> Graph:
     """Canonical preprocessed graph from an undirected edge list, fast.
 
     Equivalent to ``preprocess(from_arcs(n, u, v, 1), unit_weights=True)``

@@ -182,17 +182,15 @@ def planted_partition(n: int = 100_000, communities: int = 1_000, intra: int = 1
 
 def rmat_edges(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19,
                c: float = 0.19, seed: int = 1):
-    """Raw R-MAT edge list: one quadrant draw per bit level, no noise, no
-    vertex-id scrambling (so vertex 0 is the largest hub)."""
+    """Raw R-MAT edge list (native, ``lp_gen_rmat``): one quadrant draw per
+    bit level from a counter RNG keyed by (seed, edge, level); no noise, no
+    vertex-id scrambling (vertex 0 is the largest hub)."""
+    from . import _lib
+
     m = edge_factor << scale
-    rng = np.random.default_rng(seed)
-    src = np.zeros(m, dtype=np.int64)
-    dst = np.zeros(m, dtype=np.int64)
-    ab, abc = a + b, a + b + c
-    for bit in range(scale - 1, -1, -1):
-        x = rng.random(m, dtype=np.float32)
-        src |= (x >= ab).astype(np.int64) << bit
-        dst |= (((x >= a) & (x < ab)) | (x >= abc)).astype(np.int64) << bit
+    src = np.empty(m, dtype=np.int64)
+    dst = np.empty(m, dtype=np.int64)
+    _lib.check(_lib.lib().lp_gen_rmat(scale, m, a, b, c, seed, src, dst))
     return src, dst
 
 

@@ -1,0 +1,4 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+make -s -C paper_2301_09125_b200/csrc && make -s -C oracle
+timeout 900 python -m pytest tests/test_rak_gpu.py -x -q 2>&1 | tail -30

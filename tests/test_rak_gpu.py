@@ -1,0 +1,194 @@
+"""GPU parity for the RAK sweep, through the public API (rak_detect ->
+ctypes -> liblabelprop_cuda.so).
+
+Bars:
+* batches = 0 (the reference's visit order), strict: labels bit-exact to the
+  REFERENCE after every sweep and the same iteration count (golden fixtures
+  produced by the reference itself);
+* every schedule / tie rule: labels bit-exact to the oracle's restatement of
+  the same schedule after every sweep;
+* float weights in [1, 2) (float32-exact): bit-exact as well (exact 64-bit
+  fixed-point sums).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2301_09125_b200 as lp
+from conftest import load_graph, partition_matches
+
+pytestmark = pytest.mark.gpu
+
+ORACLE_TIE = {"scan-first": 0, "random": 1, "min-label": 2}
+
+
+def _names(z):
+    return sorted({k.split("/")[0] for k in z.files})
+
+
+def gpu_per_iteration(g, params, upto):
+    out = []
+    for k in range(1, upto + 1):
+        p = lp.RakParams(**{**params.__dict__, "max_iterations": k})
+        out.append(lp.rak_detect(g, p).assignment)
+    return np.stack(out)
+
+
+def test_exact_schedule_matches_reference_every_iteration(gpu, golden_rak):
+    checked = 0
+    for name in _names(golden_rak):
+        g = load_graph(golden_rak, name)
+        for seed in (1, 2, 3):
+            for tol in (0.05, 1e-4):
+                key = f"{name}/s/{seed}/{tol:g}"
+                want_it = int(golden_rak[f"{key}/iterations"])
+                want = golden_rak[f"{key}/labels_per_iter"]
+                p = lp.RakParams(strict=True, seed=seed, tolerance=tol, max_iterations=100)
+                res = lp.rak_detect(g, p)
+                assert res.iterations == want_it, key
+                assert np.array_equal(res.assignment, want[-1]), key
+                assert res.modularity == pytest.approx(float(golden_rak[f"{key}/modularity"]), abs=1e-12)
+                if tol == 0.05:
+                    assert np.array_equal(gpu_per_iteration(g, p, want_it), want), key
+                checked += 1
+    assert checked == 6 * len(_names(golden_rak))
+
+
+@pytest.mark.parametrize("tie", ["scan-first", "random", "min-label"])
+@pytest.mark.parametrize("batches", [0, 1, 7, 64])
+def test_schedules_match_oracle_every_iteration(gpu, golden_rak, oracle, tie, batches):
+    for name in ("gnp_1000", "gnp_3000", "planted_4000", "rmat_12", "rmat_12_w", "ring_16x6", "grid_64", "star_50"):
+        g = load_graph(golden_rak, name)
+        for seed in (1, 5):
+            want, it, changed, per = oracle.rak(g, batches=batches, tie=ORACLE_TIE[tie], seed=seed, tolerance=1e-4,
+                                                max_iterations=12, per_iteration=True)
+            p = lp.RakParams(seed=seed, tolerance=1e-4, max_iterations=12, batches=batches, tie=tie)
+            res = lp.rak_detect(g, p, changed_history=True)
+            assert res.iterations == it, (name, seed)
+            assert np.array_equal(res.stats["changed"], changed), (name, seed)
+            assert np.array_equal(res.assignment, want), (name, seed)
+            assert np.array_equal(gpu_per_iteration(g, p, it), per), (name, seed)
+
+
+def test_weighted_graph_uses_exact_fixed_point(gpu, golden_rak):
+    g = load_graph(golden_rak, "rmat_12_w")
+    info = lp._lib.device_graph(g).info()
+    assert info["weight_mode"] == "fixed"
+
+
+def test_non_strict_quality_close_to_reference(gpu, golden_rak):
+    """Counter-RNG non-strict vs the reference's xorshift non-strict: the
+    draws differ, so compare modularity (the reference's own seed spread is
+    the yardstick on these small graphs)."""
+    for name in ("gnp_3000", "planted_4000", "rmat_12"):
+        g = load_graph(golden_rak, name)
+        ref_q = [float(golden_rak[f"{name}/ns/{s}/0.05/modularity"]) for s in (1, 2, 3)]
+        ours = [lp.rak_detect(g, lp.RakParams(strict=False, seed=s)).modularity for s in (1, 2, 3)]
+        spread = max(ref_q) - min(ref_q)
+        assert abs(np.mean(ours) - np.mean(ref_q)) <= max(0.02, 2 * spread), (name, ours, ref_q)
+
+
+class TestReferenceBehaviour:
+    """The reference's own RAK tests (tests/test_rak.py), run on the GPU."""
+
+    def test_two_disjoint_four_cliques_strict(self, gpu):
+        g = lp.disjoint_cliques(2, 4)
+        assert partition_matches(lp.rak_detect(g, lp.RakParams(strict=True, seed=1)).assignment, 2, 4)
+
+    def test_isolated_vertices_keep_their_labels(self, gpu):
+        res = lp.rak_detect(lp.gnp(12, 0.0), lp.RakParams(strict=True, seed=1))
+        assert np.array_equal(res.assignment, np.arange(12)) and res.iterations == 1
+
+    def test_star_collapses_to_one_community(self, gpu):
+        res = lp.rak_detect(lp.star(5), lp.RakParams(strict=True, seed=1))
+        assert len(set(res.assignment.tolist())) == 1 and res.iterations <= 2
+
+    def test_clique_recovery_all_modes_and_seeds(self, gpu):
+        g = lp.disjoint_cliques(8, 6)
+        for strict in (True, False):
+            for seed in range(1, 11):
+                res = lp.rak_detect(g, lp.RakParams(strict=strict, seed=seed))
+                assert partition_matches(res.assignment, 8, 6), (strict, seed)
+
+    def test_ring_of_cliques_not_degenerate(self, gpu):
+        g = lp.ring_of_cliques(16, 6)
+        for strict in (True, False):
+            clean = sum(np.bincount(lp.rak_detect(g, lp.RakParams(strict=strict, seed=s)).assignment).max()
+                        <= g.vertex_count / 2 for s in range(1, 21))
+            assert clean >= 18
+
+    def test_strict_is_deterministic(self, gpu):
+        g = lp.gnp(500, 0.02, seed=5)
+        a = lp.rak_detect(g, lp.RakParams(strict=True, seed=9)).assignment
+        b = lp.rak_detect(g, lp.RakParams(strict=True, seed=9)).assignment
+        assert a.tobytes() == b.tobytes()
+
+    def test_tolerance_monotonic_and_prefix(self, gpu):
+        for g in (lp.gnp(400, 0.02, seed=2), lp.ring_of_cliques(8, 5)):
+            loose = lp.rak_detect(g, lp.RakParams(tolerance=0.1, strict=True, seed=4))
+            tight = lp.rak_detect(g, lp.RakParams(tolerance=0.0001, strict=True, seed=4))
+            assert tight.iterations >= loose.iterations
+            replay = lp.rak_detect(g, lp.RakParams(tolerance=0.0001, strict=True, seed=4,
+                                                   max_iterations=loose.iterations))
+            assert np.array_equal(loose.assignment, replay.assignment)
+
+    def test_asymmetric_graph_rejected(self, gpu):
+        with pytest.raises(ValueError, match="symmetric"):
+            lp.rak_detect(lp.from_arcs(2, [0], [1], [1.0]))
+
+    def test_empty_graph(self, gpu):
+        res = lp.rak_detect(lp.preprocess(lp.from_arcs(0, [], [], [])))
+        assert res.iterations == 0 and res.assignment.size == 0
+
+    def test_labels_stay_in_range(self, gpu):
+        res = lp.rak_detect(lp.gnp(200, 0.05, seed=8), lp.RakParams(seed=3))
+        assert res.assignment.min() >= 0 and res.assignment.max() < 200 and res.iterations <= 100
+
+
+class TestEdgeCases:
+    def test_graph_without_self_loops(self, gpu, oracle):
+        """Degree-1 rows whose arc is not a self-loop must still move."""
+        g = lp.preprocess(lp.from_arcs(6, [0, 1, 3, 4], [1, 2, 4, 5], np.ones(4)), self_loops=False)
+        for batches in (0, 1):
+            want, it, _ = oracle.rak(g, batches=batches, tie=0, tolerance=1e-4, max_iterations=10)
+            res = lp.rak_detect(g, lp.RakParams(strict=True, tolerance=1e-4, max_iterations=10, batches=batches))
+            assert np.array_equal(res.assignment, want) and res.iterations == it
+
+    def test_custom_order_and_initial_labels(self, gpu, oracle):
+        g = lp.gnp(800, 0.01, seed=4)
+        rng = np.random.default_rng(0)
+        order = rng.permutation(800)
+        init = rng.integers(0, 800, 800)
+        for batches in (0, 3):
+            want, it, _ = oracle.rak(g, batches=batches, tie=0, order=order, labels=init, tolerance=1e-3,
+                                     max_iterations=20)
+            res = lp.rak_detect(g, lp.RakParams(strict=True, tolerance=1e-3, max_iterations=20, batches=batches),
+                                order=order, labels=init)
+            assert np.array_equal(res.assignment, want) and res.iterations == it
+
+    def test_bad_order_and_labels_rejected(self, gpu):
+        g = lp.gnp(50, 0.1, seed=1)
+        with pytest.raises(ValueError):
+            lp.rak_detect(g, order=np.zeros(50, dtype=np.int64))
+        with pytest.raises(ValueError):
+            lp.rak_detect(g, labels=np.full(50, 50))
+
+    def test_single_vertex(self, gpu):
+        res = lp.rak_detect(lp.gnp(1, 0.0), lp.RakParams(strict=True))
+        assert res.assignment.tolist() == [0] and res.iterations == 1
+
+    def test_hub_multipass_matches_oracle(self, gpu, oracle):
+        """A hub whose distinct neighbour labels exceed one shared-memory
+        table (forces the multi-pass partitioned tally and its overflow retry)."""
+        n = 30_000
+        hub_edges = np.arange(1, n)
+        rng = np.random.default_rng(3)
+        extra_u = rng.integers(1, n, 40_000)
+        extra_v = rng.integers(1, n, 40_000)
+        g = lp.undirected_csr(n, np.concatenate([np.zeros(n - 1, np.int64), extra_u]),
+                              np.concatenate([hub_edges, extra_v]))
+        for tie, otie in (("scan-first", 0), ("random", 1), ("min-label", 2)):
+            for batches in (0, 1):
+                want, it, _ = oracle.rak(g, batches=batches, tie=otie, tolerance=1e-4, max_iterations=6)
+                res = lp.rak_detect(g, lp.RakParams(tie=tie, tolerance=1e-4, max_iterations=6, batches=batches))
+                assert np.array_equal(res.assignment, want) and res.iterations == it, (tie, batches)
