@@ -91,11 +91,13 @@ typedef struct lp_rak_opts {
     int64_t reserved[6];
 } lp_rak_opts;
 
-/* Degree bins of the engine, index of the bin_* arrays. */
-#define LP_BIN_HUB 0   /* deg > 2048: block per vertex, multi-pass 8K table */
-#define LP_BIN_LARGE 1 /* 257..2048: block per vertex, 4K table            */
-#define LP_BIN_MID 2   /* 17..256: warp per vertex                          */
-#define LP_BIN_SMALL 3 /* 2..16: thread per vertex                          */
+/* Kernel slots of the engine, index of the lp_run_stats
+ * bin_* arrays.  A vertex is routed each round by its degree d and its
+ * estimated distinct neighbour labels. */
+#define LP_BIN_HUB 0   /* 16-warp block per (vertex, label partition | arc slice) */
+#define LP_BIN_TEAM 1  /* 8-warp block per vertex, est <= 2048, d <= 16384   */
+#define LP_BIN_WARP 2  /* warp per vertex, est <= 256, d <= 2048              */
+#define LP_BIN_SMALL 3 /* thread per vertex, d <= 16                          */
 
 typedef struct lp_run_stats {
     int32_t iterations;     /* sweeps run (rak.py:94-95 semantics)          */
@@ -106,11 +108,11 @@ typedef struct lp_run_stats {
     int64_t arcs_dense;     /* edge_count * iterations (dense-equivalent)   */
     int32_t launches;       /* sweep kernels launched (excl. copies/memsets) */
     int32_t reserved0;
-    double bin_ms[4];       /* LP_RAK_PROFILE: summed launch time per bin   */
+    double bin_ms[4];       /* LP_RAK_PROFILE: summed launch time per slot  */
     int64_t bin_launches[4];
     int64_t bin_arcs[4];    /* arcs scanned per bin                         */
     int64_t bin_vertices[4];/* vertex evaluations per bin                   */
-    double aux_ms;          /* LP_RAK_PROFILE: frontier compaction time     */
+    double aux_ms;          /* LP_RAK_PROFILE: routing kernels' time        */
     int64_t reserved[4];
 } lp_run_stats;
 

@@ -61,7 +61,7 @@ class RakOpts(C.Structure):
 
 
 RAK_PROFILE = 1
-BIN_NAMES = ("hub", "large", "mid", "small")
+BIN_NAMES = ("hub", "team", "warp", "small")
 
 
 class RunStats(C.Structure):

@@ -38,23 +38,22 @@
 
 using namespace lp;
 
-// ---------------------------------------------------------------------------
-// bins
-// ---------------------------------------------------------------------------
-enum Bin : int { kBinHub = 0, kBinLarge = 1, kBinMid = 2, kBinSmall = 3, kBinIdle = 4, kNumBins = 4 };
-constexpr int kHubMin = 2048;   // deg > kHubMin: hub kernel (8K table, multi-pass)
-constexpr int kLargeMin = kWarpMax;  // deg > 256: block kernel (4K table)
-constexpr int kHubBits = 13, kHubThreads = 512;
-constexpr int kLargeBits = 12, kLargeThreads = 256;
+// Storage bins: rows with d > kSmallMax (sorted by degree, descending, so the
+// dense route hands out the largest hubs first), then the small rows by degree
+// class 9..16, 5..8, 2..4 (visit order inside a class), then idle vertices (no
+// arc but a self-loop: label fixed).
+enum Bin : int { kBinBig = 0, kBinS16 = 1, kBinS8 = 2, kBinS4 = 3, kBinIdle = 4, kNumBins = 5 };
+// per-kernel accounting slots (lp_run_stats.bin_*)
+enum KernelSlot : int { kKHub = 0, kKTeam = 1, kKWarp = 2, kKSmall = 3, kKSlots = 4 };
 
-#define LP_CK(call)                                                                         \
-    do {                                                                                    \
-        cudaError_t _e = (call);                                                            \
-        if (_e != cudaSuccess) {                                                            \
-            lp_set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(_e), __FILE__, __LINE__, \
-                         cudaGetErrorString(_e));                                           \
-            return LP_ERR_CUDA;                                                             \
-        }                                                                                   \
+#define LP_CK(call)                                                                                  \
+    do {                                                                                             \
+        cudaError_t _e = (call);                                                                     \
+        if (_e != cudaSuccess) {                                                                     \
+            lp_set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(_e), __FILE__, __LINE__,     \
+                         cudaGetErrorString(_e));                                                    \
+            return LP_ERR_CUDA;                                                                      \
+        }                                                                                            \
     } while (0)
 
 template <typename T> static cudaError_t dalloc(T** p, size_t count, int64_t* bytes) {
@@ -77,7 +76,9 @@ struct Plan {
     int32_t* ndist = nullptr;        // [S]
     int64_t S = 0;
     int64_t m_active = 0;
-    int32_t bin_beg[kNumBins + 1] = {0, 0, 0, 0, 0};
+    int32_t bin_beg[kNumBins + 1] = {0, 0, 0, 0, 0, 0};  // slot range of each bin (idle: [.., n))
+    int32_t big_end = 0;             // slots [0, big_end) are big rows, [big_end, S) small
+    int64_t bytes = 0;
 };
 
 struct lp_graph {
@@ -86,6 +87,7 @@ struct lp_graph {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int64_t n = 0, m = 0;
     int64_t max_degree = 0;
+    int64_t sliceable = 0;  // rows long enough to be cut into slices
     int wmode = kUnit;
     int fixed_shift = 0;
     int64_t bytes = 0;
@@ -99,11 +101,11 @@ struct lp_graph {
     int32_t* labB = nullptr;
     int32_t* cur = nullptr;  // the buffer holding the latest labels
     uint8_t* mark = nullptr;
-    int32_t* lists = nullptr;  // kNumBins frontier lists of n entries
-    int32_t* list_len = nullptr;  // kNumBins
+    Routes routes;
+    int64_t cap_items = 0;
     unsigned long long* counters = nullptr;
     int64_t* out64 = nullptr;
-    int32_t* h_list_len = nullptr;          // pinned
+    int32_t* h_len = nullptr;                  // pinned route lengths
     unsigned long long* h_counters = nullptr;  // pinned
     void* cub_tmp = nullptr;
     size_t cub_tmp_bytes = 0;
@@ -166,11 +168,16 @@ __global__ void k_weight_convert(const double* __restrict__ w, uint32_t* __restr
     }
 }
 
-__global__ void k_degree_max(const uint32_t* __restrict__ off, int64_t n, unsigned long long* out) {
-    unsigned long long mx = 0;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
-        mx = max(mx, (unsigned long long)(off[v + 1] - off[v]));
+// [0] max degree, [1] rows longer than two slices
+__global__ void k_degree_stats(const uint32_t* __restrict__ off, int64_t n, unsigned long long* out) {
+    unsigned long long mx = 0, sl = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long d = off[v + 1] - off[v];
+        mx = max(mx, d);
+        sl += d > 2ull * kSliceArcs;
+    }
     atomicMax(out, mx);
+    if (sl) atomicAdd(out + 1, sl);
 }
 
 __global__ void k_plan_pos(const int64_t* __restrict__ order, int32_t* __restrict__ vid, int32_t* __restrict__ pos,
@@ -197,29 +204,28 @@ __global__ void k_plan_check_perm(const int32_t* __restrict__ vid, const int32_t
     if (b) atomicAdd(bad, b);
 }
 
-__device__ __forceinline__ int degree_bin(uint32_t d, bool self_only) {
-    if (d == 0 || (d == 1 && self_only)) return kBinIdle;  // label provably cannot move
-    if (d > (uint32_t)kHubMin) return kBinHub;
-    if (d > (uint32_t)kLargeMin) return kBinLarge;
-    if (d > (uint32_t)kSmallMax) return kBinMid;
-    return kBinSmall;
-}
-
-__global__ void k_plan_bins(const int32_t* __restrict__ vid, const uint32_t* __restrict__ off,
-                            const int32_t* __restrict__ nbr, uint8_t* __restrict__ bin, int64_t n,
+// storage sort key: bin in bits 32..34; big rows by descending degree
+__global__ void k_plan_keys(const int32_t* __restrict__ vid, const uint32_t* __restrict__ off,
+                            const int32_t* __restrict__ nbr, unsigned long long* __restrict__ key, int64_t n,
                             unsigned long long* counts) {
-    __shared__ unsigned long long sc[kBinIdle + 1];
-    if (threadIdx.x <= kBinIdle) sc[threadIdx.x] = 0;
+    __shared__ unsigned long long sc[kNumBins];
+    if (threadIdx.x < kNumBins) sc[threadIdx.x] = 0;
     __syncthreads();
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = vid[p];
         const uint32_t d = off[v + 1] - off[v];
-        const int b = degree_bin(d, d == 1 && nbr[off[v]] == v);
-        bin[p] = (uint8_t)b;
+        int b;
+        if (d == 0 || (d == 1 && nbr[off[v]] == v))
+            b = kBinIdle;  // label provably cannot move
+        else if (d > (uint32_t)kSmallMax)
+            b = kBinBig;
+        else
+            b = d > 8 ? kBinS16 : (d > 4 ? kBinS8 : kBinS4);
+        key[p] = ((unsigned long long)b << 32) | (b == kBinBig ? (0xffffffffull - d) : 0ull);
         atomicAdd(&sc[b], 1ull);
     }
     __syncthreads();
-    if (threadIdx.x <= kBinIdle && sc[threadIdx.x]) atomicAdd(counts + threadIdx.x, sc[threadIdx.x]);
+    if (threadIdx.x < kNumBins && sc[threadIdx.x]) atomicAdd(counts + threadIdx.x, sc[threadIdx.x]);
 }
 
 __global__ void k_iota(int32_t* a, int64_t n) {
@@ -229,20 +235,24 @@ __global__ void k_iota(int32_t* a, int64_t n) {
 
 __global__ void k_plan_slots(const int32_t* __restrict__ spos, const int32_t* __restrict__ vid,
                              const uint32_t* __restrict__ off, int32_t* __restrict__ slot_of_pos,
-                             uint32_t* __restrict__ sdeg, int32_t* __restrict__ ndist, int64_t n, int64_t S) {
+                             uint32_t* __restrict__ sdeg, int64_t n, int64_t S) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         const int32_t p = spos[s];
         if (s < S) {
             const int32_t v = vid[p];
-            const uint32_t d = off[v + 1] - off[v];
             slot_of_pos[p] = (int32_t)s;
-            sdeg[s] = d;
-            ndist[s] = (int32_t)d;
+            sdeg[s] = off[v + 1] - off[v];
         } else {
             slot_of_pos[p] = -1;
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) sdeg[S] = 0;
+}
+
+// distinct-label estimates restart from the degree at every run
+__global__ void k_reset_ndist(const uint32_t* __restrict__ soff, int32_t* __restrict__ ndist, int64_t S) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S; s += (int64_t)gridDim.x * blockDim.x)
+        ndist[s] = (int32_t)(soff[s + 1] - soff[s]);
 }
 
 // one warp per slot: copy the row, translating neighbour ids to positions
@@ -282,47 +292,11 @@ __global__ void k_scatter_labels(const int32_t* __restrict__ vid, const int32_t*
         out[vid[p]] = lab[p];
 }
 
-// frontier compaction: marked positions -> per-bin slot lists (marks cleared)
-struct BinBounds {
-    int32_t beg[kNumBins + 1];
-};
-
-__global__ void k_compact(uint8_t* __restrict__ mark, const int32_t* __restrict__ slot_of_pos, int64_t n,
-                          BinBounds bins, int32_t* __restrict__ lists, int32_t* __restrict__ list_len, int64_t cap) {
-    const int lane = threadIdx.x & 31;
-    for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; base < n;
-         base += (int64_t)gridDim.x * blockDim.x * 4) {
-        uint32_t word = 0;
-        if (base + 4 <= n) {
-            word = *reinterpret_cast<const uint32_t*>(mark + base);
-            if (word) *reinterpret_cast<uint32_t*>(mark + base) = 0u;
-        } else {
-            for (int j = 0; j < 4 && base + j < n; ++j) {
-                word |= (uint32_t)mark[base + j] << (8 * j);
-                mark[base + j] = 0;
-            }
-        }
-        for (int j = 0; j < 4; ++j) {
-            int b = -1;
-            int32_t s = -1;
-            if ((word >> (8 * j)) & 0xff) {
-                s = slot_of_pos[base + j];
-                if (s >= 0) {
-                    b = 0;
-                    while (b < kNumBins - 1 && s >= bins.beg[b + 1]) ++b;
-                }
-            }
-            // warp-aggregated append per bin
-            for (int bb = 0; bb < kNumBins; ++bb) {
-                const uint32_t msk = __ballot_sync(__activemask(), b == bb);
-                if (!msk) continue;
-                int32_t base_idx = 0;
-                const int leader = __ffs(msk) - 1;
-                if (lane == leader) base_idx = atomicAdd(list_len + bb, __popc(msk));
-                base_idx = __shfl_sync(__activemask(), base_idx, leader);
-                if (b == bb) lists[bb * cap + base_idx + __popc(msk & lanemask_lt())] = s;
-            }
-        }
+__global__ void k_gtab_init(int32_t* keys, uint32_t* first, unsigned long long* acc, int64_t count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        keys[i] = kEmpty;
+        first[i] = 0xffffffffu;
+        acc[i] = 0ull;
     }
 }
 
@@ -339,9 +313,9 @@ static int grid_for(int64_t work, int per_block, int cap_blocks) {
 struct Prof {
     bool on = false;
     int launches = 0;
-    int64_t bin_launches[kNumBins] = {0, 0, 0, 0};
+    int64_t slot_launches[kKSlots] = {0, 0, 0, 0};
     std::vector<cudaEvent_t>* pool = nullptr;
-    std::vector<int> tags;  // bin per pair, -1 = auxiliary
+    std::vector<int> tags;  // kernel slot per pair, -1 = routing
     size_t used = 0;
     cudaEvent_t next() {
         if (used == pool->size()) {
@@ -352,73 +326,108 @@ struct Prof {
         return (*pool)[used++];
     }
     void begin(cudaStream_t st, int tag) {
-        if (tag >= 0) {
-            ++launches;
-            ++bin_launches[tag];
-        }
+        ++launches;
+        if (tag >= 0) ++slot_launches[tag];
         if (!on) return;
         tags.push_back(tag);
         cudaEventRecord(next(), st);
     }
-    void end(cudaStream_t st, int) {
+    void end(cudaStream_t st) {
         if (on) cudaEventRecord(next(), st);
     }
 };
 
 template <int WM, int TIE> struct Launcher {
-    static cudaError_t setup() {
+    using A = typename Acc<WM>::T;
+    static int occ_warp, occ_team, occ_hub, done_device;
+    static cudaError_t setup(int device) {
+        if (done_device == device) return cudaSuccess;
         cudaError_t e;
         e = cudaFuncSetAttribute(k_warp<WM, TIE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)warp_smem_bytes<typename Acc<WM>::T>());
+                                 (int)warp_smem_bytes<A>());
         if (e) return e;
-        e = cudaFuncSetAttribute(k_block<WM, TIE, kLargeBits, kLargeThreads, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)block_smem_bytes<typename Acc<WM>::T, kLargeBits>());
+        e = cudaFuncSetAttribute(k_team<WM, TIE, kTeamThreads, kTeamBits, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)team_smem_bytes<A, kTeamBits>());
         if (e) return e;
-        e = cudaFuncSetAttribute(k_block<WM, TIE, kHubBits, kHubThreads, true>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)block_smem_bytes<typename Acc<WM>::T, kHubBits>());
-        return e;
+        e = cudaFuncSetAttribute(k_team<WM, TIE, kHubThreads, kHubBits, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)team_smem_bytes<A, kHubBits>());
+        if (e) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_warp, k_warp<WM, TIE>, kWarpsPerBlock * 32,
+                                                          warp_smem_bytes<A>());
+        if (e) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_team, k_team<WM, TIE, kTeamThreads, kTeamBits, false>,
+                                                          kTeamThreads, team_smem_bytes<A, kTeamBits>());
+        if (e) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_hub, k_team<WM, TIE, kHubThreads, kHubBits, true>,
+                                                          kHubThreads, team_smem_bytes<A, kHubBits>());
+        if (e) return e;
+        occ_warp = std::max(occ_warp, 1);
+        occ_team = std::max(occ_team, 1);
+        occ_hub = std::max(occ_hub, 1);
+        done_device = device;
+        return cudaSuccess;
     }
-    // dense: lists == nullptr, slot ranges from the plan; frontier: per-bin lists
-    static void round(lp_graph* g, EvalArgs a, bool dense, int64_t* h_counts, Prof* prof) {
-        using A = typename Acc<WM>::T;
+    // One round.  dense: k_small sweeps the small slot range and the other
+    // slots are routed; frontier: everything comes from the marked route.
+    static void round(lp_graph* g, EvalArgs a, bool dense, const int32_t* h_len, Prof* prof) {
         const Plan& P = g->plan;
         const int sms = g->num_sms;
-        for (int b = 0; b < kNumBins; ++b) {
-            const int64_t cnt = dense ? (P.bin_beg[b + 1] - P.bin_beg[b]) : h_counts[b];
+        cudaStream_t st = g->stream;
+        if (dense && P.big_end > 0) {
+            prof->begin(st, -1);
+            k_route_dense<<<grid_for(P.big_end, 256, sms * 8), 256, 0, st>>>(a, 0, P.big_end);
+            prof->end(st);
+        }
+        // small rows, one launch per degree class (MAXD 16, 8, 4)
+        for (int c = 0; c < 3; ++c) {
+            const int bin = kBinS16 + c;
+            const int list = kLenS16 - c;
+            const int64_t cnt = dense ? (P.bin_beg[bin + 1] - P.bin_beg[bin]) : h_len[list];
             if (cnt <= 0) continue;
-            const int32_t* list = dense ? nullptr : g->lists + (int64_t)b * g->n;
-            const int32_t* len = dense ? nullptr : g->list_len + b;
-            const int32_t sb = P.bin_beg[b], se = P.bin_beg[b + 1];
-            a.bin = b;
-            prof->begin(g->stream, b);
-            switch (b) {
-                case kBinHub:
-                    k_block<WM, TIE, kHubBits, kHubThreads, true>
-                        <<<grid_for(cnt, 1, sms), kHubThreads, block_smem_bytes<A, kHubBits>(), g->stream>>>(a, list, len,
-                                                                                                       sb, se);
-                    break;
-                case kBinLarge:
-                    k_block<WM, TIE, kLargeBits, kLargeThreads, false>
-                        <<<grid_for(cnt, 1, sms * 3), kLargeThreads, block_smem_bytes<A, kLargeBits>(), g->stream>>>(
-                            a, list, len, sb, se);
-                    break;
-                case kBinMid:
-                    k_warp<WM, TIE><<<grid_for(cnt, kWarpsPerBlock, sms * 8), kWarpsPerBlock * 32,
-                                      warp_smem_bytes<A>(), g->stream>>>(a, list, len, sb, se);
-                    break;
-                default:
-                    k_small<WM, TIE><<<grid_for(cnt, 256, sms * 8), 256, 0, g->stream>>>(a, list, len, sb, se);
-                    break;
-            }
-            prof->end(g->stream, b);
+            const int32_t sb = dense ? P.bin_beg[bin] : -1, se = dense ? P.bin_beg[bin + 1] : -1;
+            a.bin = kKSmall;
+            prof->begin(st, kKSmall);
+            const int grid = grid_for(cnt, 256, sms * 8);
+            if (c == 0)
+                k_small<WM, TIE, 16><<<grid, 256, 0, st>>>(a, sb, se);
+            else if (c == 1)
+                k_small<WM, TIE, 8><<<grid, 256, 0, st>>>(a, sb, se);
+            else
+                k_small<WM, TIE, 4><<<grid, 256, 0, st>>>(a, sb, se);
+            prof->end(st);
+        }
+        if (dense ? P.big_end > 0 : h_len[kLenWarp] > 0) {
+            a.bin = kKWarp;
+            prof->begin(st, kKWarp);
+            const int grid = dense ? sms * occ_warp : grid_for(h_len[kLenWarp], kWarpsPerBlock, sms * occ_warp);
+            k_warp<WM, TIE><<<grid, kWarpsPerBlock * 32, warp_smem_bytes<A>(), st>>>(a);
+            prof->end(st);
+        }
+        // the warp kernel may spill into the team list
+        if (dense ? P.big_end > 0 : (h_len[kLenWarp] + h_len[kLenTeam]) > 0) {
+            a.bin = kKTeam;
+            prof->begin(st, kKTeam);
+            k_team<WM, TIE, kTeamThreads, kTeamBits, false>
+                <<<sms * occ_team, kTeamThreads, team_smem_bytes<A, kTeamBits>(), st>>>(a, kLenTeam);
+            prof->end(st);
+        }
+        if (dense ? P.big_end > 0 : h_len[kLenHub] > 0) {
+            a.bin = kKHub;
+            prof->begin(st, kKHub);
+            const int grid = dense ? sms * occ_hub : grid_for(h_len[kLenHub], 1, sms * occ_hub);
+            k_team<WM, TIE, kHubThreads, kHubBits, true>
+                <<<grid, kHubThreads, team_smem_bytes<A, kHubBits>(), st>>>(a, kLenHub);
+            prof->end(st);
         }
     }
 };
+template <int WM, int TIE> int Launcher<WM, TIE>::occ_warp = 1;
+template <int WM, int TIE> int Launcher<WM, TIE>::occ_team = 1;
+template <int WM, int TIE> int Launcher<WM, TIE>::occ_hub = 1;
+template <int WM, int TIE> int Launcher<WM, TIE>::done_device = -1;
 
-typedef void (*round_fn)(lp_graph*, EvalArgs, bool, int64_t*, Prof*);
-typedef cudaError_t (*setup_fn)();
+typedef void (*round_fn)(lp_graph*, EvalArgs, bool, const int32_t*, Prof*);
+typedef cudaError_t (*setup_fn)(int);
 
 template <int WM> static void pick_fns(int tie, round_fn* r, setup_fn* s) {
     switch (tie) {
@@ -451,21 +460,35 @@ static void free_plan(Plan& P) {
     P = Plan();
 }
 
+static void free_routes(Routes& r) {
+    for (int c = 0; c < 3; ++c) cudaFree(r.small[c]);
+    cudaFree(r.warp);
+    cudaFree(r.team);
+    cudaFree(r.hub);
+    cudaFree(r.len);
+    cudaFree(r.cand);
+    cudaFree(r.cand_done);
+    cudaFree(r.gkeys);
+    cudaFree(r.gfirst);
+    cudaFree(r.gacc);
+    cudaFree(r.gcount);
+    r = Routes();
+}
+
 static void destroy_graph(lp_graph* g) {
     if (!g) return;
     free_plan(g->plan);
+    free_routes(g->routes);
     cudaFree(g->off);
     cudaFree(g->nbr);
     cudaFree(g->w);
     cudaFree(g->labA);
     cudaFree(g->labB);
     cudaFree(g->mark);
-    cudaFree(g->lists);
-    cudaFree(g->list_len);
     cudaFree(g->counters);
     cudaFree(g->out64);
     cudaFree(g->cub_tmp);
-    if (g->h_list_len) cudaFreeHost(g->h_list_len);
+    if (g->h_len) cudaFreeHost(g->h_len);
     if (g->h_counters) cudaFreeHost(g->h_counters);
     for (cudaEvent_t e : g->event_pool) cudaEventDestroy(e);
     if (g->ev0) cudaEventDestroy(g->ev0);
@@ -493,14 +516,30 @@ static uint64_t hash_order(const int64_t* order, int64_t n) {
     return h;
 }
 
+struct TmpBufs {
+    int64_t* order = nullptr;
+    unsigned long long* key = nullptr;
+    unsigned long long* key_sorted = nullptr;
+    int32_t* iota = nullptr;
+    uint32_t* sdeg = nullptr;
+    ~TmpBufs() {
+        cudaFree(order);
+        cudaFree(key);
+        cudaFree(key_sorted);
+        cudaFree(iota);
+        cudaFree(sdeg);
+    }
+};
+
 // Build (or reuse) the position / storage plan for a visit order.
 static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, float* plan_ms) {
     const int64_t n = g->n;
-    bool custom = order_host != nullptr;
-    uint64_t oh = custom ? hash_order(order_host, n) : 0;
+    const bool custom = order_host != nullptr;
+    const uint64_t oh = custom ? hash_order(order_host, n) : 0;
     Plan& P = g->plan;
     *plan_ms = 0.f;
     if (P.valid && P.custom_order == custom && (custom ? P.order_hash == oh : P.seed == seed)) return LP_OK;
+    g->bytes -= P.bytes;
     free_plan(P);
     std::vector<int64_t> own;
     if (!custom) {
@@ -516,55 +555,47 @@ static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, flo
     LP_CK(dalloc(&P.spos, n, &bytes));
     LP_CK(dalloc(&P.slot_of_pos, n, &bytes));
     LP_CK(dalloc(&P.ndist, n, &bytes));
-    int64_t* d_order = nullptr;
-    uint8_t* d_bin = nullptr;
-    uint8_t* d_bin_sorted = nullptr;
-    int32_t* d_iota = nullptr;
-    uint32_t* d_sdeg = nullptr;
+    TmpBufs t;
     int64_t tmpb = 0;
-    LP_CK(dalloc(&d_order, n, &tmpb));
-    LP_CK(dalloc(&d_bin, n, &tmpb));
-    LP_CK(dalloc(&d_bin_sorted, n, &tmpb));
-    LP_CK(dalloc(&d_iota, n, &tmpb));
-    LP_CK(dalloc(&d_sdeg, n + 1, &tmpb));
-    LP_CK(cudaMemcpyAsync(d_order, order_host, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    LP_CK(dalloc(&t.order, n, &tmpb));
+    LP_CK(dalloc(&t.key, n, &tmpb));
+    LP_CK(dalloc(&t.key_sorted, n, &tmpb));
+    LP_CK(dalloc(&t.iota, n, &tmpb));
+    LP_CK(dalloc(&t.sdeg, n + 1, &tmpb));
+    LP_CK(cudaMemcpyAsync(t.order, order_host, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     LP_CK(cudaMemsetAsync(g->counters, 0, 8 * sizeof(unsigned long long), st));
-    const int G = g->num_sms * 8;
     LP_CK(cudaMemsetAsync(P.pos, 0xff, n * sizeof(int32_t), st));
-    k_plan_pos<<<G, 256, 0, st>>>(d_order, P.vid, P.pos, n, g->counters);
+    const int G = g->num_sms * 8;
+    k_plan_pos<<<G, 256, 0, st>>>(t.order, P.vid, P.pos, n, g->counters);
     k_plan_check_perm<<<G, 256, 0, st>>>(P.vid, P.pos, n, g->counters);
     LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     LP_CK(cudaStreamSynchronize(st));
     if (g->h_counters[0]) {  // checked before any kernel dereferences vid[]
-        cudaFree(d_order);
-        cudaFree(d_bin);
-        cudaFree(d_bin_sorted);
-        cudaFree(d_iota);
-        cudaFree(d_sdeg);
         free_plan(P);
-        lp_set_error("order is not a permutation of range(n)");
-        return LP_ERR_INVALID;
+        return lp_fail(LP_ERR_INVALID, "order is not a permutation of range(n)");
     }
-    k_plan_bins<<<G, 256, 0, st>>>(P.vid, g->off, g->nbr, d_bin, n, g->counters + 1);
-    k_iota<<<G, 256, 0, st>>>(d_iota, n);
-    size_t need = 0;
-    LP_CK(cub::DeviceRadixSort::SortPairs(nullptr, need, d_bin, d_bin_sorted, d_iota, P.spos, (int)n, 0, 3, st));
-    size_t need2 = 0;
-    LP_CK(cub::DeviceScan::ExclusiveSum(nullptr, need2, d_sdeg, d_sdeg, (int)(n + 1), st));
+    k_plan_keys<<<G, 256, 0, st>>>(P.vid, g->off, g->nbr, t.key, n, g->counters + 1);
+    k_iota<<<G, 256, 0, st>>>(t.iota, n);
+    size_t need = 0, need2 = 0;
+    LP_CK(cub::DeviceRadixSort::SortPairs(nullptr, need, t.key, t.key_sorted, t.iota, P.spos, (int)n, 0, 35, st));
+    LP_CK(cub::DeviceScan::ExclusiveSum(nullptr, need2, t.sdeg, t.sdeg, (int)(n + 1), st));
     if (int rc = ensure_cub_tmp(g, std::max(need, need2))) return rc;
-    LP_CK(cub::DeviceRadixSort::SortPairs(g->cub_tmp, need, d_bin, d_bin_sorted, d_iota, P.spos, (int)n, 0, 3, st));
+    LP_CK(cub::DeviceRadixSort::SortPairs(g->cub_tmp, need, t.key, t.key_sorted, t.iota, P.spos, (int)n, 0, 35, st));
     LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     LP_CK(cudaStreamSynchronize(st));
-    int64_t acc = 0;
-    for (int b = 0; b < kNumBins; ++b) {
-        P.bin_beg[b] = (int32_t)acc;
-        acc += (int64_t)g->h_counters[1 + b];
+    {
+        int64_t acc = 0;
+        for (int b = 0; b < kNumBins; ++b) {
+            P.bin_beg[b] = (int32_t)acc;
+            acc += (int64_t)g->h_counters[1 + b];
+        }
+        P.bin_beg[kNumBins] = (int32_t)acc;
     }
-    P.bin_beg[kNumBins] = (int32_t)acc;
-    P.S = acc;
-    k_plan_slots<<<G, 256, 0, st>>>(P.spos, P.vid, g->off, P.slot_of_pos, d_sdeg, P.ndist, n, P.S);
+    P.big_end = P.bin_beg[kBinS16];
+    P.S = P.bin_beg[kBinIdle];
+    k_plan_slots<<<G, 256, 0, st>>>(P.spos, P.vid, g->off, P.slot_of_pos, t.sdeg, n, P.S);
     LP_CK(dalloc(&P.soff, P.S + 1, &bytes));
-    LP_CK(cub::DeviceScan::ExclusiveSum(g->cub_tmp, need2, d_sdeg, P.soff, (int)(P.S + 1), st));
+    LP_CK(cub::DeviceScan::ExclusiveSum(g->cub_tmp, need2, t.sdeg, P.soff, (int)(P.S + 1), st));
     uint32_t m_active = 0;
     LP_CK(cudaMemcpyAsync(&m_active, P.soff + P.S, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     LP_CK(cudaStreamSynchronize(st));
@@ -577,17 +608,38 @@ static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, flo
     LP_CK(cudaEventRecord(g->ev1, st));
     LP_CK(cudaEventSynchronize(g->ev1));
     LP_CK(cudaEventElapsedTime(plan_ms, g->ev0, g->ev1));
-    cudaFree(d_order);
-    cudaFree(d_bin);
-    cudaFree(d_bin_sorted);
-    cudaFree(d_iota);
-    cudaFree(d_sdeg);
     P.valid = true;
     P.custom_order = custom;
     P.seed = seed;
     P.order_hash = oh;
+    P.bytes = bytes;
     g->bytes += bytes;
     return LP_OK;
+}
+
+static cudaError_t alloc_routes(lp_graph* g) {
+    Routes& r = g->routes;
+    const int64_t n = std::max<int64_t>(g->n, 1);
+    // hub items: one per partition (<= est / kHubPlan + 1) or per slice
+    g->cap_items = n + g->m / (kHubPlan / 2) + g->m / kSliceArcs + 1024;
+    const int64_t gpool = std::max<int64_t>(g->sliceable, 1) << kGlobalBits;
+    cudaError_t e;
+    for (int c = 0; c < 3; ++c)
+        if ((e = dalloc(&r.small[c], n, &g->bytes))) return e;
+    if ((e = dalloc(&r.warp, n, &g->bytes))) return e;
+    if ((e = dalloc(&r.team, 2 * n, &g->bytes))) return e;
+    if ((e = dalloc(&r.hub, g->cap_items, &g->bytes))) return e;
+    if ((e = dalloc(&r.len, kLenCount, &g->bytes))) return e;
+    if ((e = dalloc(&r.cand, g->cap_items, &g->bytes))) return e;
+    if ((e = dalloc(&r.cand_done, g->cap_items, &g->bytes))) return e;
+    if ((e = dalloc(&r.gcount, g->cap_items, &g->bytes))) return e;
+    if ((e = dalloc(&r.gkeys, gpool, &g->bytes))) return e;
+    if ((e = dalloc(&r.gfirst, gpool, &g->bytes))) return e;
+    if ((e = dalloc(&r.gacc, gpool, &g->bytes))) return e;
+    if ((e = cudaMemsetAsync(r.cand_done, 0, g->cap_items * sizeof(int32_t), g->stream))) return e;
+    if ((e = cudaMemsetAsync(r.gcount, 0, g->cap_items * sizeof(int32_t), g->stream))) return e;
+    k_gtab_init<<<g->num_sms * 4, 256, 0, g->stream>>>(r.gkeys, r.gfirst, r.gacc, gpool);
+    return cudaGetLastError();
 }
 
 extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, const int64_t* neighbors,
@@ -596,7 +648,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     *out = nullptr;
     if (n < 0 || m < 0) return lp_fail(LP_ERR_INVALID, "negative vertex or edge count");
     if (n >= (int64_t)INT32_MAX) return lp_fail(LP_ERR_UNSUPPORTED, "vertex count must be < 2^31-1");
-    if (m >= (int64_t)UINT32_MAX) return lp_fail(LP_ERR_UNSUPPORTED, "edge count must be < 2^32-1");
+    if (m >= (int64_t)INT32_MAX) return lp_fail(LP_ERR_UNSUPPORTED, "edge count must be < 2^31-1");
     if (n > 0 && !offsets) return lp_fail(LP_ERR_INVALID, "offsets is NULL");
     if (m > 0 && !neighbors) return lp_fail(LP_ERR_INVALID, "neighbors is NULL");
     if (n > 0 && (offsets[0] != 0 || offsets[n] != m))
@@ -608,7 +660,6 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
         return lp_fail(LP_ERR_CUDA, "no CUDA device available (liblabelprop_cuda needs a B200)");
     if (device >= 0) LP_CK(cudaSetDevice(device));
     lp_graph* g = new lp_graph();
-    int rc = LP_OK;
     auto fail = [&](int code) {
         destroy_graph(g);
         return code;
@@ -633,11 +684,9 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     G_CK(dalloc(&g->labA, n, &g->bytes));
     G_CK(dalloc(&g->labB, n, &g->bytes));
     G_CK(dalloc(&g->mark, n + 4, &g->bytes));
-    G_CK(dalloc(&g->lists, (size_t)kNumBins * std::max<int64_t>(n, 1), &g->bytes));
-    G_CK(dalloc(&g->list_len, kNumBins, &g->bytes));
     G_CK(dalloc(&g->counters, 32, &g->bytes));
     G_CK(dalloc(&g->out64, n, &g->bytes));
-    G_CK(cudaMallocHost((void**)&g->h_list_len, kNumBins * sizeof(int32_t)));
+    G_CK(cudaMallocHost((void**)&g->h_len, kLenCount * sizeof(int32_t)));
     G_CK(cudaMallocHost((void**)&g->h_counters, 32 * sizeof(unsigned long long)));
     G_CK(cudaMemsetAsync(g->mark, 0, n + 4, st));
     G_CK(cudaMemsetAsync(g->counters, 0, 32 * sizeof(unsigned long long), st));
@@ -657,7 +706,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
             G_CK(cudaMemcpyAsync(g->counters + 4, init, sizeof(init), cudaMemcpyHostToDevice, st));
             k_weight_scan<<<g->num_sms * 8, 256, 0, st>>>((const double*)tmp, m, g->counters + 4);
         }
-        k_degree_max<<<g->num_sms * 8, 256, 0, st>>>(g->off, n, g->counters + 8);
+        k_degree_stats<<<g->num_sms * 8, 256, 0, st>>>(g->off, n, g->counters + 8);
         G_CK(cudaMemcpyAsync(g->h_counters, g->counters, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         G_CK(cudaStreamSynchronize(st));
         if (g->h_counters[0]) {
@@ -665,6 +714,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
             return fail(lp_fail(LP_ERR_INVALID, "neighbor ids must lie in [0, vertex_count)"));
         }
         g->max_degree = (int64_t)g->h_counters[8];
+        g->sliceable = (int64_t)g->h_counters[9];
         g->wmode = kUnit;
         if (weights && m > 0 && g->h_counters[4 + 0] != 0) {
             const unsigned long long bad = g->h_counters[4 + 1];
@@ -685,9 +735,10 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
         G_CK(cudaStreamSynchronize(st));
         cudaFree(tmp);
     }
+    G_CK(alloc_routes(g));
+    G_CK(cudaStreamSynchronize(st));
     G_CK(cudaGetLastError());
     *out = g;
-    (void)rc;
     return LP_OK;
 #undef G_CK
 }
@@ -747,7 +798,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         pick_fns<kFloat>(o->tie, &run_round, &setup);
     else
         pick_fns<kUnit>(o->tie, &run_round, &setup);
-    LP_CK(setup());
+    LP_CK(setup(g->device));
 
     const int64_t B = (o->batches == 0 || o->batches > n) ? n : o->batches;
     const int64_t bs = (n + B - 1) / B;
@@ -765,6 +816,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     } else {
         k_init_labels<<<g->num_sms * 8, 256, 0, st>>>(P.vid, nullptr, g->labA, n);
     }
+    if (P.S > 0) k_reset_ndist<<<g->num_sms * 8, 256, 0, st>>>(P.soff, P.ndist, P.S);
     LP_CK(cudaGetLastError());
 
     int32_t* L0 = g->labA;
@@ -778,10 +830,10 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.mark = cross ? g->mark : nullptr;
     a.ndist = P.ndist;
     a.counters = g->counters;
+    a.r = g->routes;
     a.bs = (int32_t)bs;
+    a.bin = 0;
     a.seed = o->seed;
-    BinBounds bins_only;
-    memcpy(bins_only.beg, P.bin_beg, sizeof(P.bin_beg));
 
     LP_CK(cudaMemsetAsync(g->counters, 0, kCtrCount * sizeof(unsigned long long), st));
     Prof prof;
@@ -790,28 +842,28 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     LP_CK(cudaEventRecord(g->ev0, st));
     int it = 0;
     int rounds = 0;
-    int64_t h_counts[kNumBins];
     while (it < o->max_iterations) {
         ++it;
         a.sweep = (uint32_t)it;
         a.L0 = L0;
         a.x = X;
         LP_CK(cudaMemcpyAsync(X, L0, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
-        LP_CK(cudaMemsetAsync(g->counters + kCtrChanged, 0, 3 * sizeof(unsigned long long), st));
-        run_round(g, a, true, h_counts, &prof);
+        LP_CK(cudaMemsetAsync(g->counters + kCtrChanged, 0, 2 * sizeof(unsigned long long), st));
+        LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
+        run_round(g, a, true, g->h_len, &prof);
         ++rounds;
         while (cross) {
-            LP_CK(cudaMemsetAsync(g->list_len, 0, kNumBins * sizeof(int32_t), st));
+            LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
             prof.begin(st, -1);
-            k_compact<<<g->num_sms * 8, 256, 0, st>>>(g->mark, P.slot_of_pos, n, bins_only, g->lists, g->list_len, n);
-            prof.end(st, -1);
-            LP_CK(cudaMemcpyAsync(g->h_list_len, g->list_len, kNumBins * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            k_route_marked<<<g->num_sms * 8, 256, 0, st>>>(a, g->mark, P.slot_of_pos, n);
+            prof.end(st);
+            LP_CK(cudaMemcpyAsync(g->h_len, g->routes.len, kLenCount * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
             LP_CK(cudaStreamSynchronize(st));
-            int64_t total = 0;
-            for (int b = 0; b < kNumBins; ++b) total += (h_counts[b] = g->h_list_len[b]);
+            const int64_t total = (int64_t)g->h_len[kLenS4] + g->h_len[kLenS8] + g->h_len[kLenS16] +
+                                  g->h_len[kLenWarp] + g->h_len[kLenTeam] + g->h_len[kLenHub];
             if (total == 0) break;
-            LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, 2 * sizeof(unsigned long long), st));
-            run_round(g, a, false, h_counts, &prof);
+            LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
+            run_round(g, a, false, g->h_len, &prof);
             ++rounds;
         }
         LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, kCtrCount * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -834,10 +886,10 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     S->kernel_ms = ms;
     S->arcs_dense = g->m * it;
     S->launches = prof.launches;
-    for (int b = 0; b < kNumBins; ++b) {
+    for (int b = 0; b < kKSlots; ++b) {
         S->bin_arcs[b] = (int64_t)g->h_counters[kCtrArcs + b];
         S->bin_vertices[b] = (int64_t)g->h_counters[kCtrVerts + b];
-        S->bin_launches[b] = prof.bin_launches[b];
+        S->bin_launches[b] = prof.slot_launches[b];
         S->arcs_scanned += S->bin_arcs[b];
     }
     for (size_t i = 0; i < prof.tags.size(); ++i) {
