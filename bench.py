@@ -142,6 +142,25 @@ def dist_setup():
     return world, rank, local
 
 
+def reduce_max(x: float, world: int, device=None) -> float:
+    """Max of a per-rank scalar over all ranks (device-timed values are
+    combined this way: the job is as slow as its slowest rank)."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_gteps(arcs_per_rank: int, ms_max: float, world: int) -> float:
+    """Replicas: every rank processes `arcs_per_rank` arcs; whole-job GTEPS
+    is all ranks' arcs over the max-over-ranks time."""
+    return world * arcs_per_rank / (ms_max / 1e3) / 1e9
+
+
 def run_reference(args, world, rank):
     """CPU arm: OpenMP port of the reference's _rak_par on all host cores."""
     if rank != 0:
@@ -221,13 +240,9 @@ def run_ours(args, world, rank, local):
             per.append(st.as_dict())
         ev1.record(stream)
         torch.cuda.synchronize()
-    dt_ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([dt_ms], device=f"cuda:{local}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        dt_ms = float(t.item())
+    dt_ms = reduce_max(ev0.elapsed_time(ev1), world, device=f"cuda:{local}")
     arcs_dense = sum(p["arcs_dense"] for p in per)
-    value = world * arcs_dense / (dt_ms / 1e3) / 1e9
+    value = whole_job_gteps(arcs_dense, dt_ms, world)
 
     # roofline of the dominant kernel (per-launch averages over the timed region)
     bins = _lib.BIN_NAMES
@@ -333,15 +348,11 @@ def e2e(args, g, params, world, local):
             labels, it, st, _ = lp.rak_labels(fresh, params, device_graph=dg)
             dg.close()
             arcs += g.edge_count * it
-        dt = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([dt], device=f"cuda:{local}")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            dt = float(t.item())
+        dt = reduce_max(time.perf_counter() - t0, world, device=f"cuda:{local}")
     finally:
         for a in arrays:
             L.lp_host_unregister(_lib.ptr(a))
-    return {"value": world * arcs / dt / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+    return {"value": whole_job_gteps(arcs, dt * 1e3, world), "unit": "GTEPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": dt / steps * 1e3, "steps": steps,
             "what": "rak_labels() on a freshly uploaded graph each step: CSR H2D from pinned host memory "
                     "(int64 offsets/neighbours as the reference's Graph holds them), plan build, sweeps, "

@@ -1,0 +1,113 @@
+"""Host-side API contract (no GPU): parameter records and helpers keep the
+reference's semantics (tests/test_rak.py:92-125, test_quality.py, test_graph.py)."""
+
+import numpy as np
+import pytest
+
+import paper_2301_09125_b200 as lp
+from paper_2301_09125_b200 import graph as G
+
+
+class TestRakParams:
+    def test_reference_defaults(self):
+        p = lp.RakParams()
+        assert (p.tolerance, p.strict, p.max_iterations, p.workers, p.seed) == (0.05, False, 100, 1, 1)
+        assert p.batches == 0 and p.tie_rule == "random"
+        assert lp.RakParams(strict=True).tie_rule == "scan-first"
+
+    def test_validation(self):
+        for bad in (dict(tolerance=0.0), dict(tolerance=1.5), dict(max_iterations=0), dict(workers=0),
+                    dict(batches=-1), dict(tie="first"), dict(backend="cpu")):
+            with pytest.raises(ValueError):
+                lp.RakParams(**bad)
+
+
+class TestChooseMaxLabel:
+    """Known answers of the reference (tests/test_rak.py:92-113)."""
+
+    def test_unique_max(self):
+        assert lp.choose_max_label([5, 9], [2.0, 1.0], True, lp.XorShift32(1)) == 5
+        assert lp.choose_max_label([5, 9], [2.0, 1.0], False, lp.XorShift32(1)) == 5
+
+    def test_strict_first_in_scan_order(self):
+        assert lp.choose_max_label([3, 7], [2.0, 2.0], True, lp.XorShift32(1)) == 3
+        assert lp.choose_max_label([7, 3], [2.0, 2.0], True, lp.XorShift32(1)) == 7
+
+    def test_non_strict_fair(self):
+        rng = lp.XorShift32(42)
+        picks = sum(lp.choose_max_label([3, 7], [2.0, 2.0], False, rng) == 3 for _ in range(10_000))
+        assert abs(picks / 10_000 - 0.5) <= 0.02
+
+    def test_duplicates_accumulate(self):
+        assert lp.choose_max_label([4, 9, 4], [1.0, 1.5, 1.0], True, lp.XorShift32(1)) == 4
+
+    def test_empty_rejected(self):
+        with pytest.raises(ValueError):
+            lp.choose_max_label([], [], True, lp.XorShift32(1))
+
+
+class TestGraph:
+    def test_from_arcs_merges_duplicates(self):
+        g = G.from_arcs(3, [0, 0, 1], [1, 1, 2], [1.0, 2.0, 4.0])
+        assert g.edge_count == 2 and g.weights.tolist() == [3.0, 4.0]
+
+    def test_preprocess_idempotent_and_symmetric(self):
+        raw = G.from_arcs(5, [0, 1, 2, 3, 3], [1, 2, 0, 4, 3], [2.0, 3.0, 1.0, 5.0, 7.0])
+        g = G.preprocess(raw, unit_weights=False)
+        G.check_symmetric(g)
+        assert G.graphs_equal(g, G.preprocess(g, unit_weights=False))
+        assert (np.diff(g.offsets) >= 1).all()
+
+    def test_asymmetric_rejected(self):
+        with pytest.raises(ValueError, match="symmetric"):
+            G.check_symmetric(G.from_arcs(2, [0], [1], [1.0]))
+
+    def test_degree_weights_count_loops_twice(self):
+        g = lp.disjoint_cliques(1, 3)
+        assert G.degree_weights(g).tolist() == [4.0, 4.0, 4.0]
+        assert G.degree_weight(g, 0) == 4.0
+
+
+class TestModularity:
+    """Same scorer as the reference (quality.py); brute force check as in
+    tests/test_quality.py:41-50."""
+
+    def test_matches_brute_force(self):
+        rng = np.random.default_rng(11)
+        for trial in range(30):
+            n = int(rng.integers(2, 60))
+            g = lp.gnp(n, (0.05, 0.2, 0.5)[trial % 3], seed=int(rng.integers(1, 1 << 31)))
+            lab = rng.integers(0, n, size=n)
+            assert lp.modularity(g, lab) == pytest.approx(lp.brute_modularity(g, lab), abs=1e-9)
+
+    def test_one_community_zero_and_two_triangles_half(self):
+        g = lp.preprocess(lp.from_arcs(6, [0, 0, 1, 3, 3, 4], [1, 2, 2, 4, 5, 5], np.ones(6)), self_loops=False)
+        assert lp.modularity(g, np.zeros(6, np.int64)) == pytest.approx(0.0, abs=1e-12)
+        assert lp.modularity(g, np.array([0, 0, 0, 1, 1, 1])) == pytest.approx(0.5, abs=1e-12)
+
+    def test_contract(self):
+        g = lp.disjoint_cliques(2, 3)
+        with pytest.raises(ValueError):
+            lp.modularity(g, np.zeros(5, np.int64))
+        with pytest.raises(ValueError):
+            lp.modularity(g, np.full(6, 17))
+
+    def test_oracle_scorer_agrees(self, oracle):
+        g = lp.rmat(11, seed=3)
+        lab = np.random.default_rng(0).integers(0, g.vertex_count, g.vertex_count)
+        assert oracle.modularity(g, lab) == pytest.approx(lp.modularity(g, lab), abs=1e-12)
+
+
+def test_empty_graph_needs_no_gpu():
+    res = lp.rak_detect(lp.preprocess(lp.from_arcs(0, [], [], [])))
+    assert res.iterations == 0 and res.assignment.size == 0
+
+
+def test_reference_test_graphs_match_reference_fixtures(golden_rak):
+    """Our ports of the reference's test generators rebuild the stored CSRs."""
+    from conftest import load_graph
+
+    for name, mk in (("cliques_8x6", lambda: lp.disjoint_cliques(8, 6)), ("ring_16x6", lambda: lp.ring_of_cliques(16, 6)),
+                     ("gnp_400", lambda: lp.gnp(400, 0.02, seed=2)), ("gnp_3000", lambda: lp.gnp(3000, 0.005, seed=6)),
+                     ("star_50", lambda: lp.star(50)), ("path_100", lambda: lp.path(100))):
+        assert G.graphs_equal(mk(), load_graph(golden_rak, name)), name
