@@ -140,6 +140,12 @@ int lp_rak_run(lp_graph* g, const lp_rak_opts* opts, const int64_t* order, const
 int lp_rak_run_resident(lp_graph* g, const lp_rak_opts* opts, const int64_t* order, lp_run_stats* stats);
 int lp_labels_download(lp_graph* g, int64_t* labels_out);
 
+/* Calibration (device time per pass, ms): mode 0 streams the neighbour
+ * indices of the active rows once; mode 1 also gathers every neighbour's
+ * label (the sweep's memory traffic without the tally).  Needs a plan
+ * (run a detection first). */
+int lp_calibrate(lp_graph* g, int32_t mode, int32_t reps, double* ms_out);
+
 /* Host utilities (no GPU needed).  lp_shuffled_indices reproduces the
  * reference's prng.shuffled_indices (prng.py:82-94) byte for byte. */
 int lp_shuffled_indices(int64_t n, uint32_t seed, int64_t* out);

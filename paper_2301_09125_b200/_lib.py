@@ -101,6 +101,7 @@ EXPORTS = (
     "lp_rak_run",
     "lp_rak_run_resident",
     "lp_labels_download",
+    "lp_calibrate",
     "lp_shuffled_indices",
     "lp_gen_rmat",
     "lp_csr_build_undirected",
@@ -143,6 +144,7 @@ def lib():
     L.lp_rak_run.argtypes = [vp, C.POINTER(RakOpts), vp, vp, vp, vp, C.POINTER(RunStats)]
     L.lp_rak_run_resident.argtypes = [vp, C.POINTER(RakOpts), vp, C.POINTER(RunStats)]
     L.lp_labels_download.argtypes = [vp, vp]
+    L.lp_calibrate.argtypes = [vp, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
     L.lp_shuffled_indices.argtypes = [C.c_int64, C.c_uint32, _i64p]
     L.lp_gen_rmat.argtypes = [C.c_int32, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_uint64, _i64p, _i64p]
     L.lp_csr_build_undirected.argtypes = [C.c_int64, C.c_int64, _i64p, _i64p, _i64p, _i64p, C.POINTER(C.c_int64)]

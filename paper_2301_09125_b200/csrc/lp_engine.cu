@@ -73,6 +73,7 @@ struct Plan {
     uint32_t* soff = nullptr;        // [S+1]
     int32_t* snbr = nullptr;         // [m_active]
     uint32_t* sw = nullptr;          // [m_active] or null
+    unsigned long long* swsum = nullptr;  // [S] row weight totals (fixed-point mode)
     int32_t* ndist = nullptr;        // [S]
     int64_t S = 0;
     int64_t m_active = 0;
@@ -273,6 +274,19 @@ __global__ void k_plan_rows(const int32_t* __restrict__ spos, const int32_t* __r
     }
 }
 
+// per-slot total of the fixed-point row weights (majority test)
+__global__ void k_plan_wsum(const uint32_t* __restrict__ soff, const uint32_t* __restrict__ sw,
+                            unsigned long long* __restrict__ swsum, int64_t S) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
+    for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < S; s += warps) {
+        unsigned long long acc = 0;
+        for (uint32_t e = soff[s] + lane; e < soff[s + 1]; e += 32) acc += sw[e];
+        for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) swsum[s] = acc;
+    }
+}
+
 __global__ void k_init_labels(const int32_t* __restrict__ vid, const int64_t* __restrict__ init, int32_t* __restrict__ lab,
                               int64_t n) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
@@ -339,33 +353,46 @@ struct Prof {
 
 template <int WM, int TIE> struct Launcher {
     using A = typename Acc<WM>::T;
-    static int occ_warp, occ_team, occ_hub, done_device;
+    static int occ_warp[2], occ_team, occ_hub, done_device;
+    template <int WC> static cudaError_t setup_warp() {
+        cudaError_t e = cudaFuncSetAttribute(k_warp<WM, TIE, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)warp_smem_bytes<WM, WC>());
+        if (e) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_warp[WC], k_warp<WM, TIE, WC>,
+                                                          WarpClass<WC>::kWarps * 32, warp_smem_bytes<WM, WC>());
+        occ_warp[WC] = std::max(occ_warp[WC], 1);
+        return e;
+    }
     static cudaError_t setup(int device) {
         if (done_device == device) return cudaSuccess;
         cudaError_t e;
-        e = cudaFuncSetAttribute(k_warp<WM, TIE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)warp_smem_bytes<A>());
-        if (e) return e;
+        if ((e = setup_warp<0>())) return e;
+        if ((e = setup_warp<1>())) return e;
         e = cudaFuncSetAttribute(k_team<WM, TIE, kTeamThreads, kTeamBits, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)team_smem_bytes<A, kTeamBits>());
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)team_smem_bytes<WM, kTeamBits>());
         if (e) return e;
         e = cudaFuncSetAttribute(k_team<WM, TIE, kHubThreads, kHubBits, true>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)team_smem_bytes<A, kHubBits>());
-        if (e) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_warp, k_warp<WM, TIE>, kWarpsPerBlock * 32,
-                                                          warp_smem_bytes<A>());
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)team_smem_bytes<WM, kHubBits>());
         if (e) return e;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_team, k_team<WM, TIE, kTeamThreads, kTeamBits, false>,
-                                                          kTeamThreads, team_smem_bytes<A, kTeamBits>());
+                                                          kTeamThreads, team_smem_bytes<WM, kTeamBits>());
         if (e) return e;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_hub, k_team<WM, TIE, kHubThreads, kHubBits, true>,
-                                                          kHubThreads, team_smem_bytes<A, kHubBits>());
+                                                          kHubThreads, team_smem_bytes<WM, kHubBits>());
         if (e) return e;
-        occ_warp = std::max(occ_warp, 1);
         occ_team = std::max(occ_team, 1);
         occ_hub = std::max(occ_hub, 1);
         done_device = device;
         return cudaSuccess;
+    }
+    template <int WC> static void launch_warp(lp_graph* g, EvalArgs a, int64_t cnt, bool dense, Prof* prof) {
+        const int sms = g->num_sms;
+        a.bin = kKWarp;
+        prof->begin(g->stream, kKWarp);
+        const int per_block = 32 * WarpClass<WC>::kWarps;
+        const int grid = dense ? sms * occ_warp[WC] : grid_for(cnt, per_block, sms * occ_warp[WC]);
+        k_warp<WM, TIE, WC><<<grid, WarpClass<WC>::kWarps * 32, warp_smem_bytes<WM, WC>(), g->stream>>>(a);
+        prof->end(g->stream);
     }
     // One round.  dense: k_small sweeps the small slot range and the other
     // slots are routed; frontier: everything comes from the marked route.
@@ -396,32 +423,29 @@ template <int WM, int TIE> struct Launcher {
                 k_small<WM, TIE, 4><<<grid, 256, 0, st>>>(a, sb, se);
             prof->end(st);
         }
-        if (dense ? P.big_end > 0 : h_len[kLenWarp] > 0) {
-            a.bin = kKWarp;
-            prof->begin(st, kKWarp);
-            const int grid = dense ? sms * occ_warp : grid_for(h_len[kLenWarp], kWarpsPerBlock, sms * occ_warp);
-            k_warp<WM, TIE><<<grid, kWarpsPerBlock * 32, warp_smem_bytes<A>(), st>>>(a);
-            prof->end(st);
-        }
-        // the warp kernel may spill into the team list
-        if (dense ? P.big_end > 0 : (h_len[kLenWarp] + h_len[kLenTeam]) > 0) {
+        const bool big = dense && P.big_end > 0;
+        if (big || h_len[kLenWarp] > 0) launch_warp<0>(g, a, h_len[kLenWarp], dense, prof);
+        // each class may spill into the next one: launch on any upstream work
+        if (big || h_len[kLenWarp] + h_len[kLenWarpBig] > 0)
+            launch_warp<1>(g, a, h_len[kLenWarp] + h_len[kLenWarpBig], dense, prof);
+        if (big || (h_len[kLenWarp] + h_len[kLenWarpBig] + h_len[kLenTeam]) > 0) {
             a.bin = kKTeam;
             prof->begin(st, kKTeam);
             k_team<WM, TIE, kTeamThreads, kTeamBits, false>
-                <<<sms * occ_team, kTeamThreads, team_smem_bytes<A, kTeamBits>(), st>>>(a, kLenTeam);
+                <<<sms * occ_team, kTeamThreads, team_smem_bytes<WM, kTeamBits>(), st>>>(a, kLenTeam);
             prof->end(st);
         }
-        if (dense ? P.big_end > 0 : h_len[kLenHub] > 0) {
+        if (big || h_len[kLenHub] > 0) {
             a.bin = kKHub;
             prof->begin(st, kKHub);
             const int grid = dense ? sms * occ_hub : grid_for(h_len[kLenHub], 1, sms * occ_hub);
             k_team<WM, TIE, kHubThreads, kHubBits, true>
-                <<<grid, kHubThreads, team_smem_bytes<A, kHubBits>(), st>>>(a, kLenHub);
+                <<<grid, kHubThreads, team_smem_bytes<WM, kHubBits>(), st>>>(a, kLenHub);
             prof->end(st);
         }
     }
 };
-template <int WM, int TIE> int Launcher<WM, TIE>::occ_warp = 1;
+template <int WM, int TIE> int Launcher<WM, TIE>::occ_warp[2] = {1, 1};
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_team = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_hub = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::done_device = -1;
@@ -456,13 +480,15 @@ static void free_plan(Plan& P) {
     cudaFree(P.soff);
     cudaFree(P.snbr);
     cudaFree(P.sw);
+    cudaFree(P.swsum);
     cudaFree(P.ndist);
     P = Plan();
 }
 
 static void free_routes(Routes& r) {
     for (int c = 0; c < 3; ++c) cudaFree(r.small[c]);
-    cudaFree(r.warp);
+    cudaFree(r.warp[0]);
+    cudaFree(r.warp[1]);
     cudaFree(r.team);
     cudaFree(r.hub);
     cudaFree(r.len);
@@ -604,6 +630,10 @@ static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, flo
     if (g->w) LP_CK(dalloc(&P.sw, P.m_active, &bytes));
     k_plan_rows<<<g->num_sms * 16, 256, 0, st>>>(P.spos, P.vid, P.pos, g->off, g->nbr, g->w, P.soff, P.snbr, P.sw,
                                                  P.S);
+    if (g->wmode == kFixed && P.S > 0) {
+        LP_CK(dalloc(&P.swsum, P.S, &bytes));
+        k_plan_wsum<<<g->num_sms * 16, 256, 0, st>>>(P.soff, P.sw, P.swsum, P.S);
+    }
     LP_CK(cudaGetLastError());
     LP_CK(cudaEventRecord(g->ev1, st));
     LP_CK(cudaEventSynchronize(g->ev1));
@@ -626,7 +656,8 @@ static cudaError_t alloc_routes(lp_graph* g) {
     cudaError_t e;
     for (int c = 0; c < 3; ++c)
         if ((e = dalloc(&r.small[c], n, &g->bytes))) return e;
-    if ((e = dalloc(&r.warp, n, &g->bytes))) return e;
+    if ((e = dalloc(&r.warp[0], n, &g->bytes))) return e;
+    if ((e = dalloc(&r.warp[1], n, &g->bytes))) return e;
     if ((e = dalloc(&r.team, 2 * n, &g->bytes))) return e;
     if ((e = dalloc(&r.hub, g->cap_items, &g->bytes))) return e;
     if ((e = dalloc(&r.len, kLenCount, &g->bytes))) return e;
@@ -825,6 +856,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.soff = P.soff;
     a.snbr = P.snbr;
     a.sw = P.sw;
+    a.swsum = P.swsum;
     a.spos = P.spos;
     a.vid = P.vid;
     a.mark = cross ? g->mark : nullptr;
@@ -832,6 +864,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.counters = g->counters;
     a.r = g->routes;
     a.bs = (int32_t)bs;
+    a.n = (int32_t)n;
     a.bin = 0;
     a.seed = o->seed;
 
@@ -860,7 +893,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
             LP_CK(cudaMemcpyAsync(g->h_len, g->routes.len, kLenCount * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
             LP_CK(cudaStreamSynchronize(st));
             const int64_t total = (int64_t)g->h_len[kLenS4] + g->h_len[kLenS8] + g->h_len[kLenS16] +
-                                  g->h_len[kLenWarp] + g->h_len[kLenTeam] + g->h_len[kLenHub];
+                                  g->h_len[kLenWarp] + g->h_len[kLenWarpBig] + g->h_len[kLenTeam] + g->h_len[kLenHub];
             if (total == 0) break;
             LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
             run_round(g, a, false, g->h_len, &prof);
@@ -941,5 +974,69 @@ extern "C" int lp_host_register(void* ptr, int64_t bytes) {
 extern "C" int lp_host_unregister(void* ptr) {
     if (!ptr) return lp_fail(LP_ERR_INVALID, "NULL pointer");
     LP_CK(cudaHostUnregister(ptr));
+    return LP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// calibration: memory-only passes over the storage CSR (no tally)
+// ---------------------------------------------------------------------------
+// mode 0: stream every neighbour index once (the compulsory DRAM traffic)
+// mode 1: index + neighbour-label gather, per-row XOR (the sweep's memory
+//         pattern without any hashing) -- the practical floor of a sweep
+// mode 0/1: warp per row, plain loop (the naive structure)
+// mode 2/3: flat arc-parallel stream, 8 loads in flight per thread (the floor)
+__global__ void k_calib(const uint32_t* __restrict__ soff, const int32_t* __restrict__ snbr,
+                        const int32_t* __restrict__ lab, int64_t S, int mode, unsigned long long* sink) {
+    const int lane = threadIdx.x & 31;
+    unsigned acc = 0;
+    if (mode < 2) {
+        const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
+        for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < S; s += warps) {
+            const uint32_t b = soff[s], e = soff[s + 1];
+            for (uint32_t k = b + lane; k < e; k += 32) {
+                const int32_t u = __ldg(snbr + k);
+                acc ^= mode ? (unsigned)__ldg(lab + u) : (unsigned)u;
+            }
+        }
+    } else {
+        const int64_t m = soff[S];
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < m; base += stride * 8) {
+            int32_t u[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int64_t e = base + j * stride;
+                u[j] = e < m ? __ldg(snbr + e) : 0;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc ^= mode == 3 ? (unsigned)__ldg(lab + u[j]) : (unsigned)u[j];
+        }
+    }
+    acc = __reduce_xor_sync(0xffffffffu, acc);
+    if (lane == 0 && acc == 0x12345678u) atomicAdd(sink, 1ull);
+}
+
+extern "C" int lp_calibrate(lp_graph* g, int32_t mode, int32_t reps, double* ms_out) {
+    if (!g || !ms_out || reps < 1) return lp_fail(LP_ERR_INVALID, "bad arguments");
+    if (!g->plan.valid) return lp_fail(LP_ERR_INVALID, "run a detection first (plan needed)");
+    LP_CK(cudaSetDevice(g->device));
+    const Plan& P = g->plan;
+    cudaStream_t st = g->stream;
+    k_init_labels<<<g->num_sms * 8, 256, 0, st>>>(P.vid, nullptr, g->labA, g->n);
+    // mode 4/5: the same flat passes over the ORIGINAL CSR (neighbour ids in
+    // vertex-id order, labels indexed by vertex id)
+    const uint32_t* soff = mode >= 4 ? g->off : P.soff;
+    const int32_t* snbr = mode >= 4 ? g->nbr : P.snbr;
+    const int64_t rows = mode >= 4 ? g->n : P.S;
+    const int km = mode >= 4 ? mode - 2 : mode;
+    k_calib<<<g->num_sms * 16, 256, 0, st>>>(soff, snbr, g->labA, rows, km, g->counters);
+    LP_CK(cudaEventRecord(g->ev0, st));
+    for (int r = 0; r < reps; ++r)
+        k_calib<<<g->num_sms * 16, 256, 0, st>>>(soff, snbr, g->labA, rows, km, g->counters);
+    LP_CK(cudaEventRecord(g->ev1, st));
+    LP_CK(cudaEventSynchronize(g->ev1));
+    float ms = 0.f;
+    LP_CK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+    *ms_out = ms / reps;
     return LP_OK;
 }

@@ -62,19 +62,21 @@ enum {
     kLenS4 = 0,   // small rows, d <= 4
     kLenS8 = 1,   // d <= 8
     kLenS16 = 2,  // d <= 16
-    kLenWarp = 3,
+    kLenWarp = 3,     // warp per vertex, 512-slot table
     kLenTeam = 4,
     kLenHub = 5,
-    kCandCursor = 6,
-    kTeamCursor = 7,
-    kHubCursor = 8,
-    kGtabCursor = 9,
-    kLenCount = 12
+    kLenWarpBig = 6,  // warp per vertex, 2048-slot table
+    kCandCursor = 7,
+    kTeamCursor = 8,
+    kHubCursor = 9,
+    kGtabCursor = 10,
+    kWarpCursor = 11,  // + warp class (0 / 1)
+    kLenCount = 16
 };
 
 struct Routes {
     int32_t* small[3];  // slot lists by small degree class (4, 8, 16)
-    int32_t* warp;
+    int32_t* warp[2];   // slot lists of the two warp classes
     Item* team;
     Item* hub;
     int32_t* len;  // kLen*
@@ -90,6 +92,7 @@ struct EvalArgs {
     const uint32_t* __restrict__ soff;  // storage row offsets [S+1]
     const int32_t* __restrict__ snbr;   // neighbour positions
     const uint32_t* __restrict__ sw;    // arc weights (fixed-point u32 or float bits); null = unit
+    const unsigned long long* __restrict__ swsum;  // per-slot total weight (fixed mode), null otherwise
     const int32_t* __restrict__ spos;   // slot -> position
     const int32_t* __restrict__ vid;    // position -> vertex id
     const int32_t* __restrict__ L0;     // labels at sweep start (read-only in a sweep)
@@ -99,6 +102,7 @@ struct EvalArgs {
     unsigned long long* counters;       // see kCtr* below
     Routes r;
     int32_t bs;   // batch size in positions
+    int32_t n;    // vertex count
     int32_t bin;  // counter slot of this launch
     uint32_t seed;
     uint32_t sweep;
@@ -109,12 +113,25 @@ struct EvalArgs {
 // (k = 0 hub team, 1 8-warp team, 2 warp, 3 small; accumulated over a run)
 enum { kCtrChanged = 0, kCtrWrites = 1, kCtrArcs = 4, kCtrVerts = 8, kCtrCount = 12 };
 
+// ndist[s]: low 30 bits = distinct labels seen at the last evaluation;
+// kMajBit = that evaluation's winner held a strict majority of the row's
+// weight.  A vertex flagged so first tries the majority check: count the
+// weight of its current label; if it exceeds half the row it is the unique
+// argmax (no tie is possible) and the tally is skipped entirely.
+constexpr int32_t kMajBit = 1 << 30;
+__host__ __device__ __forceinline__ int32_t nd_count(int32_t v) { return v & (kMajBit - 1); }
+
 constexpr int kSmallMax = 16;     // thread-per-vertex bound (degree)
-constexpr int kWarpEst = 256;     // warp path: estimated distinct labels
-constexpr int kWarpMaxDeg = 2048;
-constexpr int kWarpBits = 9;      // 512-slot warp table
-constexpr int kWarpCap = 384;     // touched entries before a warp spills
-constexpr int kWarpsPerBlock = 8;
+// warp classes: 0 = 512-slot table (est <= 256, d <= 2048, 8 warps/block),
+// 1 = 2048-slot table (est <= 1024, d <= 8192, 4 warps/block)
+template <int WC> struct WarpClass;
+template <> struct WarpClass<0> {
+    static constexpr int kBits = 9, kEst = 256, kMaxDeg = 2048, kWarps = 8, kList = 3;
+};
+template <> struct WarpClass<1> {
+    static constexpr int kBits = 11, kEst = 1024, kMaxDeg = 8192, kWarps = 4, kList = 6;
+};
+constexpr int kWarpEst = WarpClass<0>::kEst;
 constexpr int kTeamEst = 2048;    // 8-warp team: 4096-slot table
 constexpr int kTeamMaxDeg = 16384;
 constexpr int kTeamBits = 12, kTeamThreads = 256;
@@ -133,6 +150,13 @@ template <int WM> __device__ __forceinline__ typename Acc<WM>::T arc_weight(cons
     } else {
         return __uint_as_float(__ldg(a.sw + e));
     }
+}
+
+// First position of p's batch (bs == 1: the reference order; bs >= n: sync).
+__device__ __forceinline__ int32_t batch_start(const EvalArgs& a, int32_t p) {
+    if (a.bs == 1) return p;
+    if (a.bs >= a.n) return 0;
+    return (p / a.bs) * a.bs;
 }
 
 // Neighbour label under the batched schedule: neighbours in an earlier batch
@@ -183,7 +207,7 @@ __device__ __forceinline__ void mark_row(const EvalArgs& a, uint32_t beg, int d,
 // ---------------------------------------------------------------------------
 // routing
 // ---------------------------------------------------------------------------
-// cls: 0/1/2 small (d <= 4 / 8 / 16), 3 warp, 4 team, 5 hub
+// cls: 0/1/2 small (d <= 4 / 8 / 16), 3 warp, 6 big-table warp, 4 team, 5 hub
 __device__ __forceinline__ int small_class(int d) { return d <= 4 ? 0 : (d <= 8 ? 1 : 2); }
 
 __device__ __forceinline__ int route_class(const EvalArgs& a, int32_t s, int& est, int& d) {
@@ -192,9 +216,10 @@ __device__ __forceinline__ int route_class(const EvalArgs& a, int32_t s, int& es
         est = d;
         return small_class(d);
     }
-    const int nd = __ldg(a.ndist + s);
+    const int nd = nd_count(__ldg(a.ndist + s));
     est = min(d, nd + (nd >> 2) + 16);
-    if (est <= kWarpEst && d <= kWarpMaxDeg) return 3;
+    if (est <= WarpClass<0>::kEst && d <= WarpClass<0>::kMaxDeg) return 3;
+    if (est <= WarpClass<1>::kEst && d <= WarpClass<1>::kMaxDeg) return 6;
     if (est <= kTeamEst && d <= kTeamMaxDeg) return 4;
     return 5;
 }
@@ -205,7 +230,8 @@ __device__ __forceinline__ void route_append(const EvalArgs& a, int cls, int32_t
     const int lane = threadIdx.x & 31;
     const uint32_t act = __activemask();
 #pragma unroll
-    for (int c = 0; c < 5; ++c) {
+    for (int c = 0; c < 7; ++c) {
+        if (c == 5) continue;  // hubs below
         const uint32_t m = __ballot_sync(act, cls == c);
         if (!m) continue;
         const int leader = __ffs(m) - 1;
@@ -217,7 +243,9 @@ __device__ __forceinline__ void route_append(const EvalArgs& a, int cls, int32_t
             if (c < 3) {
                 a.r.small[c][idx] = s;
             } else if (c == 3) {
-                a.r.warp[idx] = s;
+                a.r.warp[0][idx] = s;
+            } else if (c == 6) {
+                a.r.warp[1][idx] = s;
             } else {
                 Item t = {s, 0, 1, 0, 1, -1, 0, 0};
                 a.r.team[idx] = t;
@@ -293,7 +321,7 @@ __global__ void k_route_marked(EvalArgs a, uint8_t* __restrict__ mark, const int
 // Dense mode sweeps slots [s_beg, s_end); list mode (s_beg < 0) reads the
 // class's route list.
 template <int WM, int TIE, int MAXD>
-__global__ void __launch_bounds__(256) k_small(EvalArgs a, int32_t s_beg, int32_t s_end) {
+__global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, int32_t s_beg, int32_t s_end) {
     using A = typename Acc<WM>::T;
     constexpr int LIST = MAXD == 4 ? kLenS4 : (MAXD == 8 ? kLenS8 : kLenS16);
     const bool listed = s_beg < 0;
@@ -305,7 +333,7 @@ __global__ void __launch_bounds__(256) k_small(EvalArgs a, int32_t s_beg, int32_
         const int32_t p = __ldg(a.spos + s);
         const uint32_t beg = __ldg(a.soff + s);
         const int d = (int)(__ldg(a.soff + s + 1) - beg);
-        const int32_t thr = (p / a.bs) * a.bs;
+        const int32_t thr = batch_start(a, p);
         int32_t nbr[MAXD];
 #pragma unroll
         for (int k = 0; k < MAXD; ++k) nbr[k] = (k < d) ? __ldg(a.snbr + beg + k) : 0;
@@ -320,6 +348,20 @@ __global__ void __launch_bounds__(256) k_small(EvalArgs a, int32_t s_beg, int32_
                 lab[k] = kEmpty;
                 w[k] = A(0);
             }
+        }
+        const int32_t nd = __ldg(a.ndist + s);
+        arcs += d;
+        ++verts;
+        A total = A(0);
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) total += w[k];
+        if ((nd & kMajBit) && WM != kFloat) {
+            const int32_t cand = a.x[p];
+            A cw = A(0);
+#pragma unroll
+            for (int k = 0; k < MAXD; ++k)
+                if (lab[k] == cand) cw += w[k];
+            if (cw + cw > total) continue;  // strict majority: label unchanged
         }
         const uint32_t vtx = (TIE == kRandom) ? (uint32_t)__ldg(a.vid + p) : 0u;
         Cand<A> best = none_cand<A>();
@@ -341,8 +383,8 @@ __global__ void __launch_bounds__(256) k_small(EvalArgs a, int32_t s_beg, int32_
                 }
             }
         }
-        arcs += d;
-        ++verts;
+        const int32_t nd_new = (best.w + best.w > total) ? kMajBit : 0;
+        if (nd_new != nd) a.ndist[s] = nd_new;
         if (commit_label(a, p, best.lab, dchg, writes) && a.mark) {
             const int32_t nb = thr + a.bs;
 #pragma unroll
@@ -354,250 +396,19 @@ __global__ void __launch_bounds__(256) k_small(EvalArgs a, int32_t s_beg, int32_
 }
 
 // ---------------------------------------------------------------------------
-// warp per vertex
+// shared-memory tally tables
 // ---------------------------------------------------------------------------
-template <typename A> struct WarpTable {
-    int32_t keys[1 << kWarpBits];
-    A acc[1 << kWarpBits];
-    uint16_t first[1 << kWarpBits];
-    uint16_t touched[kWarpCap + 32];
-};
+// Open addressing with linear probing; entries are wiped after each vertex
+// through a touched list.  There is no first-position field: ties at the
+// maximum are resolved afterwards by scanning the row for the earliest arc
+// whose label is tied (resolve_first), so a distinct label costs a single
+// shared-memory atomic.  For unit weights (label, count) is one 64-bit word
+// inserted by CAS and bumped by atomicAdd; weighted tables keep keys and
+// 64-bit fixed-point (or float) sums side by side.
+constexpr unsigned long long kEmpty64 = 0xffffffff00000000ull;
 
-// Sum of `w` over the lanes in `m` (all lanes call; result in every lane).
-template <typename A> __device__ __forceinline__ A masked_sum(uint32_t m, A w) {
-    A v = ((m >> (threadIdx.x & 31)) & 1u) ? w : A(0);
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) v += shfl_xor_any(v, o);
-    return v;
-}
-
-// Warp per vertex.  Tally first in a warp-wide register table (entry t lives
-// in lane t: key, weight, first position; up to 32 distinct labels) -- after
-// the first sweep most rows hold a handful of labels and this path needs no
-// shared memory and no atomics.  A row with more distinct labels spills the
-// register table into the warp's shared-memory hash and continues there.
-template <int WM, int TIE>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_warp(EvalArgs a) {
-    using A = typename Acc<WM>::T;
-    constexpr int HB = 1 << kWarpBits;
-    constexpr int U = 4;  // 32-arc chunks gathered per step
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    WarpTable<A>* tab = reinterpret_cast<WarpTable<A>*>(smem_raw) + wib;
-    for (int h = lane; h < HB; h += 32) tab->keys[h] = kEmpty;
-    __syncwarp();
-
-    const int32_t cnt = a.r.len[kLenWarp];
-    const int32_t nwarps = gridDim.x * kWarpsPerBlock;
-    long long dchg = 0, arcs = 0, writes = 0, verts = 0;
-
-    // insert one chunk's labels into the shared hash (leaders of equal-label groups)
-    auto hash_chunk = [&](int32_t lab, A w, int k, int& ntouched) {
-        const uint32_t grp = __match_any_sync(0xffffffffu, lab);
-        const int leader = __ffs(grp) - 1;
-        int h = -1;
-        bool isnew = false;
-        if (lab != kEmpty && lane == leader) {
-            h = (int)slot_hash(lab, kWarpBits);
-            while (true) {
-                const int32_t cur = tab->keys[h];
-                if (cur == lab) break;
-                if (cur == kEmpty) {
-                    const int32_t old = atomicCAS(&tab->keys[h], kEmpty, lab);
-                    if (old == kEmpty) {
-                        isnew = true;
-                        tab->first[h] = (uint16_t)k;
-                        tab->acc[h] = A(0);
-                        break;
-                    }
-                    if (old == lab) break;
-                }
-                h = (h + 1) & (HB - 1);
-            }
-            // leaders hold distinct labels -> distinct slots: plain update
-            if constexpr (WM == kUnit) tab->acc[h] += (A)__popc(grp);
-        }
-        if constexpr (WM != kUnit) {
-            __syncwarp();
-            const int hb = __shfl_sync(0xffffffffu, h, leader);
-            if (lab != kEmpty) atomicAdd(&tab->acc[hb], w);
-        }
-        const uint32_t nb = __ballot_sync(0xffffffffu, isnew);
-        if (isnew) {
-            const int idx = ntouched + __popc(nb & lanemask_lt());
-            if (idx < kWarpCap + 32) tab->touched[idx] = (uint16_t)h;
-        }
-        ntouched += __popc(nb);
-        __syncwarp();
-    };
-
-    for (int32_t i = blockIdx.x * kWarpsPerBlock + wib; i < cnt; i += nwarps) {
-        const int32_t s = a.r.warp[i];
-        const int32_t p = __ldg(a.spos + s);
-        const uint32_t beg = __ldg(a.soff + s);
-        const int d = (int)(__ldg(a.soff + s + 1) - beg);
-        const int32_t thr = (p / a.bs) * a.bs;
-        // register table
-        int32_t tkey = kEmpty;
-        A tacc = A(0);
-        uint32_t tfirst = 0;
-        int K = 0;               // register entries in use (warp-uniform)
-        bool hashed = false;     // spilled to the shared hash
-        int ntouched = 0;
-        bool overflow = false;
-        for (int base = 0; base < d && !overflow; base += 32 * U) {
-            int32_t nbr[U];
-#pragma unroll
-            for (int c = 0; c < U; ++c) {
-                const int k = base + c * 32 + lane;
-                nbr[c] = (k < d) ? __ldg(a.snbr + beg + k) : -1;
-            }
-            int32_t labv[U];
-            A wv[U];
-#pragma unroll
-            for (int c = 0; c < U; ++c) {
-                const int k = base + c * 32 + lane;
-                labv[c] = (k < d) ? read_label(a, nbr[c], thr) : kEmpty;
-                wv[c] = (k < d) ? arc_weight<WM>(a, beg + k) : A(0);
-            }
-#pragma unroll
-            for (int c = 0; c < U; ++c) {
-                if (base + c * 32 >= d) break;  // warp-uniform
-                const int k0 = base + c * 32;
-                int32_t lab = labv[c];
-                if (!hashed) {
-                    uint32_t pending = __ballot_sync(0xffffffffu, lab != kEmpty);
-                    for (int t = 0; t < K && pending; ++t) {
-                        const int32_t key = __shfl_sync(0xffffffffu, tkey, t);
-                        const uint32_t m = __ballot_sync(0xffffffffu, lab == key) & pending;
-                        if (m) {
-                            pending &= ~m;
-                            A add;
-                            if constexpr (WM == kUnit)
-                                add = (A)__popc(m);
-                            else
-                                add = masked_sum<A>(m, wv[c]);
-                            if (lane == t) tacc += add;
-                        }
-                    }
-                    while (pending && K < 32) {
-                        const int leader = __ffs(pending) - 1;
-                        const int32_t key = __shfl_sync(0xffffffffu, lab, leader);
-                        const uint32_t m = __ballot_sync(0xffffffffu, lab == key) & pending;
-                        pending &= ~m;
-                        A add;
-                        if constexpr (WM == kUnit)
-                            add = (A)__popc(m);
-                        else
-                            add = masked_sum<A>(m, wv[c]);
-                        if (lane == K) {
-                            tkey = key;
-                            tacc = add;
-                            tfirst = (uint32_t)(k0 + leader);
-                        }
-                        ++K;
-                    }
-                    if (!pending) continue;
-                    // more than 32 distinct labels: move the register table to
-                    // the shared hash, then insert the rest of this chunk there
-                    bool isnew = false;
-                    int h = -1;
-                    if (lane < K) {
-                        h = (int)slot_hash(tkey, kWarpBits);
-                        while (true) {
-                            const int32_t old = atomicCAS(&tab->keys[h], kEmpty, tkey);
-                            if (old == kEmpty) break;
-                            h = (h + 1) & (HB - 1);
-                        }
-                        isnew = true;
-                        tab->acc[h] = tacc;
-                        tab->first[h] = (uint16_t)tfirst;
-                    }
-                    const uint32_t nb = __ballot_sync(0xffffffffu, isnew);
-                    if (isnew) tab->touched[__popc(nb & lanemask_lt())] = (uint16_t)h;
-                    ntouched = __popc(nb);
-                    __syncwarp();
-                    hashed = true;
-                    if (!((pending >> lane) & 1u)) lab = kEmpty;
-                }
-                hash_chunk(lab, wv[c], k0 + lane, ntouched);
-                if (ntouched > kWarpCap) {
-                    overflow = true;
-                    break;
-                }
-            }
-        }
-        if (overflow) {
-            // too many distinct labels for this table: wipe it and hand the
-            // vertex to the team kernel (launched after this one)
-            for (int h = lane; h < HB; h += 32) tab->keys[h] = kEmpty;
-            if (lane == 0) {
-                const int idx = atomicAdd(a.r.len + kLenTeam, 1);
-                Item t = {s, 0, 1, 0, 1, -1, 0, 0};
-                a.r.team[idx] = t;
-                a.ndist[s] = max(__ldg(a.ndist + s), 2 * kWarpEst);
-            }
-            __syncwarp();
-            continue;
-        }
-        const uint32_t vtx = (TIE == kRandom) ? (uint32_t)__ldg(a.vid + p) : 0u;
-        Cand<A> best = none_cand<A>();
-        if (!hashed) {
-            if (lane < K) best = make_cand<TIE, A>(tacc, tkey, tfirst, a.seed, a.sweep, vtx);
-        } else {
-            for (int t = lane; t < ntouched; t += 32) {
-                const int h = tab->touched[t];
-                Cand<A> c = make_cand<TIE, A>(tab->acc[h], tab->keys[h], tab->first[h], a.seed, a.sweep, vtx);
-                if (better(c, best)) best = c;
-            }
-        }
-        best = warp_best(best);
-        if (hashed) {
-            __syncwarp();
-            for (int t = lane; t < ntouched; t += 32) tab->keys[tab->touched[t]] = kEmpty;
-            __syncwarp();
-        }
-        bool changed = false;
-        if (lane == 0) {
-            arcs += d;
-            ++verts;
-            a.ndist[s] = hashed ? ntouched : K;
-            changed = commit_label(a, p, best.lab, dchg, writes);
-        }
-        changed = __shfl_sync(0xffffffffu, changed, 0);
-        if (changed && a.mark) mark_row(a, beg, d, thr, lane, 32);
-    }
-    flush_counters(a, dchg, arcs, writes, verts);
-}
-
-// ---------------------------------------------------------------------------
-// block (team) per work item
-// ---------------------------------------------------------------------------
-template <typename A, int TBITS> struct TeamTable {
-    static constexpr int HB = 1 << TBITS;
-    static constexpr int CAP = HB / 4 * 3;  // touched capacity; beyond it = overflow
-    int32_t keys[HB];
-    A acc[HB];
-    uint32_t first[HB];
-    uint16_t touched[CAP];
-};
-
-template <typename A> __device__ __forceinline__ unsigned long long to_bits(A w) {
-    if constexpr (std::is_same<A, float>::value)
-        return (unsigned long long)__float_as_uint(w);
-    else
-        return (unsigned long long)w;
-}
-template <typename A> __device__ __forceinline__ A from_bits(unsigned long long b) {
-    if constexpr (std::is_same<A, float>::value)
-        return __uint_as_float((uint32_t)b);
-    else
-        return (A)b;
-}
-
-// Find or insert `lab` in an open-addressing table of 2^bits keys (shared or
-// global memory).  Returns -1 only when the table is full.
+// Find or insert `lab` in an open-addressing key array of 2^bits slots
+// (shared or global memory).  Returns -1 only when the table is full.
 __device__ __forceinline__ int table_slot(int32_t* keys, int32_t lab, int bits, bool& isnew) {
     const int mask = (1 << bits) - 1;
     int h = (int)slot_hash(lab, bits);
@@ -618,6 +429,596 @@ __device__ __forceinline__ int table_slot(int32_t* keys, int32_t lab, int bits, 
     return -1;
 }
 
+template <int WM, int BITS> struct STable {
+    using A = typename Acc<WM>::T;
+    static constexpr int HB = 1 << BITS;
+    int32_t keys[HB];
+    A acc[HB];
+    __device__ __forceinline__ void init(int h) {
+        keys[h] = kEmpty;
+        acc[h] = A(0);
+    }
+    __device__ __forceinline__ int32_t key(int h) const { return keys[h]; }
+    __device__ __forceinline__ A weight(int h) const { return acc[h]; }
+    __device__ __forceinline__ int add(int32_t lab, A w, bool& isnew) {
+        const int h = table_slot(keys, lab, BITS, isnew);
+        if (h >= 0) atomicAdd(&acc[h], w);
+        return h;
+    }
+    __device__ __forceinline__ int find(int32_t lab) const {
+        int h = (int)slot_hash(lab, BITS);
+        for (int probe = 0; probe < HB; ++probe) {
+            const int32_t cur = keys[h];
+            if (cur == lab) return h;
+            if (cur == kEmpty) return -1;
+            h = (h + 1) & (HB - 1);
+        }
+        return -1;
+    }
+};
+
+template <int BITS> struct STable<kUnit, BITS> {
+    using A = uint32_t;
+    static constexpr int HB = 1 << BITS;
+    unsigned long long ent[HB];
+    __device__ __forceinline__ void init(int h) { ent[h] = kEmpty64; }
+    __device__ __forceinline__ int32_t key(int h) const { return (int32_t)(ent[h] >> 32); }
+    __device__ __forceinline__ A weight(int h) const { return (uint32_t)ent[h]; }
+    __device__ __forceinline__ int add(int32_t lab, uint32_t c, bool& isnew) {
+        int h = (int)slot_hash(lab, BITS);
+        isnew = false;
+        const unsigned long long mine = ((unsigned long long)(uint32_t)lab << 32) | c;
+        for (int probe = 0; probe < HB; ++probe) {
+            const unsigned long long e = *(volatile unsigned long long*)&ent[h];
+            const int32_t k = (int32_t)(e >> 32);
+            if (k == lab) {
+                atomicAdd(&ent[h], (unsigned long long)c);
+                return h;
+            }
+            if (k == kEmpty) {
+                const unsigned long long old = atomicCAS(&ent[h], kEmpty64, mine);
+                if (old == kEmpty64) {
+                    isnew = true;
+                    return h;
+                }
+                if ((int32_t)(old >> 32) == lab) {
+                    atomicAdd(&ent[h], (unsigned long long)c);
+                    return h;
+                }
+            }
+            h = (h + 1) & (HB - 1);
+        }
+        return -1;
+    }
+    __device__ __forceinline__ int find(int32_t lab) const {
+        int h = (int)slot_hash(lab, BITS);
+        for (int probe = 0; probe < HB; ++probe) {
+            const int32_t k = (int32_t)(ent[h] >> 32);
+            if (k == lab) return h;
+            if (k == kEmpty) return -1;
+            h = (h + 1) & (HB - 1);
+        }
+        return -1;
+    }
+};
+
+// Argmax candidate with the number of distinct labels sharing its
+// (weight, sec) key -- `mult` > 1 means the first-position scan decides.
+template <typename A> struct Best {
+    A w;
+    uint32_t sec;
+    uint32_t ter;  // ~first position once resolved, else 0
+    int32_t lab;
+    int32_t mult;
+};
+
+template <typename A> __device__ __forceinline__ A from_bits_any(unsigned long long b) {
+    if constexpr (std::is_same<A, float>::value)
+        return __uint_as_float((uint32_t)b);
+    else
+        return (A)b;
+}
+
+template <typename A> __device__ __forceinline__ Best<A> none_best() {
+    Best<A> b;
+    b.w = A(0);
+    b.sec = 0;
+    b.ter = 0;
+    b.lab = -1;
+    b.mult = 0;
+    return b;
+}
+
+template <int TIE>
+__device__ __forceinline__ uint32_t sec_of(int32_t lab, uint32_t seed, uint32_t sweep, uint32_t vtx) {
+    if (TIE == kScanFirst) return 0u;
+    if (TIE == kMinLabel) return ~(uint32_t)lab;
+    return tie_hash(seed, sweep, vtx, (uint32_t)lab);
+}
+
+// merge y into x (x keeps the larger key; equal keys add multiplicities)
+template <typename A> __device__ __forceinline__ void merge_best(Best<A>& x, const Best<A>& y) {
+    if (y.mult == 0) return;
+    if (x.mult == 0 || y.w > x.w || (y.w == x.w && (y.sec > x.sec || (y.sec == x.sec && y.ter > x.ter)))) {
+        x = y;
+    } else if (y.w == x.w && y.sec == x.sec && y.ter == x.ter) {
+        x.mult += y.mult;
+        x.lab = min(x.lab, y.lab);
+    }
+}
+
+template <typename A> __device__ __forceinline__ Best<A> warp_merge(Best<A> b) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+        Best<A> o;
+        o.w = shfl_xor_any(b.w, m);
+        o.sec = __shfl_xor_sync(0xffffffffu, b.sec, m);
+        o.ter = __shfl_xor_sync(0xffffffffu, b.ter, m);
+        o.lab = __shfl_xor_sync(0xffffffffu, b.lab, m);
+        o.mult = __shfl_xor_sync(0xffffffffu, b.mult, m);
+        merge_best(b, o);
+    }
+    return b;
+}
+
+// Order-preserving 64-bit image of a (non-negative) weight, for max-reductions.
+template <typename A> __device__ __forceinline__ unsigned long long wbits(A w) {
+    if constexpr (std::is_same<A, float>::value)
+        return (unsigned long long)__float_as_uint(w);
+    else
+        return (unsigned long long)w;
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const unsigned long long u = shfl_u64(v, o);
+        v = u > v ? u : v;
+    }
+    return v;
+}
+
+// Winner of the `nt` touched entries of a table, reduced over the calling
+// group (one warp: GROUP_NW = 1, else a block of GROUP_NW warps using the
+// shared scratch `red`).  Three cheap passes instead of a struct reduction:
+// max weight, max tie key among the maxima, then how many entries share both
+// (mult > 1 -> the caller resolves by scan order).
+struct ArgmaxScratch {
+    unsigned long long w;
+    uint32_t sec;
+    int32_t cnt;
+    int32_t lab;
+};
+
+template <int WM, int TIE, int BITS, int GROUP_NW>
+__device__ __forceinline__ Best<typename Acc<WM>::T> table_argmax(const STable<WM, BITS>& t, const uint16_t* touched,
+                                                                  int nt, int tid, uint32_t seed, uint32_t sweep,
+                                                                  uint32_t vtx, ArgmaxScratch* red) {
+    using A = typename Acc<WM>::T;
+    constexpr int NT = GROUP_NW * 32;
+    const int lane = threadIdx.x & 31;
+    // 1. max weight
+    unsigned long long mw = 0;
+    for (int i = tid; i < nt; i += NT) {
+        const unsigned long long b = wbits<A>(t.weight(touched[i]));
+        mw = b > mw ? b : mw;
+    }
+    mw = warp_max_u64(mw);
+    if (GROUP_NW > 1) {
+        if (tid == 0) {
+            red->w = 0;
+            red->sec = 0;
+            red->cnt = 0;
+            red->lab = -1;
+        }
+        __syncthreads();
+        if (lane == 0) atomicMax(&red->w, mw);
+        __syncthreads();
+        mw = red->w;
+    }
+    // 2. max tie key among the maxima (scan-first: none)
+    uint32_t ms = 0;
+    if (TIE != kScanFirst) {
+        for (int i = tid; i < nt; i += NT) {
+            const int h = touched[i];
+            if (wbits<A>(t.weight(h)) == mw) {
+                const uint32_t sc = sec_of<TIE>(t.key(h), seed, sweep, vtx);
+                ms = sc > ms ? sc : ms;
+            }
+        }
+        ms = __reduce_max_sync(0xffffffffu, ms);
+        if (GROUP_NW > 1) {
+            if (lane == 0) atomicMax(&red->sec, ms);
+            __syncthreads();
+            ms = red->sec;
+        }
+    }
+    // 3. multiplicity and one label
+    int c = 0;
+    int32_t lab = -1;
+    for (int i = tid; i < nt; i += NT) {
+        const int h = touched[i];
+        if (wbits<A>(t.weight(h)) == mw && (TIE == kScanFirst || sec_of<TIE>(t.key(h), seed, sweep, vtx) == ms)) {
+            ++c;
+            lab = t.key(h);
+        }
+    }
+    Best<A> r;
+    r.w = from_bits_any<A>(mw);
+    r.sec = ms;
+    r.ter = 0;
+    const int wc = (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+    const unsigned hasb = __ballot_sync(0xffffffffu, lab >= 0);
+    const int32_t wl = hasb ? __shfl_sync(0xffffffffu, lab, __ffs(hasb) - 1) : -1;
+    if (GROUP_NW > 1) {
+        if (lane == 0 && wc) {
+            atomicAdd(&red->cnt, wc);
+            red->lab = wl;
+        }
+        __syncthreads();
+        r.mult = red->cnt;
+        r.lab = red->lab;
+        __syncthreads();
+    } else {
+        r.mult = wc;
+        r.lab = wl;
+    }
+    return r;
+}
+
+// Sum of `w` over the lanes in `m` (all lanes call; result in every lane).
+template <typename A> __device__ __forceinline__ A masked_sum(uint32_t m, A w) {
+    A v = ((m >> (threadIdx.x & 31)) & 1u) ? w : A(0);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += shfl_xor_any(v, o);
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// warp per vertex
+// ---------------------------------------------------------------------------
+template <int WM, int WC> struct WarpTable {
+    static constexpr int kCap = (1 << WarpClass<WC>::kBits) / 4 * 3;  // touched entries before a spill
+    STable<WM, WarpClass<WC>::kBits> t;
+    uint16_t touched[kCap + 32];
+};
+
+// Insert one 32-arc chunk into a shared table.  agg: fold equal labels with
+// __match_any_sync first (rows with few distinct labels); otherwise every lane
+// inserts its own label (rows whose labels are mostly distinct).
+// Returns this lane's slot when it created a new entry, else -1.
+template <int WM, int BITS>
+__device__ __forceinline__ int insert_chunk(STable<WM, BITS>& t, int32_t lab, typename Acc<WM>::T w, bool agg,
+                                            bool& full) {
+    using A = typename Acc<WM>::T;
+    const int lane = threadIdx.x & 31;
+    bool isnew = false;
+    int h = -1;
+    if (agg) {
+        const uint32_t grp = __match_any_sync(0xffffffffu, lab);
+        const int leader = __ffs(grp) - 1;
+        if constexpr (WM == kUnit) {
+            if (lab != kEmpty && lane == leader) h = t.add(lab, (A)__popc(grp), isnew);
+        } else {
+            if (lab != kEmpty && lane == leader) h = t.add(lab, A(0), isnew);
+            const int hb = __shfl_sync(0xffffffffu, h, leader);
+            if (lab != kEmpty && hb >= 0) atomicAdd(&t.acc[hb], w);
+        }
+        if (lab != kEmpty && lane == leader && h < 0) full = true;
+    } else if (lab != kEmpty) {
+        if constexpr (WM == kUnit)
+            h = t.add(lab, 1u, isnew);
+        else
+            h = t.add(lab, w, isnew);
+        if (h < 0) full = true;
+    }
+    return isnew ? h : -1;
+}
+
+// Warp per vertex.  Tally first in a warp-wide register table (entry t lives
+// in lane t: key, weight, first position; up to 32 distinct labels) -- after
+// the first sweep most rows hold a handful of labels and this path needs no
+// shared memory and no atomics.  Rows estimated to hold more labels, or that
+// outgrow the register table, use the warp's shared-memory hash.
+template <int WM, int TIE, int WC>
+__global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 6) k_warp(EvalArgs a) {
+    using A = typename Acc<WM>::T;
+    using WT = WarpTable<WM, WC>;
+    constexpr int kWarpBits = WarpClass<WC>::kBits;
+    constexpr int kWarpCap = WT::kCap;
+    constexpr int kWarpsPerBlock = WarpClass<WC>::kWarps;
+    constexpr int HB = 1 << kWarpBits;
+    constexpr int U = 4;  // 32-arc chunks gathered per step
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    WT* tab = reinterpret_cast<WT*>(smem_raw) + wib;
+    for (int h = lane; h < HB; h += 32) tab->t.init(h);
+    __syncwarp();
+
+    const int32_t cnt = a.r.len[WarpClass<WC>::kList];
+    long long dchg = 0, arcs = 0, writes = 0, verts = 0;
+    const int32_t* list = a.r.warp[WC];
+    // batch size: 32 when the list is long, down to 1 so that short
+    // (frontier) lists still spread over every warp
+    const int bsz = max(1, min(32, cnt / (int)(gridDim.x * kWarpsPerBlock)));
+    while (true) {
+        int32_t b0 = 0;
+        if (lane == 0) b0 = atomicAdd(a.r.len + kWarpCursor + WC, bsz);
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (b0 >= cnt) break;
+        const int nv = min(bsz, cnt - b0);
+        int32_t ms = -1, mp = 0, mnd = 0;
+        uint32_t mbeg = 0, mend = 0;
+        if (lane < nv) {
+            ms = list[b0 + lane];
+            mp = __ldg(a.spos + ms);
+            mbeg = __ldg(a.soff + ms);
+            mend = __ldg(a.soff + ms + 1);
+            mnd = __ldg(a.ndist + ms);
+        }
+        // prefetched first index block of the current vertex
+        int32_t nbr_next[U];
+        {
+            const uint32_t beg0 = __shfl_sync(0xffffffffu, mbeg, 0);
+            const int d0 = (int)(__shfl_sync(0xffffffffu, mend, 0) - beg0);
+#pragma unroll
+            for (int c = 0; c < U; ++c) {
+                const int k = c * 32 + lane;
+                nbr_next[c] = (k < d0) ? __ldg(a.snbr + beg0 + k) : -1;
+            }
+        }
+        for (int v = 0; v < nv; ++v) {
+            const int32_t s = __shfl_sync(0xffffffffu, ms, v);
+            const int32_t p = __shfl_sync(0xffffffffu, mp, v);
+            const uint32_t beg = __shfl_sync(0xffffffffu, mbeg, v);
+            const int d = (int)(__shfl_sync(0xffffffffu, mend, v) - beg);
+            const int32_t nd = __shfl_sync(0xffffffffu, mnd, v);
+            const int32_t thr = batch_start(a, p);
+            const uint32_t vtx = (TIE == kRandom) ? (uint32_t)__ldg(a.vid + p) : 0u;
+            // prefetch the next block: of this row, else the next vertex's first one
+#define LP_WARP_PREFETCH(base_done)                                                             \
+    do {                                                                                        \
+        uint32_t nb_beg = beg;                                                                  \
+        int nb_base = (base_done) + 32 * U, nb_d = d;                                           \
+        if (nb_base >= d) {                                                                     \
+            const int vn = v + 1 < nv ? v + 1 : v;                                              \
+            nb_beg = __shfl_sync(0xffffffffu, mbeg, vn);                                        \
+            nb_d = v + 1 < nv ? (int)(__shfl_sync(0xffffffffu, mend, vn) - nb_beg) : 0;         \
+            nb_base = 0;                                                                        \
+        }                                                                                       \
+        _Pragma("unroll") for (int c_ = 0; c_ < U; ++c_) {                                      \
+            const int k_ = nb_base + c_ * 32 + lane;                                            \
+            nbr_next[c_] = (k_ < nb_d) ? __ldg(a.snbr + nb_beg + k_) : -1;                      \
+        }                                                                                       \
+    } while (0)
+            A total;
+            if constexpr (WM == kUnit)
+                total = (A)d;
+            else if constexpr (WM == kFixed)
+                total = (A)__ldg(a.swsum + s);
+            else
+                total = A(0);
+            // ---- majority check (vertices whose last winner held > half the row) ----
+            if (WM != kFloat && (nd & kMajBit)) {
+                const int32_t cand = a.x[p];
+                A cw = A(0);
+                for (int base = 0; base < d; base += 32 * U) {
+                    int32_t labv[U];
+#pragma unroll
+                    for (int c = 0; c < U; ++c) {
+                        const int k = base + c * 32 + lane;
+                        labv[c] = (k < d) ? read_label(a, nbr_next[c], thr) : kEmpty;
+                    }
+                    LP_WARP_PREFETCH(base);
+#pragma unroll
+                    for (int c = 0; c < U; ++c) {
+                        const int k = base + c * 32 + lane;
+                        if (labv[c] == cand && k < d) cw += arc_weight<WM>(a, beg + k);
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) cw += shfl_xor_any(cw, o);
+                if (cw + cw > total) {  // strict majority: the label stays
+                    if (lane == 0) {
+                        arcs += d;
+                        ++verts;
+                    }
+                    continue;
+                }
+                // no majority any more: full tally from the first block
+#pragma unroll
+                for (int c = 0; c < U; ++c) {
+                    const int k = c * 32 + lane;
+                    nbr_next[c] = (k < d) ? __ldg(a.snbr + beg + k) : -1;
+                }
+            }
+            const int est = min(d, nd_count(nd) + (nd_count(nd) >> 2) + 16);
+            const bool agg = true;  // fold equal labels (__match_any_sync) before inserting
+            // register table (rows estimated to hold few labels)
+            int32_t tkey = kEmpty;
+            A tacc = A(0);
+            uint32_t tfirst = 0;
+            int K = 0;                  // register entries in use (warp-uniform)
+            bool hashed = est > 32;     // use the shared hash
+            int ntouched = 0;
+            bool overflow = false;
+            for (int base = 0; base < d && !overflow; base += 32 * U) {
+                int32_t labv[U];
+                A wv[U];
+#pragma unroll
+                for (int c = 0; c < U; ++c) {
+                    const int k = base + c * 32 + lane;
+                    labv[c] = (k < d) ? read_label(a, nbr_next[c], thr) : kEmpty;
+                    wv[c] = (k < d) ? arc_weight<WM>(a, beg + k) : A(0);
+                }
+                LP_WARP_PREFETCH(base);
+#pragma unroll
+                for (int c = 0; c < U; ++c) {
+                    if (base + c * 32 >= d) break;  // warp-uniform
+                    const int k0 = base + c * 32;
+                    int32_t lab = labv[c];
+                    if (!hashed) {
+                        uint32_t pending = __ballot_sync(0xffffffffu, lab != kEmpty);
+                        for (int t = 0; t < K && pending; ++t) {
+                            const int32_t key = __shfl_sync(0xffffffffu, tkey, t);
+                            const uint32_t m = __ballot_sync(0xffffffffu, lab == key) & pending;
+                            if (m) {
+                                pending &= ~m;
+                                A add;
+                                if constexpr (WM == kUnit)
+                                    add = (A)__popc(m);
+                                else
+                                    add = masked_sum<A>(m, wv[c]);
+                                if (lane == t) tacc += add;
+                            }
+                        }
+                        while (pending && K < 32) {
+                            const int leader = __ffs(pending) - 1;
+                            const int32_t key = __shfl_sync(0xffffffffu, lab, leader);
+                            const uint32_t m = __ballot_sync(0xffffffffu, lab == key) & pending;
+                            pending &= ~m;
+                            A add;
+                            if constexpr (WM == kUnit)
+                                add = (A)__popc(m);
+                            else
+                                add = masked_sum<A>(m, wv[c]);
+                            if (lane == K) {
+                                tkey = key;
+                                tacc = add;
+                                tfirst = (uint32_t)(k0 + leader);
+                            }
+                            ++K;
+                        }
+                        if (!pending) continue;
+                        // more than 32 distinct labels: move the register table
+                        // to the shared hash, insert the rest of the chunk there
+                        bool isnew = false;
+                        int h = -1;
+                        if (lane < K) h = tab->t.add(tkey, tacc, isnew);
+                        const uint32_t nb = __ballot_sync(0xffffffffu, isnew);
+                        if (isnew) tab->touched[__popc(nb & lanemask_lt())] = (uint16_t)h;
+                        ntouched = __popc(nb);
+                        __syncwarp();
+                        hashed = true;
+                        if (!((pending >> lane) & 1u)) lab = kEmpty;
+                    }
+                    bool full = false;
+                    const int h = insert_chunk<WM, kWarpBits>(tab->t, lab, wv[c], agg, full);
+                    const uint32_t nb = __ballot_sync(0xffffffffu, h >= 0);
+                    if (h >= 0) {
+                        const int idx = ntouched + __popc(nb & lanemask_lt());
+                        if (idx < kWarpCap + 32) tab->touched[idx] = (uint16_t)h;
+                    }
+                    ntouched += __popc(nb);
+                    __syncwarp();
+                    if (ntouched > kWarpCap || __any_sync(0xffffffffu, full)) {
+                        overflow = true;
+                        break;
+                    }
+                }
+            }
+            if (overflow) {
+                // too many distinct labels for this table: wipe it and hand the
+                // vertex to the team kernel (launched after this one); the
+                // prefetched block may be this row's, refetch the next vertex's
+                for (int h = lane; h < HB; h += 32) tab->t.init(h);
+                if (lane == 0) {
+                    if (WC == 0 && d <= WarpClass<1>::kMaxDeg) {
+                        // next class up: the big-table warp kernel runs after this one
+                        const int idx = atomicAdd(a.r.len + kLenWarpBig, 1);
+                        a.r.warp[1][idx] = s;
+                    } else {
+                        const int idx = atomicAdd(a.r.len + kLenTeam, 1);
+                        Item t = {s, 0, 1, 0, 1, -1, 0, 0};
+                        a.r.team[idx] = t;
+                    }
+                    a.ndist[s] = max(nd_count(nd), 2 * WarpClass<WC>::kEst);
+                }
+                __syncwarp();
+                LP_WARP_PREFETCH(d);
+                continue;
+            }
+            int32_t winner;
+            A wbest;
+            if (!hashed) {
+                Cand<A> best = none_cand<A>();
+                if (lane < K) best = make_cand<TIE, A>(tacc, tkey, tfirst, a.seed, a.sweep, vtx);
+                // only the first K lanes hold entries: reduce over the smallest power of two >= K
+                for (int m = 16; m >= 1; m >>= 1) {
+                    if (m >= K) continue;  // warp-uniform
+                    Cand<A> o;
+                    o.w = shfl_xor_any(best.w, m);
+                    o.sec = __shfl_xor_sync(0xffffffffu, best.sec, m);
+                    o.ter = __shfl_xor_sync(0xffffffffu, best.ter, m);
+                    o.lab = __shfl_xor_sync(0xffffffffu, best.lab, m);
+                    if (better(o, best)) best = o;
+                }
+                winner = __shfl_sync(0xffffffffu, best.lab, 0);
+                wbest = best.w;  // valid in lane 0
+            } else {
+                const Best<A> b = table_argmax<WM, TIE, kWarpBits, 1>(tab->t, tab->touched, ntouched, lane, a.seed,
+                                                                     a.sweep, vtx, nullptr);
+                winner = b.lab;
+                wbest = b.w;
+                if (b.mult > 1) {
+                    // several labels tie at the maximum: the earliest in scan order wins
+                    winner = -1;
+                    for (int base = 0; base < d && winner < 0; base += 32) {
+                        const int k = base + lane;
+                        bool ok = false;
+                        int32_t lab = kEmpty;
+                        if (k < d) {
+                            lab = read_label(a, __ldg(a.snbr + beg + k), thr);
+                            const int h = tab->t.find(lab);
+                            ok = h >= 0 && tab->t.weight(h) == b.w && sec_of<TIE>(lab, a.seed, a.sweep, vtx) == b.sec;
+                        }
+                        const uint32_t hit = __ballot_sync(0xffffffffu, ok);
+                        if (hit) winner = __shfl_sync(0xffffffffu, lab, __ffs(hit) - 1);
+                    }
+                }
+                __syncwarp();
+                for (int t = lane; t < ntouched; t += 32) tab->t.init(tab->touched[t]);
+                __syncwarp();
+            }
+            bool changed = false;
+            if (lane == 0) {
+                arcs += d;
+                ++verts;
+                const bool maj = WM != kFloat && wbest + wbest > total;
+                a.ndist[s] = (hashed ? ntouched : K) | (maj ? kMajBit : 0);
+                changed = commit_label(a, p, winner, dchg, writes);
+            }
+            changed = __shfl_sync(0xffffffffu, changed, 0);
+            if (changed && a.mark) mark_row(a, beg, d, thr, lane, 32);
+        }
+    }
+    flush_counters(a, dchg, arcs, writes, verts);
+}
+
+// ---------------------------------------------------------------------------
+// block (team) per work item
+// ---------------------------------------------------------------------------
+template <int WM, int TBITS> struct TeamTable {
+    static constexpr int HB = 1 << TBITS;
+    static constexpr int CAP = HB / 4 * 3;  // touched capacity; beyond it = overflow
+    STable<WM, TBITS> t;
+    uint16_t touched[CAP];
+};
+
+template <typename A> __device__ __forceinline__ unsigned long long to_bits(A w) {
+    if constexpr (std::is_same<A, float>::value)
+        return (unsigned long long)__float_as_uint(w);
+    else
+        return (unsigned long long)w;
+}
+template <typename A> __device__ __forceinline__ A from_bits(unsigned long long b) {
+    if constexpr (std::is_same<A, float>::value)
+        return __uint_as_float((uint32_t)b);
+    else
+        return (A)b;
+}
+
 template <typename A> __device__ __forceinline__ void gacc_add(unsigned long long* acc, A w) {
     if constexpr (std::is_same<A, float>::value)
         atomicAdd(reinterpret_cast<float*>(acc), w);
@@ -632,9 +1033,9 @@ template <typename A> __device__ __forceinline__ A gacc_read(const unsigned long
 }
 
 template <int WM, int TIE, int NT, int TBITS, bool DYNAMIC>
-__global__ void __launch_bounds__(NT) k_team(EvalArgs a, int which) {
+__global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int which) {
     using A = typename Acc<WM>::T;
-    using Tab = TeamTable<A, TBITS>;
+    using Tab = TeamTable<WM, TBITS>;
     constexpr int HB = Tab::HB;
     constexpr int CAP = Tab::CAP;
     constexpr int NW = NT / 32;
@@ -648,24 +1049,144 @@ __global__ void __launch_bounds__(NT) k_team(EvalArgs a, int which) {
     __shared__ int32_t s_flag;
     __shared__ int32_t s_last;
     __shared__ int32_t s_gnew;
+    __shared__ int32_t s_full;
     __shared__ int32_t s_sp;
+    __shared__ unsigned long long s_first;  // (position << 32) | label of the earliest tied arc
     __shared__ uint32_t s_stack[STACK][2];  // (parts, want)
-    __shared__ Cand<A> s_red[NW];
+    __shared__ Best<A> s_red[NW];
+    __shared__ A s_cw[NW];
+    __shared__ ArgmaxScratch s_arg;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    for (int h = tid; h < HB; h += NT) {
-        tab->keys[h] = kEmpty;
-        tab->acc[h] = A(0);
-        tab->first[h] = 0xffffffffu;
-    }
+    for (int h = tid; h < HB; h += NT) tab->t.init(h);
     const Item* items = which == kLenHub ? a.r.hub : a.r.team;
     const int cursor = which == kLenHub ? kHubCursor : kTeamCursor;
     long long dchg = 0, arcs = 0, writes = 0, verts = 0;
     int32_t it = blockIdx.x;
     __syncthreads();
     const int32_t cnt = a.r.len[which];
+
+    auto block_merge = [&](Best<A> b) -> Best<A> {
+        b = warp_merge(b);
+        if (lane == 0) s_red[warp] = b;
+        __syncthreads();
+        Best<A> r = lane < NW ? s_red[lane] : none_best<A>();
+        r = warp_merge(r);
+        __syncthreads();
+        return r;
+    };
+
+    // Best label of row arcs [0, d) restricted to label partitions taken from
+    // the work stack (preloaded by the caller).  Sub-splits on overflow.
+    // `single`: one whole-row pass (no first position needed unless tied).
+    auto row_best = [&](const uint32_t beg, const int d, const int32_t thr, const uint32_t vtx, bool single,
+                        bool agg, int& distinct) -> Best<A> {
+        Best<A> overall = none_best<A>();
+        distinct = 0;
+        while (true) {
+            const int sp = s_sp;
+            if (sp == 0) break;
+            const uint32_t parts = s_stack[sp - 1][0], want = s_stack[sp - 1][1];
+            __syncthreads();
+            if (tid == 0) {
+                s_sp = sp - 1;
+                s_nt = 0;
+                s_full = 0;
+            }
+            __syncthreads();
+            for (int base = warp * 32 * U; base < d; base += NT * U) {
+                int32_t labv[U];
+                A wv[U];
+#pragma unroll
+                for (int c = 0; c < U; ++c) {
+                    const int k = base + c * 32 + lane;
+                    int32_t lab = kEmpty;
+                    A w = A(0);
+                    if (k < d) {
+                        lab = read_label(a, __ldg(a.snbr + beg + k), thr);
+                        w = arc_weight<WM>(a, beg + k);
+                        if (parts > 1 && part_of(lab, parts) != want) lab = kEmpty;
+                    }
+                    labv[c] = lab;
+                    wv[c] = w;
+                }
+#pragma unroll
+                for (int c = 0; c < U; ++c) {
+                    bool full = false;
+                    const int h = insert_chunk<WM, TBITS>(tab->t, labv[c], wv[c], agg, full);
+                    const uint32_t nb = __ballot_sync(0xffffffffu, h >= 0);
+                    if (nb) {
+                        int b0 = 0;
+                        if (lane == 0) b0 = atomicAdd(&s_nt, __popc(nb));
+                        b0 = __shfl_sync(0xffffffffu, b0, 0);
+                        const int idx = b0 + __popc(nb & lanemask_lt());
+                        if (h >= 0 && idx < CAP) tab->touched[idx] = (uint16_t)h;
+                    }
+                    if (__any_sync(0xffffffffu, full) && lane == 0) s_full = 1;
+                }
+                if (__shfl_sync(0xffffffffu, *(volatile int32_t*)&s_nt, 0) > CAP ||
+                    __shfl_sync(0xffffffffu, *(volatile int32_t*)&s_full, 0))
+                    break;  // overflowing
+            }
+            __syncthreads();
+            const int nt = s_nt;
+            const bool overflow = nt > CAP || s_full;
+            if (overflow) {
+                for (int h = tid; h < HB; h += NT) tab->t.init(h);
+                __syncthreads();
+                if (tid == 0) {
+                    for (int j = 3; j >= 0; --j) {
+                        s_stack[s_sp][0] = parts * 4;
+                        s_stack[s_sp][1] = want * 4 + j;
+                        ++s_sp;
+                    }
+                }
+                single = false;
+                __syncthreads();
+                continue;
+            }
+            Best<A> b = table_argmax<WM, TIE, TBITS, NW>(tab->t, tab->touched, nt, tid, a.seed, a.sweep, vtx, &s_arg);
+            const bool last_pass = single && s_sp == 0;
+            if (b.mult > 1 || !last_pass) {
+                // earliest arc (scan order) whose label carries the pass maximum
+                if (tid == 0) s_first = ~0ull;
+                __syncthreads();
+                for (int base = warp * 32; base < d; base += NT) {
+                    const unsigned long long seen = __shfl_sync(0xffffffffu, *(volatile unsigned long long*)&s_first, 0);
+                    if ((unsigned long long)base > (seen >> 32)) break;  // an earlier hit exists
+                    const int k = base + lane;
+                    bool ok = false;
+                    int32_t lab = kEmpty;
+                    if (k < d) {
+                        lab = read_label(a, __ldg(a.snbr + beg + k), thr);
+                        if (parts <= 1 || part_of(lab, parts) == want) {
+                            const int h = tab->t.find(lab);
+                            ok = h >= 0 && tab->t.weight(h) == b.w &&
+                                 sec_of<TIE>(lab, a.seed, a.sweep, vtx) == b.sec;
+                        }
+                    }
+                    const uint32_t hit = __ballot_sync(0xffffffffu, ok);
+                    if (hit) {
+                        const int j = __ffs(hit) - 1;
+                        if (lane == j) atomicMin(&s_first, ((unsigned long long)k << 32) | (uint32_t)lab);
+                        break;
+                    }
+                }
+                __syncthreads();
+                const unsigned long long f = s_first;
+                b.lab = (int32_t)(uint32_t)f;
+                b.ter = ~(uint32_t)(f >> 32);
+                b.mult = 1;
+            }
+            merge_best(overall, b);
+            distinct += nt;
+            for (int t = tid; t < nt; t += NT) tab->t.init(tab->touched[t]);
+            __syncthreads();
+        }
+        return overall;
+    };
 
     while (true) {
         if (DYNAMIC) {
@@ -679,281 +1200,192 @@ __global__ void __launch_bounds__(NT) k_team(EvalArgs a, int which) {
         const int32_t p = __ldg(a.spos + s);
         const uint32_t beg = __ldg(a.soff + s);
         const int d = (int)(__ldg(a.soff + s + 1) - beg);
-        const int32_t thr = (p / a.bs) * a.bs;
+        const int32_t thr = batch_start(a, p);
         const uint32_t vtx = (TIE == kRandom) ? (uint32_t)__ldg(a.vid + p) : 0u;
-        const int k_lo = (int)((long long)d * item.r / item.R);
-        const int k_hi = (int)((long long)d * (item.r + 1) / item.R);
-        const bool sliced = item.R > 1;
-        int32_t* gkeys = sliced ? a.r.gkeys + item.gt : nullptr;
-        uint32_t* gfirst = sliced ? a.r.gfirst + item.gt : nullptr;
-        unsigned long long* gacc = sliced ? a.r.gacc + item.gt : nullptr;
-        Cand<A> best = none_cand<A>();
-        int distinct = 0;
-        if (tid == 0) {
-            s_sp = 1;
-            s_stack[0][0] = (uint32_t)item.P;
-            s_stack[0][1] = (uint32_t)item.q;
-            s_gnew = 0;
+        const int32_t nd = __ldg(a.ndist + s);
+        A total;
+        if constexpr (WM == kUnit)
+            total = (A)d;
+        else if constexpr (WM == kFixed)
+            total = (A)__ldg(a.swsum + s);
+        else
+            total = A(0);
+        // ---- majority check for whole-row items of flagged vertices ----
+        if (WM != kFloat && item.P == 1 && item.R == 1 && (nd & kMajBit)) {
+            const int32_t cand = a.x[p];
+            A cw = A(0);
+            for (int base = warp * 32 * U; base < d; base += NT * U) {
+                int32_t labv[U];
+#pragma unroll
+                for (int c = 0; c < U; ++c) {
+                    const int k = base + c * 32 + lane;
+                    labv[c] = (k < d) ? read_label(a, __ldg(a.snbr + beg + k), thr) : kEmpty;
+                }
+#pragma unroll
+                for (int c = 0; c < U; ++c) {
+                    const int k = base + c * 32 + lane;
+                    if (k < d && labv[c] == cand) cw += arc_weight<WM>(a, beg + k);
+                }
+            }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) cw += shfl_xor_any(cw, o);
+            if (lane == 0) s_cw[warp] = cw;
+            __syncthreads();
+            A tot_cw = A(0);
+#pragma unroll
+            for (int w2 = 0; w2 < NW; ++w2) tot_cw += s_cw[w2];
+            __syncthreads();
+            if (tot_cw + tot_cw > total) {  // strict majority: the label stays
+                if (tid == 0) {
+                    arcs += d;
+                    ++verts;
+                }
+                if (!DYNAMIC) it += gridDim.x;
+                continue;
+            }
         }
-        __syncthreads();
-
-        // ---- tally this item's arcs; the work stack splits overflowing passes ----
-        while (true) {
-            const int sp = s_sp;
-            if (sp == 0) break;
-            const uint32_t parts = s_stack[sp - 1][0], want = s_stack[sp - 1][1];
+        const int est = min(d, nd_count(nd) + (nd_count(nd) >> 2) + 16);
+        const bool agg = true;
+        Best<A> best = none_best<A>();
+        int distinct = 0;
+        bool last = true;
+        if (item.R == 1) {
+            if (tid == 0) {
+                s_sp = 1;
+                s_stack[0][0] = (uint32_t)item.P;
+                s_stack[0][1] = (uint32_t)item.q;
+            }
+            __syncthreads();
+            best = row_best(beg, d, thr, vtx, item.P == 1, agg, distinct);
+            if (item.P > 1) {
+                // the last partition block merges the P candidates
+                if (tid == 0) {
+                    HubCand hc;
+                    hc.w = to_bits<A>(best.w);
+                    hc.sec = best.sec;
+                    hc.ter = best.ter;
+                    hc.lab = best.lab;
+                    hc.nd = distinct;
+                    a.r.cand[item.cb + item.q] = hc;
+                    __threadfence();
+                    s_last = atomicAdd(a.r.cand_done + item.cb, 1) == item.P - 1;
+                    if (s_last) {
+                        __threadfence();
+                        distinct = 0;
+                        best = none_best<A>();
+                        for (int j = 0; j < item.P; ++j) {
+                            const HubCand* src = a.r.cand + item.cb + j;
+                            Best<A> o;
+                            o.w = from_bits<A>(__ldcg(&src->w));
+                            o.sec = __ldcg(&src->sec);
+                            o.ter = __ldcg(&src->ter);
+                            o.lab = __ldcg(&src->lab);
+                            o.mult = 1;
+                            distinct += __ldcg(&src->nd);
+                            merge_best(best, o);
+                        }
+                        a.r.cand_done[item.cb] = 0;
+                    }
+                }
+                __syncthreads();
+                last = s_last;
+            }
+        } else {
+            // ---- arc slice: fold this slice into the per-vertex global table ----
+            const int k_lo = (int)((long long)d * item.r / item.R);
+            const int k_hi = (int)((long long)d * (item.r + 1) / item.R);
+            int32_t* gkeys = a.r.gkeys + item.gt;
+            uint32_t* gfirst = a.r.gfirst + item.gt;
+            unsigned long long* gacc = a.r.gacc + item.gt;
+            if (tid == 0) s_gnew = 0;
+            __syncthreads();
+            for (int base = k_lo + warp * 32; base < k_hi; base += NT) {
+                const int k = base + lane;
+                int32_t lab = kEmpty;
+                A w = A(0);
+                if (k < k_hi) {
+                    lab = read_label(a, __ldg(a.snbr + beg + k), thr);
+                    w = arc_weight<WM>(a, beg + k);
+                }
+                const uint32_t grp = __match_any_sync(0xffffffffu, lab);
+                const int leader = __ffs(grp) - 1;
+                int g = -1;
+                bool isnew = false;
+                if (lab != kEmpty && lane == leader) {
+                    g = table_slot(gkeys, lab, kGlobalBits, isnew);
+                    if (g >= 0) {
+                        atomicMin(gfirst + g, (uint32_t)k);
+                        if constexpr (WM == kUnit) gacc_add<A>(gacc + g, (A)__popc(grp));
+                    } else {
+                        atomicAdd(&s_gnew, 1 << 20);  // table full
+                    }
+                    if (isnew) atomicAdd(&s_gnew, 1);
+                }
+                if constexpr (WM != kUnit) {
+                    const int gb = __shfl_sync(0xffffffffu, g, leader);
+                    if (lab != kEmpty && gb >= 0) gacc_add<A>(gacc + gb, w);
+                }
+            }
             __syncthreads();
             if (tid == 0) {
-                s_sp = sp - 1;
-                s_nt = 0;
-            }
-            __syncthreads();
-            for (int base = k_lo + warp * 32 * U; base < k_hi; base += NT * U) {
-                int32_t labv[U];
-                A wv[U];
-#pragma unroll
-                for (int c = 0; c < U; ++c) {
-                    const int k = base + c * 32 + lane;
-                    int32_t lab = kEmpty;
-                    A w = A(0);
-                    if (k < k_hi) {
-                        lab = read_label(a, __ldg(a.snbr + beg + k), thr);
-                        w = arc_weight<WM>(a, beg + k);
-                        if (parts > 1 && part_of(lab, parts) != want) lab = kEmpty;
-                    }
-                    labv[c] = lab;
-                    wv[c] = w;
-                }
-#pragma unroll
-                for (int c = 0; c < U; ++c) {
-                    const int k = base + c * 32 + lane;
-                    const int32_t lab = labv[c];
-                    const uint32_t grp = __match_any_sync(0xffffffffu, lab);
-                    const int leader = __ffs(grp) - 1;
-                    int h = -1;
-                    bool isnew = false;
-                    if (lab != kEmpty && lane == leader) {
-                        h = table_slot(tab->keys, lab, TBITS, isnew);
-                        if (h >= 0) {
-                            atomicMin(&tab->first[h], (uint32_t)k);
-                            if constexpr (WM == kUnit) atomicAdd(&tab->acc[h], (A)__popc(grp));
-                        }
-                    }
-                    if constexpr (WM != kUnit) {
-                        const int hb = __shfl_sync(0xffffffffu, h, leader);
-                        if (lab != kEmpty && hb >= 0) atomicAdd(&tab->acc[hb], wv[c]);
-                    }
-                    const uint32_t nb = __ballot_sync(0xffffffffu, isnew);
-                    if (nb) {
-                        int b0 = 0;
-                        if (lane == 0) b0 = atomicAdd(&s_nt, __popc(nb));
-                        b0 = __shfl_sync(0xffffffffu, b0, 0);
-                        const int idx = b0 + __popc(nb & lanemask_lt());
-                        if (isnew && idx < CAP) tab->touched[idx] = (uint16_t)h;
-                    }
-                }
-                if (__shfl_sync(0xffffffffu, *(volatile int32_t*)&s_nt, 0) > CAP) break;  // overflowing
-            }
-            __syncthreads();
-            const int nt = s_nt;
-            const bool overflow = nt > CAP;
-            if (!overflow) {
-                // fold the touched entries into the candidate or the global slice table; wipe them
-                for (int t = tid; t < nt; t += NT) {
-                    const int h = tab->touched[t];
-                    const int32_t key = tab->keys[h];
-                    if (sliced) {
-                        bool isnew = false;
-                        const int g = table_slot(gkeys, key, kGlobalBits, isnew);
-                        if (g >= 0) {
-                            atomicMin(gfirst + g, tab->first[h]);
-                            gacc_add<A>(gacc + g, tab->acc[h]);
-                        }
-                        if (isnew || g < 0) atomicAdd(&s_gnew, g < 0 ? (1 << 20) : 1);
-                    } else {
-                        Cand<A> c = make_cand<TIE, A>(tab->acc[h], key, tab->first[h], a.seed, a.sweep, vtx);
-                        if (better(c, best)) best = c;
-                    }
-                    tab->keys[h] = kEmpty;
-                    tab->acc[h] = A(0);
-                    tab->first[h] = 0xffffffffu;
-                }
-                distinct += nt;
-            } else {
-                for (int h = tid; h < HB; h += NT) {
-                    tab->keys[h] = kEmpty;
-                    tab->acc[h] = A(0);
-                    tab->first[h] = 0xffffffffu;
-                }
-            }
-            __syncthreads();
-            if (overflow && tid == 0) {
-                for (int j = 3; j >= 0; --j) {
-                    s_stack[s_sp][0] = parts * 4;
-                    s_stack[s_sp][1] = want * 4 + j;
-                    ++s_sp;
-                }
-            }
-            __syncthreads();
-        }
-
-        // ---- merge ----
-        // block reduce of this item's candidate (all threads get it)
-        best = warp_best(best);
-        if (lane == 0) s_red[warp] = best;
-        __syncthreads();
-        best = warp_best(lane < NW ? s_red[lane] : none_cand<A>());
-        if (tid == 0) {
-            s_flag = 0;
-            s_last = 1;
-            if (sliced) {
                 if (s_gnew) atomicAdd(a.r.gcount + item.cb, s_gnew);
                 __threadfence();
                 s_last = atomicAdd(a.r.cand_done + item.cb, 1) == item.R - 1;
                 if (s_last) __threadfence();
-            } else if (item.P > 1) {
-                HubCand hc;
-                hc.w = to_bits<A>(best.w);
-                hc.sec = best.sec;
-                hc.ter = best.ter;
-                hc.lab = best.lab;
-                hc.nd = distinct;
-                a.r.cand[item.cb + item.q] = hc;
-                __threadfence();
-                s_last = atomicAdd(a.r.cand_done + item.cb, 1) == item.P - 1;
-                if (s_last) {
-                    __threadfence();
-                    distinct = 0;
-                    best = none_cand<A>();
-                    for (int j = 0; j < item.P; ++j) {
-                        const HubCand* src = a.r.cand + item.cb + j;
-                        Cand<A> o;
-                        o.w = from_bits<A>(__ldcg(&src->w));
-                        o.sec = __ldcg(&src->sec);
-                        o.ter = __ldcg(&src->ter);
-                        o.lab = __ldcg(&src->lab);
-                        distinct += __ldcg(&src->nd);
-                        if (better(o, best)) best = o;
-                    }
-                    a.r.cand_done[item.cb] = 0;
-                }
-            }
-        }
-        __syncthreads();
-        if (sliced && s_last) {
-            // last slice: argmax over the per-vertex global table, then wipe it
-            const int gcount = __ldcg(a.r.gcount + item.cb);
-            best = none_cand<A>();
-            if (gcount <= kGlobalCap) {
-                for (int g = tid; g < GHB; g += NT) {
-                    const int32_t key = __ldcg(gkeys + g);
-                    if (key == kEmpty) continue;
-                    Cand<A> c = make_cand<TIE, A>(gacc_read<A>(gacc + g), key, __ldcg(gfirst + g), a.seed, a.sweep, vtx);
-                    if (better(c, best)) best = c;
-                }
-            }
-            for (int g = tid; g < GHB; g += NT) {
-                gkeys[g] = kEmpty;
-                gfirst[g] = 0xffffffffu;
-                gacc[g] = 0ull;
-            }
-            best = warp_best(best);
-            __syncthreads();
-            if (lane == 0) s_red[warp] = best;
-            __syncthreads();
-            best = warp_best(lane < NW ? s_red[lane] : none_cand<A>());
-            if (tid == 0) {
-                distinct = gcount;
-                a.r.cand_done[item.cb] = 0;
-                a.r.gcount[item.cb] = 0;
-                if (gcount > kGlobalCap) s_last = 2;  // global table overflowed: redo whole row below
             }
             __syncthreads();
-            if (s_last == 2) {
-                // rare slow path: this block recomputes the whole row with the
-                // splitting stack (labels were underestimated)
-                if (tid == 0) {
-                    s_sp = 1;
-                    s_stack[0][0] = 4;
-                    s_stack[0][1] = 0;
-                    s_stack[1][0] = 4;
-                    s_stack[1][1] = 1;
-                    s_stack[2][0] = 4;
-                    s_stack[2][1] = 2;
-                    s_stack[3][0] = 4;
-                    s_stack[3][1] = 3;
-                    s_sp = 4;
-                }
-                __syncthreads();
-                best = none_cand<A>();
-                distinct = 0;
-                while (true) {
-                    const int sp = s_sp;
-                    if (sp == 0) break;
-                    const uint32_t parts = s_stack[sp - 1][0], want = s_stack[sp - 1][1];
-                    __syncthreads();
-                    if (tid == 0) {
-                        s_sp = sp - 1;
-                        s_nt = 0;
-                    }
-                    __syncthreads();
-                    for (int base = warp * 32; base < d; base += NT) {
-                        const int k = base + lane;
-                        int32_t lab = kEmpty;
-                        A w = A(0);
-                        if (k < d) {
-                            lab = read_label(a, __ldg(a.snbr + beg + k), thr);
-                            w = arc_weight<WM>(a, beg + k);
-                            if (part_of(lab, parts) != want) lab = kEmpty;
-                        }
-                        bool isnew = false;
-                        int h = -1;
-                        if (lab != kEmpty) {
-                            h = table_slot(tab->keys, lab, TBITS, isnew);
-                            if (h >= 0) {
-                                atomicMin(&tab->first[h], (uint32_t)k);
-                                atomicAdd(&tab->acc[h], w);
-                            }
-                            if (isnew) atomicAdd(&s_nt, 1);
-                        }
-                        if (__shfl_sync(0xffffffffu, *(volatile int32_t*)&s_nt, 0) > CAP) break;
-                    }
-                    __syncthreads();
-                    const bool overflow = s_nt > CAP;
-                    // (slow path: full-table scan instead of a touched list)
-                    for (int h = tid; h < HB; h += NT) {
-                        const int32_t key = tab->keys[h];
+            last = s_last;
+            if (last) {
+                const int gcount = __ldcg(a.r.gcount + item.cb);
+                Best<A> b = none_best<A>();
+                if (gcount <= kGlobalCap) {
+                    for (int g = tid; g < GHB; g += NT) {
+                        const int32_t key = __ldcg(gkeys + g);
                         if (key == kEmpty) continue;
-                        if (!overflow) {
-                            Cand<A> c = make_cand<TIE, A>(tab->acc[h], key, tab->first[h], a.seed, a.sweep, vtx);
-                            if (better(c, best)) best = c;
-                        }
-                        tab->keys[h] = kEmpty;
-                        tab->acc[h] = A(0);
-                        tab->first[h] = 0xffffffffu;
+                        Best<A> c;
+                        c.w = gacc_read<A>(gacc + g);
+                        c.lab = key;
+                        c.sec = sec_of<TIE>(key, a.seed, a.sweep, vtx);
+                        c.ter = ~__ldcg(gfirst + g);
+                        c.mult = 1;
+                        merge_best(b, c);
                     }
-                    if (!overflow) distinct += s_nt;
-                    __syncthreads();
-                    if (overflow && tid == 0) {
-                        for (int j = 3; j >= 0; --j) {
-                            s_stack[s_sp][0] = parts * 4;
-                            s_stack[s_sp][1] = want * 4 + j;
-                            ++s_sp;
-                        }
-                    }
-                    __syncthreads();
                 }
-                best = warp_best(best);
-                if (lane == 0) s_red[warp] = best;
-                __syncthreads();
-                best = warp_best(lane < NW ? s_red[lane] : none_cand<A>());
+                for (int g = tid; g < GHB; g += NT) {
+                    gkeys[g] = kEmpty;
+                    gfirst[g] = 0xffffffffu;
+                    gacc[g] = 0ull;
+                }
+                best = block_merge(b);
+                distinct = gcount;
+                if (tid == 0) {
+                    a.r.cand_done[item.cb] = 0;
+                    a.r.gcount[item.cb] = 0;
+                }
+                if (gcount > kGlobalCap) {
+                    // rare slow path: labels were underestimated; this block
+                    // redoes the whole row in four label partitions (or more)
+                    if (tid == 0) {
+                        for (int j = 0; j < 4; ++j) {
+                            s_stack[j][0] = 4;
+                            s_stack[j][1] = (uint32_t)j;
+                        }
+                        s_sp = 4;
+                    }
+                    __syncthreads();
+                    best = row_best(beg, d, thr, vtx, false, false, distinct);
+                }
             }
         }
-        if (tid == 0 && s_last) {
-            arcs += d;
-            ++verts;
-            a.ndist[s] = distinct;
-            s_flag = commit_label(a, p, best.lab, dchg, writes) ? 1 : 0;
+        if (tid == 0) {
+            s_flag = 0;
+            if (last) {
+                arcs += d;
+                ++verts;
+                const bool maj = WM != kFloat && best.w + best.w > total;
+                a.ndist[s] = distinct | (maj ? kMajBit : 0);
+                s_flag = commit_label(a, p, best.lab, dchg, writes) ? 1 : 0;
+            }
         }
         __syncthreads();
         if (s_flag && a.mark) mark_row(a, beg, d, thr, tid, NT);
@@ -962,7 +1394,9 @@ __global__ void __launch_bounds__(NT) k_team(EvalArgs a, int which) {
     flush_counters(a, dchg, arcs, writes, verts);
 }
 
-template <typename A> constexpr size_t warp_smem_bytes() { return sizeof(WarpTable<A>) * kWarpsPerBlock; }
-template <typename A, int TBITS> constexpr size_t team_smem_bytes() { return sizeof(TeamTable<A, TBITS>); }
+template <int WM, int WC> constexpr size_t warp_smem_bytes() {
+    return sizeof(WarpTable<WM, WC>) * WarpClass<WC>::kWarps;
+}
+template <int WM, int TBITS> constexpr size_t team_smem_bytes() { return sizeof(TeamTable<WM, TBITS>); }
 
 }  // namespace lp

@@ -31,3 +31,10 @@ for r in range(args.runs):
     print(f"run {r}: iterations {it} rounds {st['rounds']} kernel_ms {st['kernel_ms']:.3f} plan_ms {st['plan_ms']:.3f} "
           f"bin_ms {[round(x, 3) for x in st['bin_ms']]} bin_launches {st['bin_launches']} changed {changed.tolist()} "
           f"wall {time.perf_counter() - t:.3f}s", flush=True)
+
+import ctypes as C
+for mode in (0, 1, 2, 3, 4, 5):
+    ms = C.c_double(0)
+    _lib.check(_lib.lib().lp_calibrate(dg.handle, mode, 10, C.byref(ms)))
+    arcs = sum(1 for _ in [0])
+    print(f"calibrate mode {mode}: {ms.value * 1e3:.1f} us per pass over the active rows")
