@@ -113,7 +113,10 @@ typedef struct lp_run_stats {
     int64_t bin_arcs[4];    /* arcs scanned per bin                         */
     int64_t bin_vertices[4];/* vertex evaluations per bin                   */
     double aux_ms;          /* LP_RAK_PROFILE: routing kernels' time        */
-    int64_t reserved[4];
+    double gather_ms;       /* LP_RAK_PROFILE: phase-1 label gather time    */
+    int64_t arcs_gathered;  /* arcs whose neighbour label phase 1 gathered  */
+    int64_t gather_launches;
+    int64_t reserved[1];
 } lp_run_stats;
 
 /* Upload a CSR graph.  offsets[n+1], neighbors[m] (int64, rows sorted by

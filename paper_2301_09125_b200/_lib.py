@@ -79,7 +79,10 @@ class RunStats(C.Structure):
         ("bin_arcs", C.c_int64 * 4),
         ("bin_vertices", C.c_int64 * 4),
         ("aux_ms", C.c_double),
-        ("reserved", C.c_int64 * 4),
+        ("gather_ms", C.c_double),
+        ("arcs_gathered", C.c_int64),
+        ("gather_launches", C.c_int64),
+        ("reserved", C.c_int64 * 1),
     ]
 
     def as_dict(self) -> dict:

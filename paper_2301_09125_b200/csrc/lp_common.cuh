@@ -122,8 +122,10 @@ __device__ __forceinline__ uint32_t slot_hash(int32_t lab, uint32_t bits) {
     return ((uint32_t)lab * 0x9E3779B1u) >> (32 - bits);
 }
 // Partition of a label for multi-pass hub evaluation.
+// (A multiplicative hash independent of slot_hash's multiplier; nested:
+// part_of(l, 4P) / 4 == part_of(l, P), which the 4-way re-split relies on.)
 __device__ __forceinline__ uint32_t part_of(int32_t lab, uint32_t parts) {
-    return __umulhi(fmix32((uint32_t)lab ^ 0x5bd1e995u), parts);
+    return __umulhi((uint32_t)lab * 0x2C1B3C6Du + 0x297A2D39u, parts);
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {

@@ -44,7 +44,7 @@ using namespace lp;
 // arc but a self-loop: label fixed).
 enum Bin : int { kBinBig = 0, kBinS16 = 1, kBinS8 = 2, kBinS4 = 3, kBinIdle = 4, kNumBins = 5 };
 // per-kernel accounting slots (lp_run_stats.bin_*)
-enum KernelSlot : int { kKHub = 0, kKTeam = 1, kKWarp = 2, kKSmall = 3, kKSlots = 4 };
+enum KernelSlot : int { kKHub = 0, kKTeam = 1, kKWarp = 2, kKSmall = 3, kKSlots = 4, kKGather = 4 };
 
 #define LP_CK(call)                                                                                  \
     do {                                                                                             \
@@ -66,17 +66,18 @@ struct Plan {
     bool custom_order = false;
     uint32_t seed = 0;
     uint64_t order_hash = 0;
-    int32_t* vid = nullptr;          // position -> vertex
-    int32_t* pos = nullptr;          // vertex -> position
-    int32_t* spos = nullptr;         // slot -> position (n entries; first S active)
-    int32_t* slot_of_pos = nullptr;  // position -> slot or -1
+    int32_t* pos = nullptr;          // vertex -> visit position
+    int32_t* svid = nullptr;         // slot -> vertex (n entries; first S active)
+    int32_t* slot_of = nullptr;      // vertex -> slot or -1
     uint32_t* soff = nullptr;        // [S+1]
-    int32_t* snbr = nullptr;         // [m_active]
+    uint32_t* snbr = nullptr;        // [m_active] neighbour id << 2 | batch flags
     uint32_t* sw = nullptr;          // [m_active] or null
     unsigned long long* swsum = nullptr;  // [S] row weight totals (fixed-point mode)
     int32_t* ndist = nullptr;        // [S]
+    int32_t* lbuf = nullptr;         // [m_active] phase-1 gathered labels
     int64_t S = 0;
     int64_t m_active = 0;
+    int64_t flags_bs = -1;           // batch size the snbr flags were computed for
     int32_t bin_beg[kNumBins + 1] = {0, 0, 0, 0, 0, 0};  // slot range of each bin (idle: [.., n))
     int32_t big_end = 0;             // slots [0, big_end) are big rows, [big_end, S) small
     int64_t bytes = 0;
@@ -101,7 +102,9 @@ struct lp_graph {
     int32_t* labA = nullptr;
     int32_t* labB = nullptr;
     int32_t* cur = nullptr;  // the buffer holding the latest labels
-    uint8_t* mark = nullptr;
+    int32_t* mark = nullptr;    // frontier marks by vertex id
+    int32_t* mq[2] = {nullptr, nullptr};  // mark queues (alternate per round)
+    int32_t* mq_len = nullptr;  // their lengths [2]
     Routes routes;
     int64_t cap_items = 0;
     unsigned long long* counters = nullptr;
@@ -181,48 +184,48 @@ __global__ void k_degree_stats(const uint32_t* __restrict__ off, int64_t n, unsi
     if (sl) atomicAdd(out + 1, sl);
 }
 
-__global__ void k_plan_pos(const int64_t* __restrict__ order, int32_t* __restrict__ vid, int32_t* __restrict__ pos,
-                           int64_t n, unsigned long long* bad) {
+__global__ void k_plan_pos(const int64_t* __restrict__ order, int32_t* __restrict__ pos, int64_t n,
+                           unsigned long long* bad) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = order[p];
         if (v < 0 || v >= n) {
             atomicAdd(bad, 1ull);
             continue;
         }
-        vid[p] = (int32_t)v;
         pos[v] = (int32_t)p;
     }
 }
 
 // every vertex must own exactly one position: pos[] was preset to -1
-__global__ void k_plan_check_perm(const int32_t* __restrict__ vid, const int32_t* __restrict__ pos, int64_t n,
+__global__ void k_plan_check_perm(const int64_t* __restrict__ order, const int32_t* __restrict__ pos, int64_t n,
                                   unsigned long long* bad) {
     unsigned long long b = 0;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
         const int32_t p = pos[v];
-        b += (p < 0 || vid[p] != (int32_t)v);
+        b += (p < 0 || order[p] != v);
     }
     if (b) atomicAdd(bad, b);
 }
 
-// storage sort key: bin in bits 32..34; big rows by descending degree
-__global__ void k_plan_keys(const int32_t* __restrict__ vid, const uint32_t* __restrict__ off,
-                            const int32_t* __restrict__ nbr, unsigned long long* __restrict__ key, int64_t n,
-                            unsigned long long* counts) {
+// storage sort key per vertex: bin in bits 32..34; big rows by descending
+// degree (the dense route then hands out the largest hubs first); inside a
+// small class vertex-id order (neighbouring rows share neighbours: locality
+// for the label gathers)
+__global__ void k_plan_keys(const uint32_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                            unsigned long long* __restrict__ key, int64_t n, unsigned long long* counts) {
     __shared__ unsigned long long sc[kNumBins];
     if (threadIdx.x < kNumBins) sc[threadIdx.x] = 0;
     __syncthreads();
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t v = vid[p];
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t d = off[v + 1] - off[v];
         int b;
-        if (d == 0 || (d == 1 && nbr[off[v]] == v))
+        if (d == 0 || (d == 1 && nbr[off[v]] == (int32_t)v))
             b = kBinIdle;  // label provably cannot move
         else if (d > (uint32_t)kSmallMax)
             b = kBinBig;
         else
             b = d > 8 ? kBinS16 : (d > 4 ? kBinS8 : kBinS4);
-        key[p] = ((unsigned long long)b << 32) | (b == kBinBig ? (0xffffffffull - d) : 0ull);
+        key[v] = ((unsigned long long)b << 32) | (b == kBinBig ? (0xffffffffull - d) : 0ull);
         atomicAdd(&sc[b], 1ull);
     }
     __syncthreads();
@@ -234,17 +237,15 @@ __global__ void k_iota(int32_t* a, int64_t n) {
         a[i] = (int32_t)i;
 }
 
-__global__ void k_plan_slots(const int32_t* __restrict__ spos, const int32_t* __restrict__ vid,
-                             const uint32_t* __restrict__ off, int32_t* __restrict__ slot_of_pos,
-                             uint32_t* __restrict__ sdeg, int64_t n, int64_t S) {
+__global__ void k_plan_slots(const int32_t* __restrict__ svid, const uint32_t* __restrict__ off,
+                             int32_t* __restrict__ slot_of, uint32_t* __restrict__ sdeg, int64_t n, int64_t S) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t p = spos[s];
+        const int32_t v = svid[s];
         if (s < S) {
-            const int32_t v = vid[p];
-            slot_of_pos[p] = (int32_t)s;
+            slot_of[v] = (int32_t)s;
             sdeg[s] = off[v + 1] - off[v];
         } else {
-            slot_of_pos[p] = -1;
+            slot_of[v] = -1;
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) sdeg[S] = 0;
@@ -256,20 +257,40 @@ __global__ void k_reset_ndist(const uint32_t* __restrict__ soff, int32_t* __rest
         ndist[s] = (int32_t)(soff[s + 1] - soff[s]);
 }
 
-// one warp per slot: copy the row, translating neighbour ids to positions
-__global__ void k_plan_rows(const int32_t* __restrict__ spos, const int32_t* __restrict__ vid,
-                            const int32_t* __restrict__ pos, const uint32_t* __restrict__ off,
+// one warp per slot: copy the row (neighbour ids, flags cleared) and weights
+__global__ void k_plan_rows(const int32_t* __restrict__ svid, const uint32_t* __restrict__ off,
                             const int32_t* __restrict__ nbr, const uint32_t* __restrict__ w,
-                            const uint32_t* __restrict__ soff, int32_t* __restrict__ snbr, uint32_t* __restrict__ sw,
+                            const uint32_t* __restrict__ soff, uint32_t* __restrict__ snbr, uint32_t* __restrict__ sw,
                             int64_t S) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
     for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < S; s += warps) {
-        const int32_t v = vid[spos[s]];
+        const int32_t v = svid[s];
         const uint32_t src = off[v], d = off[v + 1] - src, dst = soff[s];
         for (uint32_t k = lane; k < d; k += 32) {
-            snbr[dst + k] = pos[nbr[src + k]];
+            snbr[dst + k] = (uint32_t)nbr[src + k] << 2;
             if (w) sw[dst + k] = w[src + k];
+        }
+    }
+}
+
+// batch flags of every arc for batch size bs: kEarlier when the neighbour's
+// batch precedes the row vertex's, kLater when it follows (bs >= n: none)
+__global__ void k_set_flags(const int32_t* __restrict__ svid, const int32_t* __restrict__ pos,
+                            const uint32_t* __restrict__ soff, uint32_t* __restrict__ snbr, int64_t S, int64_t bs,
+                            int clear_only) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
+    for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < S; s += warps) {
+        const int64_t bv = clear_only ? 0 : (int64_t)pos[svid[s]] / bs;
+        for (uint32_t e = soff[s] + lane; e < soff[s + 1]; e += 32) {
+            const uint32_t nb = snbr[e] & ~3u;
+            uint32_t f = 0;
+            if (!clear_only) {
+                const int64_t bu = (int64_t)pos[nb >> 2] / bs;
+                f = (bu < bv ? kEarlier : 0u) | (bu > bv ? kLater : 0u);
+            }
+            snbr[e] = nb | f;
         }
     }
 }
@@ -287,10 +308,9 @@ __global__ void k_plan_wsum(const uint32_t* __restrict__ soff, const uint32_t* _
     }
 }
 
-__global__ void k_init_labels(const int32_t* __restrict__ vid, const int64_t* __restrict__ init, int32_t* __restrict__ lab,
-                              int64_t n) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
-        lab[p] = init ? (int32_t)init[vid[p]] : vid[p];
+__global__ void k_init_labels(const int64_t* __restrict__ init, int32_t* __restrict__ lab, int64_t n) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        lab[v] = init ? (int32_t)init[v] : (int32_t)v;
 }
 
 __global__ void k_check_labels(const int64_t* __restrict__ init, int64_t n, unsigned long long* bad) {
@@ -300,10 +320,9 @@ __global__ void k_check_labels(const int64_t* __restrict__ init, int64_t n, unsi
     if (b) atomicAdd(bad, b);
 }
 
-__global__ void k_scatter_labels(const int32_t* __restrict__ vid, const int32_t* __restrict__ lab, int64_t* __restrict__ out,
-                                 int64_t n) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
-        out[vid[p]] = lab[p];
+__global__ void k_labels_to64(const int32_t* __restrict__ lab, int64_t* __restrict__ out, int64_t n) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        out[v] = lab[v];
 }
 
 __global__ void k_gtab_init(int32_t* keys, uint32_t* first, unsigned long long* acc, int64_t count) {
@@ -327,7 +346,7 @@ static int grid_for(int64_t work, int per_block, int cap_blocks) {
 struct Prof {
     bool on = false;
     int launches = 0;
-    int64_t slot_launches[kKSlots] = {0, 0, 0, 0};
+    int64_t slot_launches[kKSlots + 1] = {0, 0, 0, 0, 0};
     std::vector<cudaEvent_t>* pool = nullptr;
     std::vector<int> tags;  // kernel slot per pair, -1 = routing
     size_t used = 0;
@@ -400,6 +419,15 @@ template <int WM, int TIE> struct Launcher {
         const Plan& P = g->plan;
         const int sms = g->num_sms;
         cudaStream_t st = g->stream;
+        // ---- phase 1: gather every evaluated row's neighbour labels ----
+        prof->begin(st, kKGather);
+        if (dense) {
+            k_gather_dense<<<grid_for(P.m_active, 256 * 8, sms * 16), 256, 0, st>>>(a, P.m_active);
+        } else {
+            k_gather_pieces<<<grid_for(h_len[kLenGather], 32 * 8, sms * 16), 256, 0, st>>>(a);
+        }
+        prof->end(st);
+        // ---- phase 2: route and tally ----
         if (dense && P.big_end > 0) {
             prof->begin(st, -1);
             k_route_dense<<<grid_for(P.big_end, 256, sms * 8), 256, 0, st>>>(a, 0, P.big_end);
@@ -473,15 +501,15 @@ template <int WM> static void pick_fns(int tie, round_fn* r, setup_fn* s) {
 // graph handle
 // ---------------------------------------------------------------------------
 static void free_plan(Plan& P) {
-    cudaFree(P.vid);
     cudaFree(P.pos);
-    cudaFree(P.spos);
-    cudaFree(P.slot_of_pos);
+    cudaFree(P.svid);
+    cudaFree(P.slot_of);
     cudaFree(P.soff);
     cudaFree(P.snbr);
     cudaFree(P.sw);
     cudaFree(P.swsum);
     cudaFree(P.ndist);
+    cudaFree(P.lbuf);
     P = Plan();
 }
 
@@ -498,6 +526,8 @@ static void free_routes(Routes& r) {
     cudaFree(r.gfirst);
     cudaFree(r.gacc);
     cudaFree(r.gcount);
+    cudaFree(r.gslot);
+    cudaFree(r.gk0);
     r = Routes();
 }
 
@@ -505,6 +535,9 @@ static void destroy_graph(lp_graph* g) {
     if (!g) return;
     free_plan(g->plan);
     free_routes(g->routes);
+    cudaFree(g->mq[0]);
+    cudaFree(g->mq[1]);
+    cudaFree(g->mq_len);
     cudaFree(g->off);
     cudaFree(g->nbr);
     cudaFree(g->w);
@@ -557,7 +590,8 @@ struct TmpBufs {
     }
 };
 
-// Build (or reuse) the position / storage plan for a visit order.
+// Build (or reuse) the plan for a visit order: positions, the degree-binned
+// storage CSR (neighbour ids), the phase-1 label buffer.
 static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, float* plan_ms) {
     const int64_t n = g->n;
     const bool custom = order_host != nullptr;
@@ -576,10 +610,9 @@ static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, flo
     cudaStream_t st = g->stream;
     LP_CK(cudaEventRecord(g->ev0, st));
     int64_t bytes = 0;
-    LP_CK(dalloc(&P.vid, n, &bytes));
     LP_CK(dalloc(&P.pos, n, &bytes));
-    LP_CK(dalloc(&P.spos, n, &bytes));
-    LP_CK(dalloc(&P.slot_of_pos, n, &bytes));
+    LP_CK(dalloc(&P.svid, n, &bytes));
+    LP_CK(dalloc(&P.slot_of, n, &bytes));
     LP_CK(dalloc(&P.ndist, n, &bytes));
     TmpBufs t;
     int64_t tmpb = 0;
@@ -592,21 +625,21 @@ static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, flo
     LP_CK(cudaMemsetAsync(g->counters, 0, 8 * sizeof(unsigned long long), st));
     LP_CK(cudaMemsetAsync(P.pos, 0xff, n * sizeof(int32_t), st));
     const int G = g->num_sms * 8;
-    k_plan_pos<<<G, 256, 0, st>>>(t.order, P.vid, P.pos, n, g->counters);
-    k_plan_check_perm<<<G, 256, 0, st>>>(P.vid, P.pos, n, g->counters);
+    k_plan_pos<<<G, 256, 0, st>>>(t.order, P.pos, n, g->counters);
+    k_plan_check_perm<<<G, 256, 0, st>>>(t.order, P.pos, n, g->counters);
     LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     LP_CK(cudaStreamSynchronize(st));
-    if (g->h_counters[0]) {  // checked before any kernel dereferences vid[]
+    if (g->h_counters[0]) {
         free_plan(P);
         return lp_fail(LP_ERR_INVALID, "order is not a permutation of range(n)");
     }
-    k_plan_keys<<<G, 256, 0, st>>>(P.vid, g->off, g->nbr, t.key, n, g->counters + 1);
+    k_plan_keys<<<G, 256, 0, st>>>(g->off, g->nbr, t.key, n, g->counters + 1);
     k_iota<<<G, 256, 0, st>>>(t.iota, n);
     size_t need = 0, need2 = 0;
-    LP_CK(cub::DeviceRadixSort::SortPairs(nullptr, need, t.key, t.key_sorted, t.iota, P.spos, (int)n, 0, 35, st));
+    LP_CK(cub::DeviceRadixSort::SortPairs(nullptr, need, t.key, t.key_sorted, t.iota, P.svid, (int)n, 0, 35, st));
     LP_CK(cub::DeviceScan::ExclusiveSum(nullptr, need2, t.sdeg, t.sdeg, (int)(n + 1), st));
     if (int rc = ensure_cub_tmp(g, std::max(need, need2))) return rc;
-    LP_CK(cub::DeviceRadixSort::SortPairs(g->cub_tmp, need, t.key, t.key_sorted, t.iota, P.spos, (int)n, 0, 35, st));
+    LP_CK(cub::DeviceRadixSort::SortPairs(g->cub_tmp, need, t.key, t.key_sorted, t.iota, P.svid, (int)n, 0, 35, st));
     LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     LP_CK(cudaStreamSynchronize(st));
     {
@@ -619,7 +652,7 @@ static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, flo
     }
     P.big_end = P.bin_beg[kBinS16];
     P.S = P.bin_beg[kBinIdle];
-    k_plan_slots<<<G, 256, 0, st>>>(P.spos, P.vid, g->off, P.slot_of_pos, t.sdeg, n, P.S);
+    k_plan_slots<<<G, 256, 0, st>>>(P.svid, g->off, P.slot_of, t.sdeg, n, P.S);
     LP_CK(dalloc(&P.soff, P.S + 1, &bytes));
     LP_CK(cub::DeviceScan::ExclusiveSum(g->cub_tmp, need2, t.sdeg, P.soff, (int)(P.S + 1), st));
     uint32_t m_active = 0;
@@ -627,9 +660,9 @@ static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, flo
     LP_CK(cudaStreamSynchronize(st));
     P.m_active = m_active;
     LP_CK(dalloc(&P.snbr, P.m_active, &bytes));
+    LP_CK(dalloc(&P.lbuf, P.m_active, &bytes));
     if (g->w) LP_CK(dalloc(&P.sw, P.m_active, &bytes));
-    k_plan_rows<<<g->num_sms * 16, 256, 0, st>>>(P.spos, P.vid, P.pos, g->off, g->nbr, g->w, P.soff, P.snbr, P.sw,
-                                                 P.S);
+    k_plan_rows<<<g->num_sms * 16, 256, 0, st>>>(P.svid, g->off, g->nbr, g->w, P.soff, P.snbr, P.sw, P.S);
     if (g->wmode == kFixed && P.S > 0) {
         LP_CK(dalloc(&P.swsum, P.S, &bytes));
         k_plan_wsum<<<g->num_sms * 16, 256, 0, st>>>(P.soff, P.sw, P.swsum, P.S);
@@ -642,8 +675,30 @@ static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, flo
     P.custom_order = custom;
     P.seed = seed;
     P.order_hash = oh;
+    P.flags_bs = -1;
     P.bytes = bytes;
     g->bytes += bytes;
+    return LP_OK;
+}
+
+// (Re)compute the batch flags of the storage CSR for batch size bs.
+static int ensure_flags(lp_graph* g, int64_t bs, float* ms) {
+    Plan& P = g->plan;
+    const bool none = bs >= g->n;  // one batch: no cross-batch reads or marks
+    const int64_t key = none ? g->n : bs;
+    if (P.flags_bs == key) return LP_OK;
+    if (P.S > 0) {
+        LP_CK(cudaEventRecord(g->ev0, g->stream));
+        k_set_flags<<<g->num_sms * 16, 256, 0, g->stream>>>(P.svid, P.pos, P.soff, P.snbr, P.S, none ? 1 : bs,
+                                                           none ? 1 : 0);
+        LP_CK(cudaGetLastError());
+        LP_CK(cudaEventRecord(g->ev1, g->stream));
+        LP_CK(cudaEventSynchronize(g->ev1));
+        float e = 0.f;
+        LP_CK(cudaEventElapsedTime(&e, g->ev0, g->ev1));
+        *ms += e;
+    }
+    P.flags_bs = key;
     return LP_OK;
 }
 
@@ -667,6 +722,10 @@ static cudaError_t alloc_routes(lp_graph* g) {
     if ((e = dalloc(&r.gkeys, gpool, &g->bytes))) return e;
     if ((e = dalloc(&r.gfirst, gpool, &g->bytes))) return e;
     if ((e = dalloc(&r.gacc, gpool, &g->bytes))) return e;
+    // phase-1 pieces: one per row plus one per extra kPieceArcs arcs
+    const int64_t pieces = n + g->m / kPieceArcs + 1;
+    if ((e = dalloc(&r.gslot, pieces, &g->bytes))) return e;
+    if ((e = dalloc(&r.gk0, pieces, &g->bytes))) return e;
     if ((e = cudaMemsetAsync(r.cand_done, 0, g->cap_items * sizeof(int32_t), g->stream))) return e;
     if ((e = cudaMemsetAsync(r.gcount, 0, g->cap_items * sizeof(int32_t), g->stream))) return e;
     k_gtab_init<<<g->num_sms * 4, 256, 0, g->stream>>>(r.gkeys, r.gfirst, r.gacc, gpool);
@@ -678,7 +737,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (!out) return lp_fail(LP_ERR_INVALID, "out is NULL");
     *out = nullptr;
     if (n < 0 || m < 0) return lp_fail(LP_ERR_INVALID, "negative vertex or edge count");
-    if (n >= (int64_t)INT32_MAX) return lp_fail(LP_ERR_UNSUPPORTED, "vertex count must be < 2^31-1");
+    if (n >= ((int64_t)1 << 30)) return lp_fail(LP_ERR_UNSUPPORTED, "vertex count must be < 2^30");
     if (m >= (int64_t)INT32_MAX) return lp_fail(LP_ERR_UNSUPPORTED, "edge count must be < 2^31-1");
     if (n > 0 && !offsets) return lp_fail(LP_ERR_INVALID, "offsets is NULL");
     if (m > 0 && !neighbors) return lp_fail(LP_ERR_INVALID, "neighbors is NULL");
@@ -715,11 +774,14 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     G_CK(dalloc(&g->labA, n, &g->bytes));
     G_CK(dalloc(&g->labB, n, &g->bytes));
     G_CK(dalloc(&g->mark, n + 4, &g->bytes));
+    G_CK(dalloc(&g->mq[0], n + 4, &g->bytes));
+    G_CK(dalloc(&g->mq[1], n + 4, &g->bytes));
+    G_CK(dalloc(&g->mq_len, 4, &g->bytes));
     G_CK(dalloc(&g->counters, 32, &g->bytes));
     G_CK(dalloc(&g->out64, n, &g->bytes));
     G_CK(cudaMallocHost((void**)&g->h_len, kLenCount * sizeof(int32_t)));
     G_CK(cudaMallocHost((void**)&g->h_counters, 32 * sizeof(unsigned long long)));
-    G_CK(cudaMemsetAsync(g->mark, 0, n + 4, st));
+    G_CK(cudaMemsetAsync(g->mark, 0, (n + 4) * sizeof(int32_t), st));
     G_CK(cudaMemsetAsync(g->counters, 0, 32 * sizeof(unsigned long long), st));
     {
         int64_t* tmp = nullptr;
@@ -818,6 +880,10 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     }
     float plan_ms = 0.f;
     if (int rc = build_plan(g, order, o->seed, &plan_ms)) return rc;
+    const int64_t B = (o->batches == 0 || o->batches > n) ? n : o->batches;
+    const int64_t bs = (n + B - 1) / B;
+    const bool cross = bs < n;  // some vertex depends on an earlier batch
+    if (int rc = ensure_flags(g, bs, &plan_ms)) return rc;
     S->plan_ms = plan_ms;
     Plan& P = g->plan;
     cudaStream_t st = g->stream;
@@ -831,9 +897,6 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         pick_fns<kUnit>(o->tie, &run_round, &setup);
     LP_CK(setup(g->device));
 
-    const int64_t B = (o->batches == 0 || o->batches > n) ? n : o->batches;
-    const int64_t bs = (n + B - 1) / B;
-    const bool cross = bs < n;  // some vertex depends on an earlier batch
     if (labels_init) {
         int64_t* tmp = g->out64;
         LP_CK(cudaMemcpyAsync(tmp, labels_init, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
@@ -843,9 +906,9 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         LP_CK(cudaMemcpyAsync(&bad, g->counters, sizeof(bad), cudaMemcpyDeviceToHost, st));
         LP_CK(cudaStreamSynchronize(st));
         if (bad) return lp_fail(LP_ERR_INVALID, "initial labels must lie in [0, vertex_count)");
-        k_init_labels<<<g->num_sms * 8, 256, 0, st>>>(P.vid, tmp, g->labA, n);
+        k_init_labels<<<g->num_sms * 8, 256, 0, st>>>(tmp, g->labA, n);
     } else {
-        k_init_labels<<<g->num_sms * 8, 256, 0, st>>>(P.vid, nullptr, g->labA, n);
+        k_init_labels<<<g->num_sms * 8, 256, 0, st>>>(nullptr, g->labA, n);
     }
     if (P.S > 0) k_reset_ndist<<<g->num_sms * 8, 256, 0, st>>>(P.soff, P.ndist, P.S);
     LP_CK(cudaGetLastError());
@@ -857,14 +920,14 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.snbr = P.snbr;
     a.sw = P.sw;
     a.swsum = P.swsum;
-    a.spos = P.spos;
-    a.vid = P.vid;
+    a.svid = P.svid;
+    a.lbuf = P.lbuf;
     a.mark = cross ? g->mark : nullptr;
+    a.mq_out = nullptr;
+    a.mq_len = nullptr;
     a.ndist = P.ndist;
     a.counters = g->counters;
     a.r = g->routes;
-    a.bs = (int32_t)bs;
-    a.n = (int32_t)n;
     a.bin = 0;
     a.seed = o->seed;
 
@@ -875,6 +938,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     LP_CK(cudaEventRecord(g->ev0, st));
     int it = 0;
     int rounds = 0;
+    int64_t gathered = 0;
     while (it < o->max_iterations) {
         ++it;
         a.sweep = (uint32_t)it;
@@ -883,18 +947,26 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         LP_CK(cudaMemcpyAsync(X, L0, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
         LP_CK(cudaMemsetAsync(g->counters + kCtrChanged, 0, 2 * sizeof(unsigned long long), st));
         LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
+        int q = 0;  // this round's writes queue into mq[q]
+        a.mq_out = g->mq[q];
+        a.mq_len = g->mq_len + q;
+        LP_CK(cudaMemsetAsync(g->mq_len, 0, 2 * sizeof(int32_t), st));
         run_round(g, a, true, g->h_len, &prof);
+        gathered += P.m_active;
         ++rounds;
         while (cross) {
+            // route last round's queue; this round's writes queue into the other one
             LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
+            LP_CK(cudaMemsetAsync(g->mq_len + (q ^ 1), 0, sizeof(int32_t), st));
             prof.begin(st, -1);
-            k_route_marked<<<g->num_sms * 8, 256, 0, st>>>(a, g->mark, P.slot_of_pos, n);
+            k_route_queue<<<g->num_sms * 4, 256, 0, st>>>(a, g->mq[q], g->mq_len + q, P.slot_of);
             prof.end(st);
             LP_CK(cudaMemcpyAsync(g->h_len, g->routes.len, kLenCount * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
             LP_CK(cudaStreamSynchronize(st));
-            const int64_t total = (int64_t)g->h_len[kLenS4] + g->h_len[kLenS8] + g->h_len[kLenS16] +
-                                  g->h_len[kLenWarp] + g->h_len[kLenWarpBig] + g->h_len[kLenTeam] + g->h_len[kLenHub];
-            if (total == 0) break;
+            if (g->h_len[kLenGather] == 0) break;
+            q ^= 1;
+            a.mq_out = g->mq[q];
+            a.mq_len = g->mq_len + q;
             LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
             run_round(g, a, false, g->h_len, &prof);
             ++rounds;
@@ -919,6 +991,8 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     S->kernel_ms = ms;
     S->arcs_dense = g->m * it;
     S->launches = prof.launches;
+    S->arcs_gathered = gathered + (int64_t)g->h_counters[kCtrGathered];
+    S->gather_launches = prof.slot_launches[kKGather];
     for (int b = 0; b < kKSlots; ++b) {
         S->bin_arcs[b] = (int64_t)g->h_counters[kCtrArcs + b];
         S->bin_vertices[b] = (int64_t)g->h_counters[kCtrVerts + b];
@@ -928,7 +1002,9 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     for (size_t i = 0; i < prof.tags.size(); ++i) {
         float e = 0.f;
         LP_CK(cudaEventElapsedTime(&e, g->event_pool[2 * i], g->event_pool[2 * i + 1]));
-        if (prof.tags[i] >= 0)
+        if (prof.tags[i] == kKGather)
+            S->gather_ms += e;
+        else if (prof.tags[i] >= 0)
             S->bin_ms[prof.tags[i]] += e;
         else
             S->aux_ms += e;
@@ -945,7 +1021,7 @@ extern "C" int lp_labels_download(lp_graph* g, int64_t* labels_out) {
     if (!g->labels_valid) return lp_fail(LP_ERR_INVALID, "no labels: run a detection first");
     if (g->n == 0) return LP_OK;
     LP_CK(cudaSetDevice(g->device));
-    k_scatter_labels<<<g->num_sms * 8, 256, 0, g->stream>>>(g->plan.vid, g->cur, g->out64, g->n);
+    k_labels_to64<<<g->num_sms * 8, 256, 0, g->stream>>>(g->cur, g->out64, g->n);
     LP_CK(cudaMemcpyAsync(labels_out, g->out64, g->n * sizeof(int64_t), cudaMemcpyDeviceToHost, g->stream));
     LP_CK(cudaStreamSynchronize(g->stream));
     return LP_OK;
@@ -985,7 +1061,8 @@ extern "C" int lp_host_unregister(void* ptr) {
 //         pattern without any hashing) -- the practical floor of a sweep
 // mode 0/1: warp per row, plain loop (the naive structure)
 // mode 2/3: flat arc-parallel stream, 8 loads in flight per thread (the floor)
-__global__ void k_calib(const uint32_t* __restrict__ soff, const int32_t* __restrict__ snbr,
+// (the storage CSR packs neighbour id << 2; the original CSR holds plain ids)
+__global__ void k_calib(const uint32_t* __restrict__ soff, const uint32_t* __restrict__ snbr, int shift,
                         const int32_t* __restrict__ lab, int64_t S, int mode, unsigned long long* sink) {
     const int lane = threadIdx.x & 31;
     unsigned acc = 0;
@@ -994,22 +1071,22 @@ __global__ void k_calib(const uint32_t* __restrict__ soff, const int32_t* __rest
         for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < S; s += warps) {
             const uint32_t b = soff[s], e = soff[s + 1];
             for (uint32_t k = b + lane; k < e; k += 32) {
-                const int32_t u = __ldg(snbr + k);
-                acc ^= mode ? (unsigned)__ldg(lab + u) : (unsigned)u;
+                const uint32_t u = __ldg(snbr + k) >> shift;
+                acc ^= mode ? (unsigned)__ldg(lab + u) : u;
             }
         }
     } else {
         const int64_t m = soff[S];
         const int64_t stride = (int64_t)gridDim.x * blockDim.x;
         for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < m; base += stride * 8) {
-            int32_t u[8];
+            uint32_t u[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int64_t e = base + j * stride;
-                u[j] = e < m ? __ldg(snbr + e) : 0;
+                u[j] = e < m ? (__ldg(snbr + e) >> shift) : 0u;
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc ^= mode == 3 ? (unsigned)__ldg(lab + u[j]) : (unsigned)u[j];
+            for (int j = 0; j < 8; ++j) acc ^= mode == 3 ? (unsigned)__ldg(lab + u[j]) : u[j];
         }
     }
     acc = __reduce_xor_sync(0xffffffffu, acc);
@@ -1017,22 +1094,22 @@ __global__ void k_calib(const uint32_t* __restrict__ soff, const int32_t* __rest
 }
 
 extern "C" int lp_calibrate(lp_graph* g, int32_t mode, int32_t reps, double* ms_out) {
-    if (!g || !ms_out || reps < 1) return lp_fail(LP_ERR_INVALID, "bad arguments");
+    if (!g || !ms_out || reps < 1 || mode < 0 || mode > 5) return lp_fail(LP_ERR_INVALID, "bad arguments");
     if (!g->plan.valid) return lp_fail(LP_ERR_INVALID, "run a detection first (plan needed)");
     LP_CK(cudaSetDevice(g->device));
     const Plan& P = g->plan;
     cudaStream_t st = g->stream;
-    k_init_labels<<<g->num_sms * 8, 256, 0, st>>>(P.vid, nullptr, g->labA, g->n);
-    // mode 4/5: the same flat passes over the ORIGINAL CSR (neighbour ids in
-    // vertex-id order, labels indexed by vertex id)
+    k_init_labels<<<g->num_sms * 8, 256, 0, st>>>(nullptr, g->labA, g->n);
+    // mode 4/5: the same flat passes over the ORIGINAL CSR (vertex-id order)
     const uint32_t* soff = mode >= 4 ? g->off : P.soff;
-    const int32_t* snbr = mode >= 4 ? g->nbr : P.snbr;
+    const uint32_t* snbr = mode >= 4 ? (const uint32_t*)g->nbr : P.snbr;
+    const int shift = mode >= 4 ? 0 : 2;
     const int64_t rows = mode >= 4 ? g->n : P.S;
     const int km = mode >= 4 ? mode - 2 : mode;
-    k_calib<<<g->num_sms * 16, 256, 0, st>>>(soff, snbr, g->labA, rows, km, g->counters);
+    k_calib<<<g->num_sms * 16, 256, 0, st>>>(soff, snbr, shift, g->labA, rows, km, g->counters);
     LP_CK(cudaEventRecord(g->ev0, st));
     for (int r = 0; r < reps; ++r)
-        k_calib<<<g->num_sms * 16, 256, 0, st>>>(soff, snbr, g->labA, rows, km, g->counters);
+        k_calib<<<g->num_sms * 16, 256, 0, st>>>(soff, snbr, shift, g->labA, rows, km, g->counters);
     LP_CK(cudaEventRecord(g->ev1, st));
     LP_CK(cudaEventSynchronize(g->ev1));
     float ms = 0.f;

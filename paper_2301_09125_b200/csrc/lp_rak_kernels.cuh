@@ -5,6 +5,13 @@
 // neighbours' labels, take the argmax under the tie rule, write the label
 // and count the change.
 //
+// Every round has two phases.  Phase 1 (k_gather_*) streams the neighbour
+// index of every arc of the rows to evaluate and gathers that neighbour's
+// label into an arc-aligned buffer `lbuf` -- a flat, coalesced pass with
+// eight loads in flight per thread, which is what the memory system needs
+// (a warp walking one row at a time keeps too few loads in flight).
+// Phase 2 (the kernels below) tallies each row from `lbuf`, contiguously.
+//
 // Work is routed per round by the degree d and an estimate `est` of the
 // vertex's distinct neighbour labels (the count seen at its previous
 // evaluation, plus margin): label diversity collapses after the first sweep,
@@ -71,6 +78,8 @@ enum {
     kHubCursor = 9,
     kGtabCursor = 10,
     kWarpCursor = 11,  // + warp class (0 / 1)
+    kLenGather = 13,   // phase-1 pieces (row, arc range) of frontier rounds
+    kGatherCursor = 14,
     kLenCount = 16
 };
 
@@ -86,32 +95,39 @@ struct Routes {
     uint32_t* gfirst;
     unsigned long long* gacc;
     int32_t* gcount;  // distinct count per slice table (indexed by cb)
+    int32_t* gslot;   // frontier rounds: phase-1 pieces: slot ...
+    int32_t* gk0;     // ... and first arc of the piece within the row (<= kPieceArcs arcs)
 };
 
 struct EvalArgs {
     const uint32_t* __restrict__ soff;  // storage row offsets [S+1]
-    const int32_t* __restrict__ snbr;   // neighbour positions
+    const uint32_t* __restrict__ snbr;  // neighbour vertex id << 2 | kEarlier | kLater
     const uint32_t* __restrict__ sw;    // arc weights (fixed-point u32 or float bits); null = unit
     const unsigned long long* __restrict__ swsum;  // per-slot total weight (fixed mode), null otherwise
-    const int32_t* __restrict__ spos;   // slot -> position
-    const int32_t* __restrict__ vid;    // position -> vertex id
-    const int32_t* __restrict__ L0;     // labels at sweep start (read-only in a sweep)
-    int32_t* x;                         // working labels (read + written in place)
-    uint8_t* mark;                      // next-round marks by position, null = no cross-batch deps
+    const int32_t* __restrict__ svid;   // slot -> vertex id
+    const int32_t* __restrict__ L0;     // labels at sweep start, by vertex id (read-only in a sweep)
+    int32_t* x;                         // working labels, by vertex id
+    int32_t* lbuf;                      // phase 1 output: label of every arc's neighbour
+    int32_t* mark;                      // next-round marks by vertex id, null = no cross-batch deps
+    int32_t* mq_out;                    // queue of newly marked vertices (this round's writes)
+    int32_t* mq_len;                    // its length
     int32_t* ndist;                     // per-slot distinct-label count of the last evaluation
     unsigned long long* counters;       // see kCtr* below
     Routes r;
-    int32_t bs;   // batch size in positions
-    int32_t n;    // vertex count
     int32_t bin;  // counter slot of this launch
     uint32_t seed;
     uint32_t sweep;
 };
 
+// neighbour flags (low bits of snbr): the neighbour is in an earlier batch
+// (read its current-sweep label) / in a later batch (mark it when this
+// row's label changes).  Neither: same batch -> sweep-start label.
+constexpr uint32_t kEarlier = 1u, kLater = 2u;
+
 // counters: [0] changed delta (reset per sweep), [1] label writes (reset per
 // round), [4+k] arcs scanned and [8+k] vertices evaluated by kernel k
 // (k = 0 hub team, 1 8-warp team, 2 warp, 3 small; accumulated over a run)
-enum { kCtrChanged = 0, kCtrWrites = 1, kCtrArcs = 4, kCtrVerts = 8, kCtrCount = 12 };
+enum { kCtrChanged = 0, kCtrWrites = 1, kCtrGathered = 2, kCtrArcs = 4, kCtrVerts = 8, kCtrCount = 12 };
 
 // ndist[s]: low 30 bits = distinct labels seen at the last evaluation;
 // kMajBit = that evaluation's winner held a strict majority of the row's
@@ -123,13 +139,13 @@ __host__ __device__ __forceinline__ int32_t nd_count(int32_t v) { return v & (kM
 
 constexpr int kSmallMax = 16;     // thread-per-vertex bound (degree)
 // warp classes: 0 = 512-slot table (est <= 256, d <= 2048, 8 warps/block),
-// 1 = 2048-slot table (est <= 1024, d <= 8192, 4 warps/block)
+// 1 = 1024-slot table (est <= 512, d <= 8192, 8 warps/block)
 template <int WC> struct WarpClass;
 template <> struct WarpClass<0> {
     static constexpr int kBits = 9, kEst = 256, kMaxDeg = 2048, kWarps = 8, kList = 3;
 };
 template <> struct WarpClass<1> {
-    static constexpr int kBits = 11, kEst = 1024, kMaxDeg = 8192, kWarps = 4, kList = 6;
+    static constexpr int kBits = 10, kEst = 512, kMaxDeg = 8192, kWarps = 8, kList = 6;
 };
 constexpr int kWarpEst = WarpClass<0>::kEst;
 constexpr int kTeamEst = 2048;    // 8-warp team: 4096-slot table
@@ -152,17 +168,10 @@ template <int WM> __device__ __forceinline__ typename Acc<WM>::T arc_weight(cons
     }
 }
 
-// First position of p's batch (bs == 1: the reference order; bs >= n: sync).
-__device__ __forceinline__ int32_t batch_start(const EvalArgs& a, int32_t p) {
-    if (a.bs == 1) return p;
-    if (a.bs >= a.n) return 0;
-    return (p / a.bs) * a.bs;
-}
-
-// Neighbour label under the batched schedule: neighbours in an earlier batch
-// have already been solved this sweep (x), the rest still hold L0.
-__device__ __forceinline__ int32_t read_label(const EvalArgs& a, int32_t u, int32_t thr) {
-    return (u < thr) ? a.x[u] : __ldg(a.L0 + u);
+// Label of a neighbour under the batched schedule (phase 1).
+__device__ __forceinline__ int32_t gather_label(const EvalArgs& a, uint32_t nb) {
+    const int32_t u = (int32_t)(nb >> 2);
+    return (nb & kEarlier) ? a.x[u] : __ldg(a.L0 + u);
 }
 
 __device__ __forceinline__ void flush_counters(const EvalArgs& a, long long dchg, long long arcs, long long writes,
@@ -184,23 +193,125 @@ __device__ __forceinline__ void flush_counters(const EvalArgs& a, long long dchg
 }
 
 // Write a vertex's new label (one thread).  Returns true when it changed.
-__device__ __forceinline__ bool commit_label(const EvalArgs& a, int32_t p, int32_t lab, long long& dchg,
+__device__ __forceinline__ bool commit_label(const EvalArgs& a, int32_t v, int32_t lab, long long& dchg,
                                              long long& writes) {
-    const int32_t old = a.x[p];
+    const int32_t old = a.x[v];
     if (lab == old || lab < 0) return false;
-    a.x[p] = lab;
-    const int32_t l0 = __ldg(a.L0 + p);
+    a.x[v] = lab;
+    const int32_t l0 = __ldg(a.L0 + v);
     dchg += (long long)(lab != l0) - (long long)(old != l0);
     ++writes;
     return true;
 }
 
-// Mark the later-batch neighbours of a vertex whose label changed.
-__device__ __forceinline__ void mark_row(const EvalArgs& a, uint32_t beg, int d, int32_t thr, int from, int step) {
-    const int32_t nb = thr + a.bs;
+// Same, with the vertex's current and sweep-start labels already loaded.
+__device__ __forceinline__ bool commit_label_known(const EvalArgs& a, int32_t v, int32_t lab, int32_t old, int32_t l0,
+                                                   long long& dchg, long long& writes) {
+    if (lab == old || lab < 0) return false;
+    a.x[v] = lab;
+    dchg += (long long)(lab != l0) - (long long)(old != l0);
+    ++writes;
+    return true;
+}
+
+// Mark the later-batch neighbours of a vertex whose label changed; a vertex
+// marked for the first time this round joins the mark queue (warp-aggregated
+// append), so the next round routes only the queue instead of scanning n.
+__device__ __forceinline__ void mark_row(const EvalArgs& a, uint32_t beg, int d, int from, int step) {
+    const int lane = threadIdx.x & 31;
     for (int k = from; k < d; k += step) {
-        const int32_t u = __ldg(a.snbr + beg + k);
-        if (u >= nb) a.mark[u] = 1;
+        const uint32_t nb = __ldg(a.snbr + beg + k);
+        const int32_t u = (int32_t)(nb >> 2);
+        const bool win = (nb & kLater) && atomicExch(a.mark + u, 1) == 0;
+        const uint32_t act = __activemask();
+        const uint32_t bal = __ballot_sync(act, win);
+        if (bal) {
+            const int leader = __ffs(bal) - 1;
+            int b0 = 0;
+            if (lane == leader) b0 = atomicAdd(a.mq_len, __popc(bal));
+            b0 = __shfl_sync(act, b0, leader);
+            if (win) a.mq_out[b0 + __popc(bal & lanemask_lt())] = u;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// phase 1: label gather
+// ---------------------------------------------------------------------------
+// Dense round: every arc of the active slots, flat and coalesced.
+__global__ void __launch_bounds__(256) k_gather_dense(EvalArgs a, int64_t m) {
+    constexpr int J = 8;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < m; base += stride * J) {
+        uint32_t nb[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int64_t e = base + j * stride;
+            nb[j] = e < m ? __ldg(a.snbr + e) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int64_t e = base + j * stride;
+            if (e < m) a.lbuf[e] = gather_label(a, nb[j]);
+        }
+    }
+}
+
+// Frontier round: the routed rows, as pieces of at most kPieceArcs arcs.  A
+// warp takes 32 pieces at a time (lane j loads piece j), scans their lengths
+// in registers and streams the flattened arcs eight loads deep; each lane
+// finds its piece by a 5-step search over the warp's prefix (shuffles only).
+constexpr int kPieceArcs = 256;
+
+__global__ void __launch_bounds__(256) k_gather_pieces(EvalArgs a) {
+    constexpr int J = 8;
+    const int lane = threadIdx.x & 31;
+    const int cnt = a.r.len[kLenGather];
+    while (true) {
+        int b0 = 0;
+        if (lane == 0) b0 = atomicAdd(a.r.len + kGatherCursor, 32);
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (b0 >= cnt) break;
+        uint32_t pbeg = 0, plen = 0;
+        if (b0 + lane < cnt) {
+            const int32_t s = a.r.gslot[b0 + lane];
+            const int32_t k0 = a.r.gk0[b0 + lane];
+            const uint32_t rb = __ldg(a.soff + s), re = __ldg(a.soff + s + 1);
+            pbeg = rb + (uint32_t)k0;
+            plen = min((uint32_t)kPieceArcs, re - pbeg);
+        }
+        // inclusive prefix of piece lengths
+        uint32_t incl = plen;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t excl = incl - plen;
+        if (lane == 0) atomicAdd(a.counters + kCtrGathered, (unsigned long long)total);
+        for (uint32_t base = 0; base < total; base += 32 * J) {
+            uint32_t e[J];
+            uint32_t nb[J];
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const uint32_t i = base + j * 32 + lane;
+                // piece r: largest r with excl[r] <= i
+                int r = 0;
+#pragma unroll
+                for (int step = 16; step >= 1; step >>= 1) {
+                    const uint32_t ex = __shfl_sync(0xffffffffu, excl, r + step);
+                    if (r + step < 32 && ex <= i) r += step;
+                }
+                const uint32_t pb = __shfl_sync(0xffffffffu, pbeg, r);
+                const uint32_t pe = __shfl_sync(0xffffffffu, excl, r);
+                e[j] = i < total ? pb + (i - pe) : 0xffffffffu;
+                nb[j] = i < total ? __ldg(a.snbr + e[j]) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < J; ++j)
+                if (e[j] != 0xffffffffu) a.lbuf[e[j]] = gather_label(a, nb[j]);
+        }
     }
 }
 
@@ -286,30 +397,39 @@ __global__ void k_route_dense(EvalArgs a, int32_t s_beg, int32_t s_end) {
     }
 }
 
-// Frontier round: marked positions -> route lists (marks cleared).
-__global__ void k_route_marked(EvalArgs a, uint8_t* __restrict__ mark, const int32_t* __restrict__ slot_of_pos,
-                               int64_t n) {
-    for (int64_t base = (blockIdx.x * (int64_t)blockDim.x) * 4; base < n; base += (int64_t)gridDim.x * blockDim.x * 4) {
-        const int64_t p0 = base + (int64_t)threadIdx.x * 4;
-        uint32_t word = 0;
-        if (p0 + 4 <= n) {
-            word = *reinterpret_cast<const uint32_t*>(mark + p0);
-            if (word) *reinterpret_cast<uint32_t*>(mark + p0) = 0u;
-        } else {
-            for (int j = 0; j < 4 && p0 + j < n; ++j) {
-                word |= (uint32_t)mark[p0 + j] << (8 * j);
-                mark[p0 + j] = 0;
-            }
+// Frontier round: the queued (marked) vertices -> route lists + phase-1
+// pieces; marks are cleared so this round's writes can queue them again.
+__global__ void k_route_queue(EvalArgs a, const int32_t* __restrict__ mq_in, const int32_t* __restrict__ mq_in_len,
+                              const int32_t* __restrict__ slot_of) {
+    const int lane = threadIdx.x & 31;
+    const int cnt = *mq_in_len;
+    for (int base = blockIdx.x * blockDim.x; base < cnt; base += gridDim.x * blockDim.x) {
+        const int i = base + threadIdx.x;
+        int cls = -1, est = 0, d = 0;
+        int32_t s = -1;
+        if (i < cnt) {
+            const int32_t v = mq_in[i];
+            a.mark[v] = 0;
+            s = slot_of[v];
+            if (s >= 0) cls = route_class(a, s, est, d);
         }
+        route_append(a, cls, s, est, d);
+        // phase-1 pieces of the routed row
+        const int np = cls >= 0 ? (d + kPieceArcs - 1) / kPieceArcs : 0;
+        const uint32_t act = __activemask();
+        int incl = np;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            int cls = -1, est = 0, d = 0;
-            int32_t s = -1;
-            if ((word >> (8 * j)) & 0xffu) {
-                s = slot_of_pos[p0 + j];
-                if (s >= 0) cls = route_class(a, s, est, d);
-            }
-            route_append(a, cls, s, est, d);
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(act, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int tot = __shfl_sync(act, incl, 31);
+        int b0 = 0;
+        if (lane == 31 && tot) b0 = atomicAdd(a.r.len + kLenGather, tot);
+        b0 = __shfl_sync(act, b0, 31);
+        for (int q = 0; q < np; ++q) {
+            a.r.gslot[b0 + incl - np + q] = s;
+            a.r.gk0[b0 + incl - np + q] = q * kPieceArcs;
         }
     }
 }
@@ -330,19 +450,17 @@ __global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, i
     long long dchg = 0, arcs = 0, writes = 0, verts = 0;
     for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
         const int32_t s = listed ? list[i] : s_beg + i;
-        const int32_t p = __ldg(a.spos + s);
+        const int32_t p = __ldg(a.svid + s);
         const uint32_t beg = __ldg(a.soff + s);
         const int d = (int)(__ldg(a.soff + s + 1) - beg);
-        const int32_t thr = batch_start(a, p);
-        int32_t nbr[MAXD];
-#pragma unroll
-        for (int k = 0; k < MAXD; ++k) nbr[k] = (k < d) ? __ldg(a.snbr + beg + k) : 0;
+        const int32_t xv = a.x[p];
+        const int32_t l0v = __ldg(a.L0 + p);
         int32_t lab[MAXD];
         A w[MAXD];
 #pragma unroll
         for (int k = 0; k < MAXD; ++k) {
             if (k < d) {
-                lab[k] = read_label(a, nbr[k], thr);
+                lab[k] = a.lbuf[beg + k];
                 w[k] = arc_weight<WM>(a, beg + k);
             } else {
                 lab[k] = kEmpty;
@@ -356,14 +474,14 @@ __global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, i
 #pragma unroll
         for (int k = 0; k < MAXD; ++k) total += w[k];
         if ((nd & kMajBit) && WM != kFloat) {
-            const int32_t cand = a.x[p];
+            const int32_t cand = xv;
             A cw = A(0);
 #pragma unroll
             for (int k = 0; k < MAXD; ++k)
                 if (lab[k] == cand) cw += w[k];
             if (cw + cw > total) continue;  // strict majority: label unchanged
         }
-        const uint32_t vtx = (TIE == kRandom) ? (uint32_t)__ldg(a.vid + p) : 0u;
+        const uint32_t vtx = (uint32_t)p;
         Cand<A> best = none_cand<A>();
 #pragma unroll
         for (int i2 = 0; i2 < MAXD; ++i2) {
@@ -385,12 +503,7 @@ __global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, i
         }
         const int32_t nd_new = (best.w + best.w > total) ? kMajBit : 0;
         if (nd_new != nd) a.ndist[s] = nd_new;
-        if (commit_label(a, p, best.lab, dchg, writes) && a.mark) {
-            const int32_t nb = thr + a.bs;
-#pragma unroll
-            for (int k = 0; k < MAXD; ++k)
-                if (k < d && nbr[k] >= nb) a.mark[nbr[k]] = 1;
-        }
+        if (commit_label_known(a, p, best.lab, xv, l0v, dchg, writes) && a.mark) mark_row(a, beg, d, 0, 1);
     }
     flush_counters(a, dchg, arcs, writes, verts);
 }
@@ -721,7 +834,7 @@ __device__ __forceinline__ int insert_chunk(STable<WM, BITS>& t, int32_t lab, ty
 // shared memory and no atomics.  Rows estimated to hold more labels, or that
 // outgrow the register table, use the warp's shared-memory hash.
 template <int WM, int TIE, int WC>
-__global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 6) k_warp(EvalArgs a) {
+__global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k_warp(EvalArgs a) {
     using A = typename Acc<WM>::T;
     using WT = WarpTable<WM, WC>;
     constexpr int kWarpBits = WarpClass<WC>::kBits;
@@ -748,16 +861,20 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 6) k
         b0 = __shfl_sync(0xffffffffu, b0, 0);
         if (b0 >= cnt) break;
         const int nv = min(bsz, cnt - b0);
-        int32_t ms = -1, mp = 0, mnd = 0;
+        int32_t ms = -1, mp = 0, mnd = 0, mx = 0, ml0 = 0;
         uint32_t mbeg = 0, mend = 0;
         if (lane < nv) {
             ms = list[b0 + lane];
-            mp = __ldg(a.spos + ms);
+            mp = __ldg(a.svid + ms);
             mbeg = __ldg(a.soff + ms);
             mend = __ldg(a.soff + ms + 1);
             mnd = __ldg(a.ndist + ms);
+            // a vertex's label is written only by its own evaluation, once per
+            // round: safe to load it with the batch
+            mx = a.x[mp];
+            ml0 = __ldg(a.L0 + mp);
         }
-        // prefetched first index block of the current vertex
+        // prefetched first label block of the current vertex
         int32_t nbr_next[U];
         {
             const uint32_t beg0 = __shfl_sync(0xffffffffu, mbeg, 0);
@@ -765,7 +882,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 6) k
 #pragma unroll
             for (int c = 0; c < U; ++c) {
                 const int k = c * 32 + lane;
-                nbr_next[c] = (k < d0) ? __ldg(a.snbr + beg0 + k) : -1;
+                nbr_next[c] = (k < d0) ? a.lbuf[beg0 + k] : kEmpty;
             }
         }
         for (int v = 0; v < nv; ++v) {
@@ -774,8 +891,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 6) k
             const uint32_t beg = __shfl_sync(0xffffffffu, mbeg, v);
             const int d = (int)(__shfl_sync(0xffffffffu, mend, v) - beg);
             const int32_t nd = __shfl_sync(0xffffffffu, mnd, v);
-            const int32_t thr = batch_start(a, p);
-            const uint32_t vtx = (TIE == kRandom) ? (uint32_t)__ldg(a.vid + p) : 0u;
+            const uint32_t vtx = (uint32_t)p;
             // prefetch the next block: of this row, else the next vertex's first one
 #define LP_WARP_PREFETCH(base_done)                                                             \
     do {                                                                                        \
@@ -789,7 +905,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 6) k
         }                                                                                       \
         _Pragma("unroll") for (int c_ = 0; c_ < U; ++c_) {                                      \
             const int k_ = nb_base + c_ * 32 + lane;                                            \
-            nbr_next[c_] = (k_ < nb_d) ? __ldg(a.snbr + nb_beg + k_) : -1;                      \
+            nbr_next[c_] = (k_ < nb_d) ? a.lbuf[nb_beg + k_] : kEmpty;                         \
         }                                                                                       \
     } while (0)
             A total;
@@ -800,15 +916,17 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 6) k
             else
                 total = A(0);
             // ---- majority check (vertices whose last winner held > half the row) ----
+            const int32_t xv = __shfl_sync(0xffffffffu, mx, v);
+            const int32_t l0v = __shfl_sync(0xffffffffu, ml0, v);
             if (WM != kFloat && (nd & kMajBit)) {
-                const int32_t cand = a.x[p];
+                const int32_t cand = xv;
                 A cw = A(0);
                 for (int base = 0; base < d; base += 32 * U) {
                     int32_t labv[U];
 #pragma unroll
                     for (int c = 0; c < U; ++c) {
                         const int k = base + c * 32 + lane;
-                        labv[c] = (k < d) ? read_label(a, nbr_next[c], thr) : kEmpty;
+                        labv[c] = (k < d) ? nbr_next[c] : kEmpty;
                     }
                     LP_WARP_PREFETCH(base);
 #pragma unroll
@@ -830,7 +948,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 6) k
 #pragma unroll
                 for (int c = 0; c < U; ++c) {
                     const int k = c * 32 + lane;
-                    nbr_next[c] = (k < d) ? __ldg(a.snbr + beg + k) : -1;
+                    nbr_next[c] = (k < d) ? a.lbuf[beg + k] : kEmpty;
                 }
             }
             const int est = min(d, nd_count(nd) + (nd_count(nd) >> 2) + 16);
@@ -849,7 +967,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 6) k
 #pragma unroll
                 for (int c = 0; c < U; ++c) {
                     const int k = base + c * 32 + lane;
-                    labv[c] = (k < d) ? read_label(a, nbr_next[c], thr) : kEmpty;
+                    labv[c] = (k < d) ? nbr_next[c] : kEmpty;
                     wv[c] = (k < d) ? arc_weight<WM>(a, beg + k) : A(0);
                 }
                 LP_WARP_PREFETCH(base);
@@ -969,7 +1087,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 6) k
                         bool ok = false;
                         int32_t lab = kEmpty;
                         if (k < d) {
-                            lab = read_label(a, __ldg(a.snbr + beg + k), thr);
+                            lab = a.lbuf[beg + k];
                             const int h = tab->t.find(lab);
                             ok = h >= 0 && tab->t.weight(h) == b.w && sec_of<TIE>(lab, a.seed, a.sweep, vtx) == b.sec;
                         }
@@ -987,10 +1105,10 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 6) k
                 ++verts;
                 const bool maj = WM != kFloat && wbest + wbest > total;
                 a.ndist[s] = (hashed ? ntouched : K) | (maj ? kMajBit : 0);
-                changed = commit_label(a, p, winner, dchg, writes);
+                changed = commit_label_known(a, p, winner, xv, l0v, dchg, writes);
             }
             changed = __shfl_sync(0xffffffffu, changed, 0);
-            if (changed && a.mark) mark_row(a, beg, d, thr, lane, 32);
+            if (changed && a.mark) mark_row(a, beg, d, lane, 32);
         }
     }
     flush_counters(a, dchg, arcs, writes, verts);
@@ -1081,7 +1199,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
     // Best label of row arcs [0, d) restricted to label partitions taken from
     // the work stack (preloaded by the caller).  Sub-splits on overflow.
     // `single`: one whole-row pass (no first position needed unless tied).
-    auto row_best = [&](const uint32_t beg, const int d, const int32_t thr, const uint32_t vtx, bool single,
+    auto row_best = [&](const uint32_t beg, const int d, const uint32_t vtx, bool single,
                         bool agg, int& distinct) -> Best<A> {
         Best<A> overall = none_best<A>();
         distinct = 0;
@@ -1105,7 +1223,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
                     int32_t lab = kEmpty;
                     A w = A(0);
                     if (k < d) {
-                        lab = read_label(a, __ldg(a.snbr + beg + k), thr);
+                        lab = a.lbuf[beg + k];
                         w = arc_weight<WM>(a, beg + k);
                         if (parts > 1 && part_of(lab, parts) != want) lab = kEmpty;
                     }
@@ -1160,7 +1278,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
                     bool ok = false;
                     int32_t lab = kEmpty;
                     if (k < d) {
-                        lab = read_label(a, __ldg(a.snbr + beg + k), thr);
+                        lab = a.lbuf[beg + k];
                         if (parts <= 1 || part_of(lab, parts) == want) {
                             const int h = tab->t.find(lab);
                             ok = h >= 0 && tab->t.weight(h) == b.w &&
@@ -1197,11 +1315,10 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
         if (it >= cnt) break;
         const Item item = items[it];
         const int32_t s = item.s;
-        const int32_t p = __ldg(a.spos + s);
+        const int32_t p = __ldg(a.svid + s);
         const uint32_t beg = __ldg(a.soff + s);
         const int d = (int)(__ldg(a.soff + s + 1) - beg);
-        const int32_t thr = batch_start(a, p);
-        const uint32_t vtx = (TIE == kRandom) ? (uint32_t)__ldg(a.vid + p) : 0u;
+        const uint32_t vtx = (uint32_t)p;
         const int32_t nd = __ldg(a.ndist + s);
         A total;
         if constexpr (WM == kUnit)
@@ -1219,7 +1336,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
 #pragma unroll
                 for (int c = 0; c < U; ++c) {
                     const int k = base + c * 32 + lane;
-                    labv[c] = (k < d) ? read_label(a, __ldg(a.snbr + beg + k), thr) : kEmpty;
+                    labv[c] = (k < d) ? a.lbuf[beg + k] : kEmpty;
                 }
 #pragma unroll
                 for (int c = 0; c < U; ++c) {
@@ -1256,7 +1373,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
                 s_stack[0][1] = (uint32_t)item.q;
             }
             __syncthreads();
-            best = row_best(beg, d, thr, vtx, item.P == 1, agg, distinct);
+            best = row_best(beg, d, vtx, item.P == 1, agg, distinct);
             if (item.P > 1) {
                 // the last partition block merges the P candidates
                 if (tid == 0) {
@@ -1304,7 +1421,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
                 int32_t lab = kEmpty;
                 A w = A(0);
                 if (k < k_hi) {
-                    lab = read_label(a, __ldg(a.snbr + beg + k), thr);
+                    lab = a.lbuf[beg + k];
                     w = arc_weight<WM>(a, beg + k);
                 }
                 const uint32_t grp = __match_any_sync(0xffffffffu, lab);
@@ -1373,7 +1490,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
                         s_sp = 4;
                     }
                     __syncthreads();
-                    best = row_best(beg, d, thr, vtx, false, false, distinct);
+                    best = row_best(beg, d, vtx, false, false, distinct);
                 }
             }
         }
@@ -1388,7 +1505,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
             }
         }
         __syncthreads();
-        if (s_flag && a.mark) mark_row(a, beg, d, thr, tid, NT);
+        if (s_flag && a.mark) mark_row(a, beg, d, tid, NT);
         if (!DYNAMIC) it += gridDim.x;
     }
     flush_counters(a, dchg, arcs, writes, verts);
