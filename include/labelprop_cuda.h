@@ -91,6 +91,18 @@ typedef struct lp_rak_opts {
     int64_t reserved[6];
 } lp_rak_opts;
 
+/* SLPA (slpa.py SlpaParams :34-48).  Speaking rounds t = 1 .. T-1 over the
+ * identity visit order (slpa.py:99), self-loops silent (:75). */
+typedef struct lp_slpa_opts {
+    double tolerance;       /* (0, 1]; stop once repeats >= (1-tol) * n, t >= 2 */
+    int32_t memory_size;    /* T >= 2                                        */
+    int32_t tie;            /* LP_TIE_SCAN_FIRST (strict) / LP_TIE_RANDOM     */
+    int64_t batches;        /* 0 or n = the reference's in-place sweep; 1 = synchronous */
+    uint32_t seed;          /* speaker draws and random ties (counter RNG)   */
+    int32_t flags;          /* LP_RAK_PROFILE                                */
+    int64_t reserved[6];
+} lp_slpa_opts;
+
 /* Kernel slots of the engine, index of the lp_run_stats
  * bin_* arrays.  A vertex is routed each round by its degree d and its
  * estimated distinct neighbour labels. */
@@ -142,6 +154,13 @@ int lp_rak_run(lp_graph* g, const lp_rak_opts* opts, const int64_t* order, const
  * with inputs resident in HBM).  lp_labels_download() copies them out. */
 int lp_rak_run_resident(lp_graph* g, const lp_rak_opts* opts, const int64_t* order, lp_run_stats* stats);
 int lp_labels_download(lp_graph* g, int64_t* labels_out);
+
+/* SLPA: replaces _slpa_seq/_slpa_par + _project (slpa.py:91-150).
+ * labels_out[n]: modal label of every memory (NULL: skip); slots_out[n*T]:
+ * the memories, row-major, unfilled slots 0 (NULL: skip); every memory
+ * holds stats->iterations + 1 labels.  repeats_per_iter: NULL or T-1. */
+int lp_slpa_run(lp_graph* g, const lp_slpa_opts* opts, int64_t* labels_out, int64_t* slots_out,
+                int64_t* repeats_per_iter, lp_run_stats* stats);
 
 /* Calibration (device time per pass, ms): mode 0 streams the neighbour
  * indices of the active rows once; mode 1 also gathers every neighbour's

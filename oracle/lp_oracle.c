@@ -509,8 +509,9 @@ static int64_t modal_label(const int64_t* row, int64_t filled) {
     return best;
 }
 
-/* Counter RNG for the speaker draw (GPU rule): slot index of speaker u
- * heard by listener v in round t. */
+/* Counter RNG for the speaker draw (GPU rule): keyed by the round t, the
+ * listener v and the speaker's index k among v's non-self arcs (scan
+ * order); the slot is the hash mod filled[u]. */
 uint32_t or_speak_hash(uint32_t seed, uint32_t t, uint32_t listener, uint32_t e) {
     return or_tie_hash(seed ^ 0x53504B52u, t, listener, e);
 }
@@ -543,11 +544,11 @@ int or_slpa(int64_t n, const int64_t* off, const int64_t* nbr, const double* w, 
             int64_t b1 = b0 + bs < n ? b0 + bs : n;
             for (int64_t v = b0; v < b1; ++v) {
                 int64_t count = 0;
+                uint32_t spk = 0; /* index of the speaker among v's non-self arcs */
                 for (int64_t e = off[v]; e < off[v + 1]; ++e) {
                     int64_t u = nbr[e];
                     if (u == v) continue; /* slpa.py:75 */
-                    uint32_t j = speaker_rng ? or_speak_hash(seed, (uint32_t)t, (uint32_t)v, (uint32_t)(e - off[v])) %
-                                                   (uint32_t)filled[u]
+                    uint32_t j = speaker_rng ? or_speak_hash(seed, (uint32_t)t, (uint32_t)v, spk++) % (uint32_t)filled[u]
                                              : or_draw(&xs, (uint32_t)filled[u]);
                     int64_t lab = slots[u * T + j];
                     if (s.tally[lab] == 0.0) s.touched[count++] = lab;

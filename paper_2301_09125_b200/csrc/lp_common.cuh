@@ -47,6 +47,13 @@ __host__ __device__ __forceinline__ uint32_t tie_hash(uint32_t seed, uint32_t sw
     return h;
 }
 
+// Counter RNG for SLPA's speaker draw: listener `listener` hears its k-th
+// speaking (non-self) neighbour in round t; same definition as the oracle's
+// or_speak_hash (oracle/lp_oracle.c).
+__host__ __device__ __forceinline__ uint32_t speak_hash(uint32_t seed, uint32_t t, uint32_t listener, uint32_t k) {
+    return tie_hash(seed ^ 0x53504B52u, t, listener, k);
+}
+
 // Candidate label for the argmax.  Ordering: larger weight, then larger
 // `sec`, then larger `ter`.  (sec, ter) encode the tie rule so that the
 // maximum is unique per distinct label:

@@ -35,6 +35,7 @@
 #include "lp_common.cuh"
 #include "lp_host.h"
 #include "lp_rak_kernels.cuh"
+#include "lp_slpa_kernels.cuh"
 
 using namespace lp;
 
@@ -61,9 +62,16 @@ template <typename T> static cudaError_t dalloc(T** p, size_t count, int64_t* by
     return cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
 }
 
+// Plan kinds: RAK (seeded/custom visit order, self-loop arcs kept: the
+// reference tally counts them, rak.py:99-105) and INDEX (identity order,
+// self arcs dropped: COPRA and SLPA skip them, copra.py:137-139,
+// slpa.py:75).
+enum PlanKind : int { kPlanRak = 0, kPlanIndex = 1, kNumPlanKinds = 2 };
+
 struct Plan {
     bool valid = false;
     bool custom_order = false;
+    int kind = kPlanRak;
     uint32_t seed = 0;
     uint64_t order_hash = 0;
     int32_t* pos = nullptr;          // vertex -> visit position
@@ -80,6 +88,11 @@ struct Plan {
     int64_t flags_bs = -1;           // batch size the snbr flags were computed for
     int32_t bin_beg[kNumBins + 1] = {0, 0, 0, 0, 0, 0};  // slot range of each bin (idle: [.., n))
     int32_t big_end = 0;             // slots [0, big_end) are big rows, [big_end, S) small
+    // every active row as phase-1 pieces (INDEX plans: SLPA's dense rounds)
+    int32_t* dslot = nullptr;
+    int32_t* dk0 = nullptr;
+    int32_t* dcount = nullptr;       // device copy of the piece count
+    int64_t npieces = 0;
     int64_t bytes = 0;
 };
 
@@ -97,7 +110,9 @@ struct lp_graph {
     uint32_t* off = nullptr;
     int32_t* nbr = nullptr;
     uint32_t* w = nullptr;  // converted weights (fixed-point or float bits)
-    Plan plan;
+    Plan plans[kNumPlanKinds];
+    int pk = kPlanRak;  // the plan the current run uses
+    Plan& plan() { return plans[pk]; }
     // run state
     int32_t* labA = nullptr;
     int32_t* labB = nullptr;
@@ -105,6 +120,8 @@ struct lp_graph {
     int32_t* mark = nullptr;    // frontier marks by vertex id
     int32_t* mq[2] = {nullptr, nullptr};  // mark queues (alternate per round)
     int32_t* mq_len = nullptr;  // their lengths [2]
+    int32_t* slots = nullptr;   // SLPA memories [n x T]
+    size_t slots_cap = 0;
     Routes routes;
     int64_t cap_items = 0;
     unsigned long long* counters = nullptr;
@@ -211,16 +228,28 @@ __global__ void k_plan_check_perm(const int64_t* __restrict__ order, const int32
 // degree (the dense route then hands out the largest hubs first); inside a
 // small class vertex-id order (neighbouring rows share neighbours: locality
 // for the label gathers)
+// arcs of row v that are not its self-loop (INDEX plans)
+__device__ __forceinline__ uint32_t row_degree(const uint32_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                                               int64_t v, int noself) {
+    const uint32_t b = off[v], e = off[v + 1];
+    if (!noself) return e - b;
+    uint32_t selfs = 0;
+    for (uint32_t i = b; i < e; ++i) selfs += nbr[i] == (int32_t)v;
+    return e - b - selfs;
+}
+
 __global__ void k_plan_keys(const uint32_t* __restrict__ off, const int32_t* __restrict__ nbr,
-                            unsigned long long* __restrict__ key, int64_t n, unsigned long long* counts) {
+                            unsigned long long* __restrict__ key, int64_t n, unsigned long long* counts,
+                            uint32_t* __restrict__ deg, int noself) {
     __shared__ unsigned long long sc[kNumBins];
     if (threadIdx.x < kNumBins) sc[threadIdx.x] = 0;
     __syncthreads();
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t d = off[v + 1] - off[v];
+        const uint32_t d = row_degree(off, nbr, v, noself);
+        deg[v] = d;
         int b;
-        if (d == 0 || (d == 1 && nbr[off[v]] == (int32_t)v))
-            b = kBinIdle;  // label provably cannot move
+        if (d == 0 || (!noself && d == 1 && nbr[off[v]] == (int32_t)v))
+            b = kBinIdle;  // RAK: label provably cannot move; INDEX: no speaker / contributor
         else if (d > (uint32_t)kSmallMax)
             b = kBinBig;
         else
@@ -237,13 +266,13 @@ __global__ void k_iota(int32_t* a, int64_t n) {
         a[i] = (int32_t)i;
 }
 
-__global__ void k_plan_slots(const int32_t* __restrict__ svid, const uint32_t* __restrict__ off,
+__global__ void k_plan_slots(const int32_t* __restrict__ svid, const uint32_t* __restrict__ deg,
                              int32_t* __restrict__ slot_of, uint32_t* __restrict__ sdeg, int64_t n, int64_t S) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = svid[s];
         if (s < S) {
             slot_of[v] = (int32_t)s;
-            sdeg[s] = off[v + 1] - off[v];
+            sdeg[s] = deg[v];
         } else {
             slot_of[v] = -1;
         }
@@ -257,19 +286,46 @@ __global__ void k_reset_ndist(const uint32_t* __restrict__ soff, int32_t* __rest
         ndist[s] = (int32_t)(soff[s + 1] - soff[s]);
 }
 
-// one warp per slot: copy the row (neighbour ids, flags cleared) and weights
+// one warp per slot: copy the row (neighbour ids, flags cleared) and weights;
+// INDEX plans drop the self-loop arcs (order of the others kept)
 __global__ void k_plan_rows(const int32_t* __restrict__ svid, const uint32_t* __restrict__ off,
                             const int32_t* __restrict__ nbr, const uint32_t* __restrict__ w,
                             const uint32_t* __restrict__ soff, uint32_t* __restrict__ snbr, uint32_t* __restrict__ sw,
-                            int64_t S) {
+                            int64_t S, int noself) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
     for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < S; s += warps) {
         const int32_t v = svid[s];
-        const uint32_t src = off[v], d = off[v + 1] - src, dst = soff[s];
-        for (uint32_t k = lane; k < d; k += 32) {
-            snbr[dst + k] = (uint32_t)nbr[src + k] << 2;
-            if (w) sw[dst + k] = w[src + k];
+        const uint32_t src = off[v], d = off[v + 1] - src;
+        uint32_t dst = soff[s];
+        for (uint32_t k0 = 0; k0 < d; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            const int32_t u = k < d ? nbr[src + k] : -1;
+            const bool keep = k < d && !(noself && u == v);
+            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const uint32_t o = dst + __popc(bal & lanemask_lt());
+                snbr[o] = (uint32_t)u << 2;
+                if (w) sw[o] = w[src + k];
+            }
+            dst += __popc(bal);
+        }
+    }
+}
+
+// INDEX plans: pieces (slot, first arc) of every active row, for phase-1
+// gathers that need the row of each arc
+__global__ void k_plan_piece_counts(const uint32_t* __restrict__ soff, uint32_t* __restrict__ cnt, int64_t S) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s <= S; s += (int64_t)gridDim.x * blockDim.x)
+        cnt[s] = s < S ? (soff[s + 1] - soff[s] + kPieceArcs - 1) / kPieceArcs : 0u;
+}
+__global__ void k_plan_pieces(const uint32_t* __restrict__ soff, const uint32_t* __restrict__ pbeg,
+                              int32_t* __restrict__ dslot, int32_t* __restrict__ dk0, int64_t S) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S; s += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t np = pbeg[s + 1] - pbeg[s];
+        for (uint32_t q = 0; q < np; ++q) {
+            dslot[pbeg[s] + q] = (int32_t)s;
+            dk0[pbeg[s] + q] = (int32_t)(q * kPieceArcs);
         }
     }
 }
@@ -415,16 +471,24 @@ template <int WM, int TIE> struct Launcher {
     }
     // One round.  dense: k_small sweeps the small slot range and the other
     // slots are routed; frontier: everything comes from the marked route.
-    static void round(lp_graph* g, EvalArgs a, bool dense, const int32_t* h_len, Prof* prof) {
-        const Plan& P = g->plan;
+    static void round(lp_graph* g, EvalArgs a, bool dense, const int32_t* h_len, Prof* prof, int alg) {
+        const Plan& P = g->plan();
         const int sms = g->num_sms;
         cudaStream_t st = g->stream;
         // ---- phase 1: gather every evaluated row's neighbour labels ----
         prof->begin(st, kKGather);
-        if (dense) {
+        if (alg == kGatherSlpa) {
+            if (dense)
+                k_gather_pieces<kGatherSlpa><<<grid_for(P.npieces, 32 * 8, sms * 16), 256, 0, st>>>(
+                    a, P.dslot, P.dk0, P.dcount, a.r.len + kGatherCursor);
+            else
+                k_gather_pieces<kGatherSlpa><<<grid_for(h_len[kLenGather], 32 * 8, sms * 16), 256, 0, st>>>(
+                    a, a.r.gslot, a.r.gk0, a.r.len + kLenGather, a.r.len + kGatherCursor);
+        } else if (dense) {
             k_gather_dense<<<grid_for(P.m_active, 256 * 8, sms * 16), 256, 0, st>>>(a, P.m_active);
         } else {
-            k_gather_pieces<<<grid_for(h_len[kLenGather], 32 * 8, sms * 16), 256, 0, st>>>(a);
+            k_gather_pieces<kGatherRak><<<grid_for(h_len[kLenGather], 32 * 8, sms * 16), 256, 0, st>>>(
+                a, a.r.gslot, a.r.gk0, a.r.len + kLenGather, a.r.len + kGatherCursor);
         }
         prof->end(st);
         // ---- phase 2: route and tally ----
@@ -478,7 +542,7 @@ template <int WM, int TIE> int Launcher<WM, TIE>::occ_team = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_hub = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::done_device = -1;
 
-typedef void (*round_fn)(lp_graph*, EvalArgs, bool, const int32_t*, Prof*);
+typedef void (*round_fn)(lp_graph*, EvalArgs, bool, const int32_t*, Prof*, int);
 typedef cudaError_t (*setup_fn)(int);
 
 template <int WM> static void pick_fns(int tie, round_fn* r, setup_fn* s) {
@@ -510,6 +574,9 @@ static void free_plan(Plan& P) {
     cudaFree(P.swsum);
     cudaFree(P.ndist);
     cudaFree(P.lbuf);
+    cudaFree(P.dslot);
+    cudaFree(P.dk0);
+    cudaFree(P.dcount);
     P = Plan();
 }
 
@@ -533,11 +600,12 @@ static void free_routes(Routes& r) {
 
 static void destroy_graph(lp_graph* g) {
     if (!g) return;
-    free_plan(g->plan);
+    for (Plan& P : g->plans) free_plan(P);
     free_routes(g->routes);
     cudaFree(g->mq[0]);
     cudaFree(g->mq[1]);
     cudaFree(g->mq_len);
+    cudaFree(g->slots);
     cudaFree(g->off);
     cudaFree(g->nbr);
     cudaFree(g->w);
@@ -581,7 +649,9 @@ struct TmpBufs {
     unsigned long long* key_sorted = nullptr;
     int32_t* iota = nullptr;
     uint32_t* sdeg = nullptr;
+    uint32_t* deg = nullptr;
     ~TmpBufs() {
+        cudaFree(deg);
         cudaFree(order);
         cudaFree(key);
         cudaFree(key_sorted);
@@ -590,21 +660,30 @@ struct TmpBufs {
     }
 };
 
-// Build (or reuse) the plan for a visit order: positions, the degree-binned
-// storage CSR (neighbour ids), the phase-1 label buffer.
-static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, float* plan_ms) {
+// Build (or reuse) the plan of a kind and visit order: positions, the
+// degree-binned storage CSR (neighbour ids), the phase-1 label buffer.
+// RAK plans follow `order_host` (NULL: shuffled_indices(n, seed)); INDEX
+// plans use the identity order and ignore both.
+static int build_plan(lp_graph* g, int kind, const int64_t* order_host, uint32_t seed, float* plan_ms) {
     const int64_t n = g->n;
+    g->pk = kind;
+    const bool index = kind == kPlanIndex;
+    if (index) order_host = nullptr;
     const bool custom = order_host != nullptr;
     const uint64_t oh = custom ? hash_order(order_host, n) : 0;
-    Plan& P = g->plan;
+    Plan& P = g->plan();
     *plan_ms = 0.f;
-    if (P.valid && P.custom_order == custom && (custom ? P.order_hash == oh : P.seed == seed)) return LP_OK;
+    if (P.valid && (index || (P.custom_order == custom && (custom ? P.order_hash == oh : P.seed == seed))))
+        return LP_OK;
     g->bytes -= P.bytes;
     free_plan(P);
     std::vector<int64_t> own;
     if (!custom) {
         own.resize((size_t)n);
-        lp_host_shuffled_indices(n, seed, own.data());
+        if (index)
+            for (int64_t i = 0; i < n; ++i) own[(size_t)i] = i;
+        else
+            lp_host_shuffled_indices(n, seed, own.data());
         order_host = own.data();
     }
     cudaStream_t st = g->stream;
@@ -621,6 +700,7 @@ static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, flo
     LP_CK(dalloc(&t.key_sorted, n, &tmpb));
     LP_CK(dalloc(&t.iota, n, &tmpb));
     LP_CK(dalloc(&t.sdeg, n + 1, &tmpb));
+    LP_CK(dalloc(&t.deg, n, &tmpb));
     LP_CK(cudaMemcpyAsync(t.order, order_host, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     LP_CK(cudaMemsetAsync(g->counters, 0, 8 * sizeof(unsigned long long), st));
     LP_CK(cudaMemsetAsync(P.pos, 0xff, n * sizeof(int32_t), st));
@@ -633,7 +713,7 @@ static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, flo
         free_plan(P);
         return lp_fail(LP_ERR_INVALID, "order is not a permutation of range(n)");
     }
-    k_plan_keys<<<G, 256, 0, st>>>(g->off, g->nbr, t.key, n, g->counters + 1);
+    k_plan_keys<<<G, 256, 0, st>>>(g->off, g->nbr, t.key, n, g->counters + 1, t.deg, index ? 1 : 0);
     k_iota<<<G, 256, 0, st>>>(t.iota, n);
     size_t need = 0, need2 = 0;
     LP_CK(cub::DeviceRadixSort::SortPairs(nullptr, need, t.key, t.key_sorted, t.iota, P.svid, (int)n, 0, 35, st));
@@ -652,7 +732,7 @@ static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, flo
     }
     P.big_end = P.bin_beg[kBinS16];
     P.S = P.bin_beg[kBinIdle];
-    k_plan_slots<<<G, 256, 0, st>>>(P.svid, g->off, P.slot_of, t.sdeg, n, P.S);
+    k_plan_slots<<<G, 256, 0, st>>>(P.svid, t.deg, P.slot_of, t.sdeg, n, P.S);
     LP_CK(dalloc(&P.soff, P.S + 1, &bytes));
     LP_CK(cub::DeviceScan::ExclusiveSum(g->cub_tmp, need2, t.sdeg, P.soff, (int)(P.S + 1), st));
     uint32_t m_active = 0;
@@ -662,7 +742,23 @@ static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, flo
     LP_CK(dalloc(&P.snbr, P.m_active, &bytes));
     LP_CK(dalloc(&P.lbuf, P.m_active, &bytes));
     if (g->w) LP_CK(dalloc(&P.sw, P.m_active, &bytes));
-    k_plan_rows<<<g->num_sms * 16, 256, 0, st>>>(P.svid, g->off, g->nbr, g->w, P.soff, P.snbr, P.sw, P.S);
+    k_plan_rows<<<g->num_sms * 16, 256, 0, st>>>(P.svid, g->off, g->nbr, g->w, P.soff, P.snbr, P.sw, P.S,
+                                                 index ? 1 : 0);
+    if (index) {
+        // dense piece list (reuses t.sdeg as the per-slot piece counts / offsets)
+        k_plan_piece_counts<<<G, 256, 0, st>>>(P.soff, t.sdeg, P.S);
+        LP_CK(cub::DeviceScan::ExclusiveSum(g->cub_tmp, need2, t.sdeg, t.sdeg, (int)(P.S + 1), st));
+        uint32_t np = 0;
+        LP_CK(cudaMemcpyAsync(&np, t.sdeg + P.S, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        LP_CK(cudaStreamSynchronize(st));
+        P.npieces = np;
+        LP_CK(dalloc(&P.dslot, np, &bytes));
+        LP_CK(dalloc(&P.dk0, np, &bytes));
+        LP_CK(dalloc(&P.dcount, 1, &bytes));
+        const int32_t npi = (int32_t)np;
+        LP_CK(cudaMemcpyAsync(P.dcount, &npi, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        k_plan_pieces<<<G, 256, 0, st>>>(P.soff, t.sdeg, P.dslot, P.dk0, P.S);
+    }
     if (g->wmode == kFixed && P.S > 0) {
         LP_CK(dalloc(&P.swsum, P.S, &bytes));
         k_plan_wsum<<<g->num_sms * 16, 256, 0, st>>>(P.soff, P.sw, P.swsum, P.S);
@@ -672,6 +768,7 @@ static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, flo
     LP_CK(cudaEventSynchronize(g->ev1));
     LP_CK(cudaEventElapsedTime(plan_ms, g->ev0, g->ev1));
     P.valid = true;
+    P.kind = kind;
     P.custom_order = custom;
     P.seed = seed;
     P.order_hash = oh;
@@ -683,7 +780,7 @@ static int build_plan(lp_graph* g, const int64_t* order_host, uint32_t seed, flo
 
 // (Re)compute the batch flags of the storage CSR for batch size bs.
 static int ensure_flags(lp_graph* g, int64_t bs, float* ms) {
-    Plan& P = g->plan;
+    Plan& P = g->plan();
     const bool none = bs >= g->n;  // one batch: no cross-batch reads or marks
     const int64_t key = none ? g->n : bs;
     if (P.flags_bs == key) return LP_OK;
@@ -858,6 +955,71 @@ extern "C" int lp_graph_get_info(const lp_graph* g, lp_graph_info* info) {
 
 extern "C" void* lp_graph_stream(lp_graph* g) { return g ? (void*)g->stream : nullptr; }
 
+// One sweep (RAK) or speaking round (SLPA): the dense round over every
+// active row, then frontier rounds over the mark queue until a round marks
+// nothing.  One host sync per frontier round (route sizes).
+static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round, int alg, Prof* prof, int* rounds,
+                       int64_t* gathered) {
+    const Plan& P = g->plan();
+    cudaStream_t st = g->stream;
+    LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
+    int q = 0;  // this round's writes queue into mq[q]
+    a.mq_out = g->mq[q];
+    a.mq_len = g->mq_len + q;
+    LP_CK(cudaMemsetAsync(g->mq_len, 0, 2 * sizeof(int32_t), st));
+    run_round(g, a, true, g->h_len, prof, alg);
+    if (alg == kGatherRak) *gathered += P.m_active;  // (piece gathers count themselves)
+    ++*rounds;
+    while (cross) {
+        // route last round's queue; this round's writes queue into the other one
+        LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
+        LP_CK(cudaMemsetAsync(g->mq_len + (q ^ 1), 0, sizeof(int32_t), st));
+        prof->begin(st, -1);
+        k_route_queue<<<g->num_sms * 4, 256, 0, st>>>(a, g->mq[q], g->mq_len + q, P.slot_of);
+        prof->end(st);
+        LP_CK(cudaMemcpyAsync(g->h_len, g->routes.len, kLenCount * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        LP_CK(cudaStreamSynchronize(st));
+        if (g->h_len[kLenGather] == 0) break;
+        q ^= 1;
+        a.mq_out = g->mq[q];
+        a.mq_len = g->mq_len + q;
+        LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
+        run_round(g, a, false, g->h_len, prof, alg);
+        ++*rounds;
+    }
+    return LP_OK;
+}
+
+// Per-run statistics from the counters (already downloaded to h_counters)
+// and the profiling events.
+static int finish_stats(lp_graph* g, const Prof& prof, lp_run_stats* S, int it, int rounds, int64_t gathered,
+                        float ms) {
+    S->iterations = it;
+    S->rounds = rounds;
+    S->kernel_ms = ms;
+    S->arcs_dense = g->plan().m_active * it;
+    S->launches = prof.launches;
+    S->arcs_gathered = gathered + (int64_t)g->h_counters[kCtrGathered];
+    S->gather_launches = prof.slot_launches[kKGather];
+    for (int b = 0; b < kKSlots; ++b) {
+        S->bin_arcs[b] = (int64_t)g->h_counters[kCtrArcs + b];
+        S->bin_vertices[b] = (int64_t)g->h_counters[kCtrVerts + b];
+        S->bin_launches[b] = prof.slot_launches[b];
+        S->arcs_scanned += S->bin_arcs[b];
+    }
+    for (size_t i = 0; i < prof.tags.size(); ++i) {
+        float e = 0.f;
+        LP_CK(cudaEventElapsedTime(&e, g->event_pool[2 * i], g->event_pool[2 * i + 1]));
+        if (prof.tags[i] == kKGather)
+            S->gather_ms += e;
+        else if (prof.tags[i] >= 0)
+            S->bin_ms[prof.tags[i]] += e;
+        else
+            S->aux_ms += e;
+    }
+    return LP_OK;
+}
+
 // ---------------------------------------------------------------------------
 // RAK driver
 // ---------------------------------------------------------------------------
@@ -879,13 +1041,13 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         return LP_OK;
     }
     float plan_ms = 0.f;
-    if (int rc = build_plan(g, order, o->seed, &plan_ms)) return rc;
+    if (int rc = build_plan(g, kPlanRak, order, o->seed, &plan_ms)) return rc;
     const int64_t B = (o->batches == 0 || o->batches > n) ? n : o->batches;
     const int64_t bs = (n + B - 1) / B;
     const bool cross = bs < n;  // some vertex depends on an earlier batch
     if (int rc = ensure_flags(g, bs, &plan_ms)) return rc;
     S->plan_ms = plan_ms;
-    Plan& P = g->plan;
+    Plan& P = g->plan();
     cudaStream_t st = g->stream;
     round_fn run_round = nullptr;
     setup_fn setup = nullptr;
@@ -946,31 +1108,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         a.x = X;
         LP_CK(cudaMemcpyAsync(X, L0, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
         LP_CK(cudaMemsetAsync(g->counters + kCtrChanged, 0, 2 * sizeof(unsigned long long), st));
-        LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
-        int q = 0;  // this round's writes queue into mq[q]
-        a.mq_out = g->mq[q];
-        a.mq_len = g->mq_len + q;
-        LP_CK(cudaMemsetAsync(g->mq_len, 0, 2 * sizeof(int32_t), st));
-        run_round(g, a, true, g->h_len, &prof);
-        gathered += P.m_active;
-        ++rounds;
-        while (cross) {
-            // route last round's queue; this round's writes queue into the other one
-            LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
-            LP_CK(cudaMemsetAsync(g->mq_len + (q ^ 1), 0, sizeof(int32_t), st));
-            prof.begin(st, -1);
-            k_route_queue<<<g->num_sms * 4, 256, 0, st>>>(a, g->mq[q], g->mq_len + q, P.slot_of);
-            prof.end(st);
-            LP_CK(cudaMemcpyAsync(g->h_len, g->routes.len, kLenCount * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-            LP_CK(cudaStreamSynchronize(st));
-            if (g->h_len[kLenGather] == 0) break;
-            q ^= 1;
-            a.mq_out = g->mq[q];
-            a.mq_len = g->mq_len + q;
-            LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
-            run_round(g, a, false, g->h_len, &prof);
-            ++rounds;
-        }
+        if (int rc = solve_sweep(g, a, cross, run_round, kGatherRak, &prof, &rounds, &gathered)) return rc;
         LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, kCtrCount * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                               st));
         LP_CK(cudaStreamSynchronize(st));
@@ -986,29 +1124,8 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     LP_CK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
     g->cur = L0;
     g->labels_valid = true;
-    S->iterations = it;
-    S->rounds = rounds;
-    S->kernel_ms = ms;
+    if (int rc = finish_stats(g, prof, S, it, rounds, gathered, ms)) return rc;
     S->arcs_dense = g->m * it;
-    S->launches = prof.launches;
-    S->arcs_gathered = gathered + (int64_t)g->h_counters[kCtrGathered];
-    S->gather_launches = prof.slot_launches[kKGather];
-    for (int b = 0; b < kKSlots; ++b) {
-        S->bin_arcs[b] = (int64_t)g->h_counters[kCtrArcs + b];
-        S->bin_vertices[b] = (int64_t)g->h_counters[kCtrVerts + b];
-        S->bin_launches[b] = prof.slot_launches[b];
-        S->arcs_scanned += S->bin_arcs[b];
-    }
-    for (size_t i = 0; i < prof.tags.size(); ++i) {
-        float e = 0.f;
-        LP_CK(cudaEventElapsedTime(&e, g->event_pool[2 * i], g->event_pool[2 * i + 1]));
-        if (prof.tags[i] == kKGather)
-            S->gather_ms += e;
-        else if (prof.tags[i] >= 0)
-            S->bin_ms[prof.tags[i]] += e;
-        else
-            S->aux_ms += e;
-    }
     return LP_OK;
 }
 
@@ -1032,6 +1149,134 @@ extern "C" int lp_rak_run(lp_graph* g, const lp_rak_opts* opts, const int64_t* o
     if (!labels_out) return lp_fail(LP_ERR_INVALID, "labels_out is NULL");
     if (int rc = rak_core(g, opts, order, labels_init, changed_per_iter, stats)) return rc;
     return lp_labels_download(g, labels_out);
+}
+
+// ---------------------------------------------------------------------------
+// SLPA driver (slpa.py:91-111 _slpa_seq, :166-193 _detect_full)
+// ---------------------------------------------------------------------------
+// Round t = 1 .. T-1 is a RAK sweep over the INDEX plan (identity order, no
+// self arcs) with the SLPA phase-1 gather; the working array x starts from
+// a guess (the previous round's appends; own ids in round 1) and is solved
+// exactly under the batched schedule, then appended to the memories.
+extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_out, int64_t* slots_out,
+                           int64_t* repeats_per_iter, lp_run_stats* stats) {
+    if (!g || !o) return lp_fail(LP_ERR_INVALID, "NULL argument");
+    if (o->memory_size < 2) return lp_fail(LP_ERR_INVALID, "memory_size must be >= 2");
+    if (!(o->tolerance > 0.0 && o->tolerance <= 1.0)) return lp_fail(LP_ERR_INVALID, "tolerance must be in (0, 1]");
+    if (o->tie < 0 || o->tie > 2) return lp_fail(LP_ERR_INVALID, "unknown tie rule");
+    if (o->batches < 0) return lp_fail(LP_ERR_INVALID, "batches must be >= 0");
+    LP_CK(cudaSetDevice(g->device));
+    lp_run_stats st_local;
+    lp_run_stats* S = stats ? stats : &st_local;
+    memset(S, 0, sizeof(*S));
+    const int64_t n = g->n;
+    const int T = o->memory_size;
+    g->labels_valid = false;
+    if (n == 0) return LP_OK;
+    if ((double)n * T >= 2147483647.0 * 4) return lp_fail(LP_ERR_UNSUPPORTED, "memories too large");
+    float plan_ms = 0.f;
+    if (int rc = build_plan(g, kPlanIndex, nullptr, 0, &plan_ms)) return rc;
+    const int64_t B = (o->batches == 0 || o->batches > n) ? n : o->batches;
+    const int64_t bs = (n + B - 1) / B;
+    const bool cross = bs < n;
+    if (int rc = ensure_flags(g, bs, &plan_ms)) return rc;
+    S->plan_ms = plan_ms;
+    Plan& P = g->plan();
+    cudaStream_t st = g->stream;
+    round_fn run_round = nullptr;
+    setup_fn setup = nullptr;
+    if (g->wmode == kFixed)
+        pick_fns<kFixed>(o->tie, &run_round, &setup);
+    else if (g->wmode == kFloat)
+        pick_fns<kFloat>(o->tie, &run_round, &setup);
+    else
+        pick_fns<kUnit>(o->tie, &run_round, &setup);
+    LP_CK(setup(g->device));
+    const size_t cells = (size_t)n * T;
+    if (cells > g->slots_cap) {
+        cudaFree(g->slots);
+        g->slots = nullptr;
+        g->slots_cap = 0;
+        LP_CK(cudaMalloc(&g->slots, cells * sizeof(int32_t)));
+        g->slots_cap = cells;
+    }
+    int32_t* A = g->labA;  // previous appends (round 1: own ids, the guess)
+    int32_t* X = g->labB;  // working appends of this round
+    LP_CK(cudaMemsetAsync(g->slots, 0, cells * sizeof(int32_t), st));
+    k_slpa_init<<<g->num_sms * 8, 256, 0, st>>>(g->slots, A, n, T);
+    if (P.S > 0) k_reset_ndist<<<g->num_sms * 8, 256, 0, st>>>(P.soff, P.ndist, P.S);
+    LP_CK(cudaGetLastError());
+    EvalArgs a;
+    memset(&a, 0, sizeof(a));
+    a.soff = P.soff;
+    a.snbr = P.snbr;
+    a.sw = P.sw;
+    a.swsum = P.swsum;
+    a.svid = P.svid;
+    a.lbuf = P.lbuf;
+    a.mark = cross ? g->mark : nullptr;
+    a.ndist = P.ndist;
+    a.counters = g->counters;
+    a.r = g->routes;
+    a.seed = o->seed;
+    a.slots = g->slots;
+    a.T = T;
+    LP_CK(cudaMemsetAsync(g->counters, 0, kCtrCount * sizeof(unsigned long long), st));
+    unsigned long long* rep_ctr = g->counters + kCtrCount;  // spare counter slot
+    Prof prof;
+    prof.on = (o->flags & LP_RAK_PROFILE) != 0;
+    prof.pool = &g->event_pool;
+    LP_CK(cudaEventRecord(g->ev0, st));
+    int it = 0, rounds = 0;
+    int64_t gathered = 0;
+    for (int t = 1; t < T; ++t) {  // slpa.py:98
+        ++it;
+        a.sweep = (uint32_t)t;
+        a.L0 = A;
+        a.x = X;
+        LP_CK(cudaMemcpyAsync(X, A, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        LP_CK(cudaMemsetAsync(g->counters + kCtrChanged, 0, 2 * sizeof(unsigned long long), st));
+        if (P.S < n) {
+            prof.begin(st, -1);
+            k_slpa_idle<<<grid_for(n - P.S, 256, g->num_sms * 8), 256, 0, st>>>(P.svid, P.S, n, g->slots, T, t, X);
+            prof.end(st);
+        }
+        if (P.S > 0)
+            if (int rc = solve_sweep(g, a, cross, run_round, kGatherSlpa, &prof, &rounds, &gathered)) return rc;
+        LP_CK(cudaMemsetAsync(rep_ctr, 0, sizeof(unsigned long long), st));
+        prof.begin(st, -1);
+        k_slpa_commit<<<g->num_sms * 8, 256, 0, st>>>(X, A, g->slots, n, T, t, t >= 2 ? 1 : 0, rep_ctr);
+        prof.end(st);
+        LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, (kCtrCount + 1) * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, st));
+        LP_CK(cudaStreamSynchronize(st));
+        LP_CK(cudaGetLastError());
+        const int64_t repeats = (int64_t)g->h_counters[kCtrCount];
+        if (repeats_per_iter) repeats_per_iter[t - 1] = repeats;
+        std::swap(A, X);  // A = this round's appends (the next round's prev)
+        if (t >= 2 && (double)repeats >= (1.0 - o->tolerance) * (double)n) break;  // slpa.py:109-110
+    }
+    // projection (slpa.py:147-150) inside the timed region like the reference (:183-185)
+    if (labels_out) k_slpa_project<<<g->num_sms * 8, 256, 0, st>>>(g->slots, n, T, it + 1, g->out64);
+    LP_CK(cudaEventRecord(g->ev1, st));
+    LP_CK(cudaEventSynchronize(g->ev1));
+    float ms = 0.f;
+    LP_CK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+    if (int rc = finish_stats(g, prof, S, it, rounds, gathered, ms)) return rc;
+    if (labels_out) {
+        LP_CK(cudaMemcpyAsync(labels_out, g->out64, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        LP_CK(cudaStreamSynchronize(st));
+    }
+    if (slots_out) {
+        int64_t* tmp = nullptr;
+        LP_CK(cudaMalloc(&tmp, cells * sizeof(int64_t)));
+        k_slots_to64<<<g->num_sms * 8, 256, 0, st>>>(g->slots, tmp, (int64_t)cells);
+        cudaError_t e = cudaMemcpyAsync(slots_out, tmp, cells * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        cudaFree(tmp);
+        LP_CK(e);
+    }
+    return LP_OK;
 }
 
 extern "C" int lp_device_count(int32_t* count) {
@@ -1095,9 +1340,9 @@ __global__ void k_calib(const uint32_t* __restrict__ soff, const uint32_t* __res
 
 extern "C" int lp_calibrate(lp_graph* g, int32_t mode, int32_t reps, double* ms_out) {
     if (!g || !ms_out || reps < 1 || mode < 0 || mode > 5) return lp_fail(LP_ERR_INVALID, "bad arguments");
-    if (!g->plan.valid) return lp_fail(LP_ERR_INVALID, "run a detection first (plan needed)");
+    if (!g->plan().valid) return lp_fail(LP_ERR_INVALID, "run a detection first (plan needed)");
     LP_CK(cudaSetDevice(g->device));
-    const Plan& P = g->plan;
+    const Plan& P = g->plan();
     cudaStream_t st = g->stream;
     k_init_labels<<<g->num_sms * 8, 256, 0, st>>>(nullptr, g->labA, g->n);
     // mode 4/5: the same flat passes over the ORIGINAL CSR (vertex-id order)

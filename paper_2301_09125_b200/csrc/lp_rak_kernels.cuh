@@ -116,8 +116,13 @@ struct EvalArgs {
     Routes r;
     int32_t bin;  // counter slot of this launch
     uint32_t seed;
-    uint32_t sweep;
+    uint32_t sweep;                     // RAK: sweep number; SLPA: speaking round t
+    const int32_t* __restrict__ slots;  // SLPA memories [n x T] (slot t lives in x until the round ends)
+    int32_t T;
 };
+
+// phase-1 variants: what an arc's neighbour contributes to the tally
+enum GatherAlg : int { kGatherRak = 0, kGatherSlpa = 1 };
 
 // neighbour flags (low bits of snbr): the neighbour is in an earlier batch
 // (read its current-sweep label) / in a later batch (mark it when this
@@ -263,22 +268,27 @@ __global__ void __launch_bounds__(256) k_gather_dense(EvalArgs a, int64_t m) {
 // finds its piece by a 5-step search over the warp's prefix (shuffles only).
 constexpr int kPieceArcs = 256;
 
-__global__ void __launch_bounds__(256) k_gather_pieces(EvalArgs a) {
+template <int ALG>
+__global__ void __launch_bounds__(256) k_gather_pieces(EvalArgs a, const int32_t* __restrict__ gslot,
+                                                       const int32_t* __restrict__ gk0,
+                                                       const int32_t* __restrict__ count, int32_t* cursor) {
     constexpr int J = 8;
     const int lane = threadIdx.x & 31;
-    const int cnt = a.r.len[kLenGather];
+    const int cnt = *count;
     while (true) {
         int b0 = 0;
-        if (lane == 0) b0 = atomicAdd(a.r.len + kGatherCursor, 32);
+        if (lane == 0) b0 = atomicAdd(cursor, 32);
         b0 = __shfl_sync(0xffffffffu, b0, 0);
         if (b0 >= cnt) break;
-        uint32_t pbeg = 0, plen = 0;
+        uint32_t pbeg = 0, plen = 0, pk0 = 0;
+        int32_t pv = 0;
         if (b0 + lane < cnt) {
-            const int32_t s = a.r.gslot[b0 + lane];
-            const int32_t k0 = a.r.gk0[b0 + lane];
+            const int32_t s = gslot[b0 + lane];
+            pk0 = (uint32_t)gk0[b0 + lane];
             const uint32_t rb = __ldg(a.soff + s), re = __ldg(a.soff + s + 1);
-            pbeg = rb + (uint32_t)k0;
+            pbeg = rb + pk0;
             plen = min((uint32_t)kPieceArcs, re - pbeg);
+            if (ALG == kGatherSlpa) pv = __ldg(a.svid + s);
         }
         // inclusive prefix of piece lengths
         uint32_t incl = plen;
@@ -293,6 +303,8 @@ __global__ void __launch_bounds__(256) k_gather_pieces(EvalArgs a) {
         for (uint32_t base = 0; base < total; base += 32 * J) {
             uint32_t e[J];
             uint32_t nb[J];
+            uint32_t key[J];
+            int32_t lv[J];
 #pragma unroll
             for (int j = 0; j < J; ++j) {
                 const uint32_t i = base + j * 32 + lane;
@@ -305,12 +317,29 @@ __global__ void __launch_bounds__(256) k_gather_pieces(EvalArgs a) {
                 }
                 const uint32_t pb = __shfl_sync(0xffffffffu, pbeg, r);
                 const uint32_t pe = __shfl_sync(0xffffffffu, excl, r);
+                if (ALG == kGatherSlpa) {
+                    key[j] = __shfl_sync(0xffffffffu, pk0, r) + (i - pe);  // arc index within the row
+                    lv[j] = __shfl_sync(0xffffffffu, pv, r);
+                }
                 e[j] = i < total ? pb + (i - pe) : 0xffffffffu;
                 nb[j] = i < total ? __ldg(a.snbr + e[j]) : 0u;
             }
 #pragma unroll
-            for (int j = 0; j < J; ++j)
-                if (e[j] != 0xffffffffu) a.lbuf[e[j]] = gather_label(a, nb[j]);
+            for (int j = 0; j < J; ++j) {
+                if (e[j] == 0xffffffffu) continue;
+                if (ALG == kGatherRak) {
+                    a.lbuf[e[j]] = gather_label(a, nb[j]);
+                } else {
+                    // slpa.py:76-77: the speaker u says slots[u, draw(filled[u])]; u has
+                    // t + 1 filled slots if it is in an earlier batch (it already
+                    // listened and appended this round), else t.
+                    const int32_t u = (int32_t)(nb[j] >> 2);
+                    const uint32_t t = a.sweep;
+                    const uint32_t filled = t + ((nb[j] & kEarlier) ? 1u : 0u);
+                    const uint32_t q = speak_hash(a.seed, t, (uint32_t)lv[j], key[j]) % filled;
+                    a.lbuf[e[j]] = q == t ? a.x[u] : __ldg(a.slots + (size_t)u * a.T + q);
+                }
+            }
         }
     }
 }

@@ -111,3 +111,25 @@ def test_reference_test_graphs_match_reference_fixtures(golden_rak):
                      ("gnp_400", lambda: lp.gnp(400, 0.02, seed=2)), ("gnp_3000", lambda: lp.gnp(3000, 0.005, seed=6)),
                      ("star_50", lambda: lp.star(50)), ("path_100", lambda: lp.path(100))):
         assert G.graphs_equal(mk(), load_graph(golden_rak, name)), name
+
+
+def test_most_popular_label_reference_cases():
+    # pkg/tests/test_slpa.py:82-96
+    assert lp.most_popular_label([5, 5, 3]) == 5
+    assert lp.most_popular_label([5, 3]) == 3
+    assert lp.most_popular_label([7]) == 7
+    with pytest.raises(ValueError):
+        lp.most_popular_label([])
+
+
+def test_slpa_params_validation():
+    # slpa.py:42-48
+    with pytest.raises(ValueError):
+        lp.SlpaParams(memory_size=1)
+    with pytest.raises(ValueError):
+        lp.SlpaParams(tolerance=0.0)
+    with pytest.raises(ValueError):
+        lp.SlpaParams(workers=0)
+    with pytest.raises(ValueError):
+        lp.SlpaParams(batches=-1)
+    assert lp.SlpaParams().tie_rule == "random" and lp.SlpaParams(strict=True).tie_rule == "scan-first"
