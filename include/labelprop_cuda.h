@@ -103,6 +103,18 @@ typedef struct lp_slpa_opts {
     int64_t reserved[6];
 } lp_slpa_opts;
 
+/* COPRA (copra.py CopraParams :34-50).  Sweeps over the identity visit
+ * order (copra.py:134), self arcs skipped (:137-139). */
+typedef struct lp_copra_opts {
+    double tolerance;       /* (0, 1]; stop when best labels changed <= tolerance * n */
+    int32_t max_labels;     /* k in 1 .. 32                                  */
+    int32_t max_iterations; /* >= 1                                          */
+    int64_t batches;        /* 0 or n = the reference's in-place sweep; 1 = synchronous */
+    uint32_t seed;          /* fallback ties (counter RNG)                   */
+    int32_t flags;          /* LP_RAK_PROFILE                                */
+    int64_t reserved[6];
+} lp_copra_opts;
+
 /* Kernel slots of the engine, index of the lp_run_stats
  * bin_* arrays.  A vertex is routed each round by its degree d and its
  * estimated distinct neighbour labels. */
@@ -161,6 +173,16 @@ int lp_labels_download(lp_graph* g, int64_t* labels_out);
  * holds stats->iterations + 1 labels.  repeats_per_iter: NULL or T-1. */
 int lp_slpa_run(lp_graph* g, const lp_slpa_opts* opts, int64_t* labels_out, int64_t* slots_out,
                 int64_t* repeats_per_iter, lp_run_stats* stats);
+
+/* COPRA: replaces _copra_seq/_copra_par (copra.py:124-237).  best_out[n]
+ * (required): the best label per vertex (the disjoint projection);
+ * labs_out[n*k] / bels_out[n*k] (both or neither): label sets sorted by
+ * label, belongings float64, entries past sizes_out[v] zero; sizes_out[n]
+ * optional.  changed_per_iter: NULL or max_iterations entries.  Belongings
+ * use float64 arithmetic in the reference's order (bit-exact to the CPU
+ * restatement of the same schedule). */
+int lp_copra_run(lp_graph* g, const lp_copra_opts* opts, int64_t* labs_out, double* bels_out, int64_t* sizes_out,
+                 int64_t* best_out, int64_t* changed_per_iter, lp_run_stats* stats);
 
 /* Calibration (device time per pass, ms): mode 0 streams the neighbour
  * indices of the active rows once; mode 1 also gathers every neighbour's

@@ -72,6 +72,18 @@ class SlpaOpts(C.Structure):
     ]
 
 
+class CopraOpts(C.Structure):
+    _fields_ = [
+        ("tolerance", C.c_double),
+        ("max_labels", C.c_int32),
+        ("max_iterations", C.c_int32),
+        ("batches", C.c_int64),
+        ("seed", C.c_uint32),
+        ("flags", C.c_int32),
+        ("reserved", C.c_int64 * 6),
+    ]
+
+
 RAK_PROFILE = 1
 BIN_NAMES = ("hub", "team", "warp", "small")
 
@@ -117,6 +129,7 @@ EXPORTS = (
     "lp_rak_run_resident",
     "lp_labels_download",
     "lp_slpa_run",
+    "lp_copra_run",
     "lp_calibrate",
     "lp_shuffled_indices",
     "lp_gen_rmat",
@@ -160,6 +173,7 @@ def lib():
     L.lp_rak_run.argtypes = [vp, C.POINTER(RakOpts), vp, vp, vp, vp, C.POINTER(RunStats)]
     L.lp_rak_run_resident.argtypes = [vp, C.POINTER(RakOpts), vp, C.POINTER(RunStats)]
     L.lp_labels_download.argtypes = [vp, vp]
+    L.lp_copra_run.argtypes = [vp, C.POINTER(CopraOpts), vp, vp, vp, vp, vp, C.POINTER(RunStats)]
     L.lp_slpa_run.argtypes = [vp, C.POINTER(SlpaOpts), vp, vp, vp, C.POINTER(RunStats)]
     L.lp_calibrate.argtypes = [vp, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
     L.lp_shuffled_indices.argtypes = [C.c_int64, C.c_uint32, _i64p]

@@ -36,6 +36,7 @@
 #include "lp_host.h"
 #include "lp_rak_kernels.cuh"
 #include "lp_slpa_kernels.cuh"
+#include "lp_copra_kernels.cuh"
 
 using namespace lp;
 
@@ -122,6 +123,19 @@ struct lp_graph {
     int32_t* mq_len = nullptr;  // their lengths [2]
     int32_t* slots = nullptr;   // SLPA memories [n x T]
     size_t slots_cap = 0;
+    // COPRA label sets (sweep-start and working), [n x K] rows
+    int32_t* clabs[2] = {nullptr, nullptr};
+    double* cbels[2] = {nullptr, nullptr};
+    int32_t* csize[2] = {nullptr, nullptr};
+    int32_t* cbest[2] = {nullptr, nullptr};
+    size_t ccap = 0;            // cells (n * K) the label-set buffers hold
+    int32_t* ccur = nullptr;    // work cursors [4]
+    int32_t* cbig = nullptr;    // spill list [n]
+    int32_t* gkeys = nullptr;   // big-table scratch
+    double* gvals = nullptr;
+    int32_t* gtl = nullptr;
+    uint32_t gbits = 0;
+    int gblocks = 0;
     Routes routes;
     int64_t cap_items = 0;
     unsigned long long* counters = nullptr;
@@ -606,6 +620,17 @@ static void destroy_graph(lp_graph* g) {
     cudaFree(g->mq[1]);
     cudaFree(g->mq_len);
     cudaFree(g->slots);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(g->clabs[i]);
+        cudaFree(g->cbels[i]);
+        cudaFree(g->csize[i]);
+        cudaFree(g->cbest[i]);
+    }
+    cudaFree(g->ccur);
+    cudaFree(g->cbig);
+    cudaFree(g->gkeys);
+    cudaFree(g->gvals);
+    cudaFree(g->gtl);
     cudaFree(g->off);
     cudaFree(g->nbr);
     cudaFree(g->w);
@@ -1195,6 +1220,17 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     const size_t cells = (size_t)n * T;
     if (cells > g->slots_cap) {
         cudaFree(g->slots);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(g->clabs[i]);
+        cudaFree(g->cbels[i]);
+        cudaFree(g->csize[i]);
+        cudaFree(g->cbest[i]);
+    }
+    cudaFree(g->ccur);
+    cudaFree(g->cbig);
+    cudaFree(g->gkeys);
+    cudaFree(g->gvals);
+    cudaFree(g->gtl);
         g->slots = nullptr;
         g->slots_cap = 0;
         LP_CK(cudaMalloc(&g->slots, cells * sizeof(int32_t)));
@@ -1276,6 +1312,231 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
         cudaFree(tmp);
         LP_CK(e);
     }
+    return LP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// COPRA driver (copra.py:124-176 _copra_seq, :240-283 _detect_full)
+// ---------------------------------------------------------------------------
+static int copra_buffers(lp_graph* g, int K) {
+    const int64_t n = g->n;
+    const size_t cells = (size_t)n * K;
+    if (cells > g->ccap) {
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(g->clabs[i]);
+            cudaFree(g->cbels[i]);
+            g->clabs[i] = nullptr;
+            g->cbels[i] = nullptr;
+        }
+        g->ccap = 0;
+        for (int i = 0; i < 2; ++i) {
+            LP_CK(cudaMalloc(&g->clabs[i], cells * sizeof(int32_t)));
+            LP_CK(cudaMalloc(&g->cbels[i], cells * sizeof(double)));
+        }
+        g->ccap = cells;
+    }
+    if (!g->csize[0]) {
+        for (int i = 0; i < 2; ++i) {
+            LP_CK(cudaMalloc(&g->csize[i], std::max<int64_t>(n, 1) * sizeof(int32_t)));
+            LP_CK(cudaMalloc(&g->cbest[i], std::max<int64_t>(n, 1) * sizeof(int32_t)));
+        }
+        LP_CK(cudaMalloc(&g->ccur, 4 * sizeof(int32_t)));
+        LP_CK(cudaMalloc(&g->cbig, std::max<int64_t>(n, 1) * sizeof(int32_t)));
+    }
+    // big tables: 2^gbits >= 2 * (the most distinct labels a row can see), so the
+    // big kernel never overflows; blocks bounded by a 4 GiB scratch budget
+    const double most = std::min<double>((double)n, (double)g->max_degree * K);
+    uint32_t bits = 8;
+    while ((double)(1u << bits) < 2.0 * most + 64.0) ++bits;
+    if (bits > g->gbits) {
+        cudaFree(g->gkeys);
+        cudaFree(g->gvals);
+        cudaFree(g->gtl);
+        g->gkeys = nullptr;
+        g->gvals = nullptr;
+        g->gtl = nullptr;
+        g->gbits = 0;
+        const size_t per = ((size_t)1 << bits) * (sizeof(int32_t) * 2 + sizeof(double));
+        const int blocks = (int)std::max<size_t>(1, std::min<size_t>(g->num_sms, ((size_t)4 << 30) / per));
+        const size_t slots = ((size_t)1 << bits) * blocks;
+        LP_CK(cudaMalloc(&g->gkeys, slots * sizeof(int32_t)));
+        LP_CK(cudaMalloc(&g->gvals, slots * sizeof(double)));
+        LP_CK(cudaMalloc(&g->gtl, slots * sizeof(int32_t)));
+        k_copra_gtab_init<<<g->num_sms * 8, 256, 0, g->stream>>>(g->gkeys, g->gvals, (int64_t)slots);
+        LP_CK(cudaGetLastError());
+        g->gbits = bits;
+        g->gblocks = blocks;
+    }
+    return LP_OK;
+}
+
+static size_t copra_smem_bytes() {
+    return (size_t)kCopraWarps * (1 << kCopraBits) * (sizeof(double) + 2 * sizeof(int32_t)) +
+           kCopraWarps * sizeof(CopraWarpSmem);
+}
+
+extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_out, double* bels_out,
+                            int64_t* sizes_out, int64_t* best_out, int64_t* changed_per_iter, lp_run_stats* stats) {
+    if (!g || !o) return lp_fail(LP_ERR_INVALID, "NULL argument");
+    if (!(o->tolerance > 0.0 && o->tolerance <= 1.0)) return lp_fail(LP_ERR_INVALID, "tolerance must be in (0, 1]");
+    if (o->max_labels < 1) return lp_fail(LP_ERR_INVALID, "max_labels must be >= 1");
+    if (o->max_iterations < 1) return lp_fail(LP_ERR_INVALID, "max_iterations must be >= 1");
+    if (o->batches < 0) return lp_fail(LP_ERR_INVALID, "batches must be >= 0");
+    if (o->max_labels > kCopraMaxLabels) return lp_fail(LP_ERR_UNSUPPORTED, "max_labels > 32 is not supported on the GPU");
+    if (!best_out) return lp_fail(LP_ERR_INVALID, "best_out is NULL");
+    if ((labs_out == nullptr) != (bels_out == nullptr)) return lp_fail(LP_ERR_INVALID, "labs_out and bels_out go together");
+    LP_CK(cudaSetDevice(g->device));
+    lp_run_stats st_local;
+    lp_run_stats* S = stats ? stats : &st_local;
+    memset(S, 0, sizeof(*S));
+    const int64_t n = g->n;
+    const int K = o->max_labels;
+    g->labels_valid = false;
+    if (n == 0) return LP_OK;
+    if ((double)n * K >= 2147483647.0) return lp_fail(LP_ERR_UNSUPPORTED, "n * max_labels must be < 2^31");
+    float plan_ms = 0.f;
+    if (int rc = build_plan(g, kPlanIndex, nullptr, 0, &plan_ms)) return rc;
+    const int64_t B = (o->batches == 0 || o->batches > n) ? n : o->batches;
+    const int64_t bs = (n + B - 1) / B;
+    const bool cross = bs < n;
+    if (int rc = ensure_flags(g, bs, &plan_ms)) return rc;
+    S->plan_ms = plan_ms;
+    if (int rc = copra_buffers(g, K)) return rc;
+    Plan& P = g->plan();
+    cudaStream_t st = g->stream;
+    static int smem_set_device = -1;
+    if (smem_set_device != g->device) {
+        LP_CK(cudaFuncSetAttribute(k_copra_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)copra_smem_bytes()));
+        smem_set_device = g->device;
+    }
+    int occ = 1;
+    LP_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_copra_warp, kCopraWarps * 32, copra_smem_bytes()));
+    occ = std::max(occ, 1);
+    int c0 = 0, c1 = 1;  // L0 / X buffer index
+    k_copra_init<<<g->num_sms * 8, 256, 0, st>>>(g->clabs[c0], g->cbels[c0], g->csize[c0], g->cbest[c0], n, K);
+    if (P.S > 0) k_reset_ndist<<<g->num_sms * 8, 256, 0, st>>>(P.soff, P.ndist, P.S);
+    LP_CK(cudaGetLastError());
+    CopraArgs a;
+    memset(&a, 0, sizeof(a));
+    a.soff = P.soff;
+    a.snbr = P.snbr;
+    a.sw = P.sw;
+    a.wmode = g->wmode;
+    a.shift = g->fixed_shift;
+    a.svid = P.svid;
+    a.slot_of = P.slot_of;
+    a.K = K;
+    a.ndist = P.ndist;
+    a.mark = cross ? g->mark : nullptr;
+    a.S = (int32_t)P.S;
+    a.cursor = g->ccur;
+    a.big_len = g->ccur + 1;
+    a.big_cursor = g->ccur + 2;
+    a.big = g->cbig;
+    a.gkeys = g->gkeys;
+    a.gvals = g->gvals;
+    a.gtl = g->gtl;
+    a.gbits = g->gbits;
+    a.counters = g->counters;
+    a.seed = o->seed;
+    Prof prof;
+    prof.on = (o->flags & LP_RAK_PROFILE) != 0;
+    prof.pool = &g->event_pool;
+    LP_CK(cudaMemsetAsync(g->counters, 0, kCtrCount * sizeof(unsigned long long), st));
+    LP_CK(cudaEventRecord(g->ev0, st));
+    int it = 0, rounds = 0;
+    auto launch = [&](int64_t work) -> int {
+        LP_CK(cudaMemsetAsync(g->ccur, 0, 4 * sizeof(int32_t), st));
+        prof.begin(st, kKWarp);
+        k_copra_warp<<<grid_for(work, kCopraWarps, g->num_sms * occ), kCopraWarps * 32, copra_smem_bytes(), st>>>(a);
+        prof.end(st);
+        prof.begin(st, kKHub);
+        k_copra_big<<<g->gblocks, 32, 0, st>>>(a);
+        prof.end(st);
+        ++rounds;
+        return LP_OK;
+    };
+    const size_t cells = (size_t)n * K;
+    while (it < o->max_iterations) {
+        ++it;
+        a.sweep = (uint32_t)it;
+        a.labs0 = g->clabs[c0];
+        a.bels0 = g->cbels[c0];
+        a.size0 = g->csize[c0];
+        a.labsX = g->clabs[c1];
+        a.belsX = g->cbels[c1];
+        a.sizeX = g->csize[c1];
+        a.bestX = g->cbest[c1];
+        LP_CK(cudaMemcpyAsync(g->clabs[c1], g->clabs[c0], cells * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        LP_CK(cudaMemcpyAsync(g->cbels[c1], g->cbels[c0], cells * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        LP_CK(cudaMemcpyAsync(g->csize[c1], g->csize[c0], n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        LP_CK(cudaMemcpyAsync(g->cbest[c1], g->cbest[c0], n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        // dense round over every active slot
+        int q = 0;
+        a.queue = nullptr;
+        a.queue_len = nullptr;
+        a.mq_out = g->mq[q];
+        a.mq_len = g->mq_len + q;
+        LP_CK(cudaMemsetAsync(g->mq_len, 0, 2 * sizeof(int32_t), st));
+        if (P.S > 0)
+            if (int rc = launch(P.S)) return rc;
+        while (cross && P.S > 0) {
+            prof.begin(st, -1);
+            k_clear_marks<<<g->num_sms * 4, 256, 0, st>>>(g->mq[q], g->mq_len + q, g->mark);
+            prof.end(st);
+            LP_CK(cudaMemcpyAsync(g->h_len, g->mq_len + q, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            LP_CK(cudaStreamSynchronize(st));
+            const int32_t work = g->h_len[0];
+            if (work == 0) break;
+            a.queue = g->mq[q];
+            a.queue_len = g->mq_len + q;
+            a.mq_out = g->mq[q ^ 1];
+            a.mq_len = g->mq_len + (q ^ 1);
+            LP_CK(cudaMemsetAsync(g->mq_len + (q ^ 1), 0, sizeof(int32_t), st));
+            if (int rc = launch(work)) return rc;
+            q ^= 1;
+        }
+        LP_CK(cudaMemsetAsync(g->counters + kCtrChanged, 0, sizeof(unsigned long long), st));
+        k_count_changed<<<g->num_sms * 8, 256, 0, st>>>(g->cbest[c0], g->cbest[c1], n, g->counters + kCtrChanged);
+        LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, kCtrCount * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, st));
+        LP_CK(cudaStreamSynchronize(st));
+        LP_CK(cudaGetLastError());
+        const int64_t changed = (int64_t)g->h_counters[kCtrChanged];
+        if (changed_per_iter) changed_per_iter[it - 1] = changed;
+        std::swap(c0, c1);  // c0 = this sweep's state
+        if ((double)changed <= o->tolerance * (double)n) break;  // copra.py:174-175
+    }
+    LP_CK(cudaEventRecord(g->ev1, st));
+    LP_CK(cudaEventSynchronize(g->ev1));
+    float ms = 0.f;
+    LP_CK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+    if (int rc = finish_stats(g, prof, S, it, rounds, 0, ms)) return rc;
+    // download (int64 / float64 like the reference's arrays)
+    int64_t* l64 = nullptr;
+    double* b64 = nullptr;
+    int64_t* s64 = nullptr;
+    int64_t* best64 = g->out64;
+    cudaError_t e = cudaSuccess;
+    if (labs_out) {
+        e = cudaMalloc(&l64, cells * sizeof(int64_t));
+        if (e == cudaSuccess) e = cudaMalloc(&b64, cells * sizeof(double));
+    }
+    if (e == cudaSuccess && sizes_out) e = cudaMalloc(&s64, n * sizeof(int64_t));
+    if (e == cudaSuccess) {
+        k_copra_download<<<g->num_sms * 8, 256, 0, st>>>(g->clabs[c0], g->cbels[c0], g->csize[c0], g->cbest[c0], l64,
+                                                        b64, s64, best64, n, K, K);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(best_out, best64, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && labs_out) e = cudaMemcpyAsync(labs_out, l64, cells * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && labs_out) e = cudaMemcpyAsync(bels_out, b64, cells * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && sizes_out) e = cudaMemcpyAsync(sizes_out, s64, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(l64);
+    cudaFree(b64);
+    cudaFree(s64);
+    LP_CK(e);
     return LP_OK;
 }
 

@@ -222,7 +222,8 @@ __device__ __forceinline__ bool commit_label_known(const EvalArgs& a, int32_t v,
 // Mark the later-batch neighbours of a vertex whose label changed; a vertex
 // marked for the first time this round joins the mark queue (warp-aggregated
 // append), so the next round routes only the queue instead of scanning n.
-__device__ __forceinline__ void mark_row(const EvalArgs& a, uint32_t beg, int d, int from, int step) {
+template <typename Args>
+__device__ __forceinline__ void mark_row(const Args& a, uint32_t beg, int d, int from, int step) {
     const int lane = threadIdx.x & 31;
     for (int k = from; k < d; k += step) {
         const uint32_t nb = __ldg(a.snbr + beg + k);

@@ -133,3 +133,42 @@ def test_slpa_params_validation():
     with pytest.raises(ValueError):
         lp.SlpaParams(batches=-1)
     assert lp.SlpaParams().tie_rule == "random" and lp.SlpaParams(strict=True).tie_rule == "scan-first"
+
+
+def test_collect_and_threshold_reference_cases():
+    # pkg/tests/test_copra.py:68-110
+    labels, bels = lp.collect_and_threshold([10, 20], [0.6, 0.4], 4, lp.XorShift32(1))
+    assert labels.tolist() == [10, 20] and bels.tolist() == pytest.approx([0.6, 0.4])
+    labels, bels = lp.collect_and_threshold([1, 2, 3], [0.5, 0.3, 0.2], 4, lp.XorShift32(1))
+    assert labels.tolist() == [1, 2] and bels.tolist() == pytest.approx([0.625, 0.375])
+    seen = set()
+    rng = lp.XorShift32(5)
+    for _ in range(200):
+        labels, bels = lp.collect_and_threshold([0, 1, 2, 3, 4], [0.2] * 5, 4, rng)
+        assert labels.size == 1 and bels.tolist() == [1.0]
+        seen.add(int(labels[0]))
+    assert seen == {0, 1, 2, 3, 4}
+    labels, bels = lp.collect_and_threshold([0, 2], [1.0, 1.0], 2, lp.XorShift32(1))
+    assert labels.tolist() == [0, 2] and bels.tolist() == pytest.approx([0.5, 0.5])
+    labels, _ = lp.collect_and_threshold([9, 1, 5], [0.4, 0.3, 0.3], 4, lp.XorShift32(1))
+    assert labels.tolist() == sorted(labels.tolist())
+    with pytest.raises(ValueError):
+        lp.collect_and_threshold([], [], 4, lp.XorShift32(1))
+
+
+def test_best_label_reference_cases():
+    # pkg/tests/test_copra.py:113-126
+    assert lp.best_label([7, 2], [0.6, 0.4]) == 7
+    assert lp.best_label([7, 2], [0.5, 0.5]) == 2
+    assert lp.best_label([3], [1.0]) == 3
+    with pytest.raises(ValueError):
+        lp.best_label([], [])
+
+
+def test_copra_params_validation():
+    # copra.py:42-50
+    for bad in (dict(max_labels=0), dict(tolerance=0.0), dict(workers=0), dict(max_iterations=0), dict(batches=-1)):
+        with pytest.raises(ValueError):
+            lp.CopraParams(**bad)
+    p = lp.CopraParams()
+    assert (p.tolerance, p.max_labels, p.max_iterations, p.workers, p.seed) == (0.01, 8, 100, 1, 1)
