@@ -65,11 +65,20 @@ struct CopraArgs {
     int32_t* big;                       // slots whose tables exceed the warp table
     int32_t* big_len;
     int32_t* big_cursor;
-    // big-table scratch (per block of the big kernel)
-    int32_t* gkeys;
-    double* gvals;
-    int32_t* gtl;
-    uint32_t gbits;
+    // team scratch (per block of the team kernel): entries, first-touch order, contribution map
+    int32_t* gelab;
+    double* geval;
+    int32_t* gefirst;
+    int32_t* grlab;
+    double* grval;
+    int32_t* gfmap;     // [gcap_contrib] per block, -1 between uses
+    int32_t* gblab;     // [gcap_contrib] per block: bucketed contributions
+    double* gbval;
+    int32_t* gbc;
+    int32_t* gwc;       // [W x kCopraMaxParts] per block: partition counts / offsets
+    int32_t* gqs;       // [kCopraMaxParts + 1] per block: bucket starts
+    size_t gcap_entries;
+    size_t gcap_contrib;
     unsigned long long* counters;
     uint32_t seed;
     uint32_t sweep;
@@ -89,33 +98,28 @@ __device__ __forceinline__ double shfl_f64(double x, int src) {
     return __longlong_as_double(((long long)hi << 32) | (unsigned int)lo);
 }
 
-// Per-warp evaluation scratch (shared memory for the warp kernel).
+// Per-warp evaluation scratch.
 struct CopraWarpSmem {
     double stage[32];
     int32_t outl[kCopraMaxLabels];
     double outb[kCopraMaxLabels];
 };
 
-// Evaluate one vertex (slot s) with the whole warp into a table of 2^bits
-// slots (keys kEmpty, vals 0 on entry; restored on exit).  Returns false if
-// the distinct labels exceeded `limit` (nothing written).
-__device__ bool copra_eval(const CopraArgs& a, int32_t s, int32_t* keys, double* vals, int32_t* tl, uint32_t bits,
-                           int limit, CopraWarpSmem& sm) {
+// Walk the contributions (label, bels[u,j] * w) of arcs [k_lo, k_hi) of row
+// s in scan order (copra.py:135-146), 32 at a time; fn(lab, val, c, valid)
+// is called by the whole warp per chunk, c = contribution index from k_lo.
+template <class Fn>
+__device__ __forceinline__ void for_each_contribution(const CopraArgs& a, int32_t s, int k_lo, int k_hi, Fn fn) {
     const int lane = threadIdx.x & 31;
-    const uint32_t mask = (1u << bits) - 1u;
-    const int32_t v = __ldg(a.svid + s);
     const uint32_t beg = __ldg(a.soff + s);
-    const int d = (int)(__ldg(a.soff + s + 1) - beg);
     const int K = a.K;
-    int cnt = 0;
-    bool overflow = false;
-    // ---- tally (copra.py:135-146) ----
-    for (int k0 = 0; k0 < d && !overflow; k0 += 32) {
+    int cbase = 0;
+    for (int k0 = k_lo; k0 < k_hi; k0 += 32) {
         const int k = k0 + lane;
         uint32_t nb = 0;
         int su = 0;
         double w = 0.0;
-        if (k < d) {
+        if (k < k_hi) {
             nb = __ldg(a.snbr + beg + k);
             const int32_t u = (int32_t)(nb >> 2);
             su = (nb & kEarlier) ? *((volatile int32_t*)a.sizeX + u) : __ldg(a.size0 + u);
@@ -156,80 +160,107 @@ __device__ bool copra_eval(const CopraArgs& a, int32_t s, int32_t* keys, double*
                 }
                 val = __dmul_rn(bel, wr);  // bels[u, j] * w, rounded (copra.py:146)
             }
-            sm.stage[lane] = val;
-            const uint32_t grp = __match_any_sync(0xffffffffu, lab);
-            const bool leader = lab != kEmpty && (__ffs(grp) - 1) == lane;
-            int slot = -1;
-            bool isnew = false;
-            if (leader) {
-                uint32_t h = slot_hash(lab, bits);
-                while (true) {
-                    const int32_t key = keys[h];
-                    if (key == lab) {
-                        slot = (int)h;
-                        break;
-                    }
-                    if (key == kEmpty) {
-                        const int32_t prev = atomicCAS(keys + h, kEmpty, lab);
-                        if (prev == kEmpty) {
-                            slot = (int)h;
-                            isnew = true;
-                            break;
-                        }
-                        if (prev == lab) {
-                            slot = (int)h;
-                            break;
-                        }
-                    }
-                    h = (h + 1) & mask;
-                }
-            }
-            const uint32_t nbal = __ballot_sync(0xffffffffu, isnew);
-            if (isnew) tl[cnt + __popc(nbal & lanemask_lt())] = slot;
-            cnt += __popc(nbal);
-            __syncwarp();
-            if (leader) {
-                double acc = vals[slot];
-                for (uint32_t m = grp; m; m &= m - 1) acc = __dadd_rn(acc, sm.stage[__ffs(m) - 1]);
-                vals[slot] = acc;
-            }
-            __syncwarp();
-            if (cnt > limit) {
-                overflow = true;
+            fn(lab, val, cbase + c, c < tot);
+        }
+        cbase += tot;
+    }
+}
+
+// Add one chunk of up to 32 contributions (lab kEmpty = none) to a warp's
+// table of 2^bits slots, in lane order: each label's lowest lane inserts
+// it (new labels join the touched list tl in lane order) and adds the
+// group's values one by one.  cnt (warp-uniform) = distinct labels so far.
+__device__ __forceinline__ void tally_chunk(int32_t lab, double val, int c, int32_t* keys, double* vals,
+                                            int32_t* firsts, int32_t* tl, uint32_t bits, int& cnt, double* stage) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t mask = (1u << bits) - 1u;
+    stage[lane] = val;
+    const uint32_t grp = __match_any_sync(0xffffffffu, lab);
+    const bool leader = lab != kEmpty && (__ffs(grp) - 1) == lane;
+    int slot = -1;
+    bool isnew = false;
+    if (leader) {
+        uint32_t h = slot_hash(lab, bits);
+        while (true) {
+            const int32_t key = keys[h];
+            if (key == lab) {
+                slot = (int)h;
                 break;
             }
+            if (key == kEmpty) {
+                const int32_t prev = atomicCAS(keys + h, kEmpty, lab);
+                if (prev == kEmpty) {
+                    slot = (int)h;
+                    isnew = true;
+                    break;
+                }
+                if (prev == lab) {
+                    slot = (int)h;
+                    break;
+                }
+            }
+            h = (h + 1) & mask;
         }
     }
-    if (overflow) {
-        for (int i = lane; i < cnt; i += 32) {
-            const int sl = tl[i];
-            keys[sl] = kEmpty;
-            vals[sl] = 0.0;
+    const uint32_t nbal = __ballot_sync(0xffffffffu, isnew);
+    if (isnew) {
+        tl[cnt + __popc(nbal & lanemask_lt())] = slot;
+        if (firsts) firsts[slot] = c;
+    }
+    cnt += __popc(nbal);
+    __syncwarp();
+    if (leader) {
+        double acc = vals[slot];
+        for (uint32_t m = grp; m; m &= m - 1) acc = __dadd_rn(acc, stage[__ffs(m) - 1]);
+        vals[slot] = acc;
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void table_restore(int32_t* keys, double* vals, const int32_t* tl, int cnt) {
+    const int lane = threadIdx.x & 31;
+    for (int i = lane; i < cnt; i += 32) {
+        const int sl = tl[i];
+        keys[sl] = kEmpty;
+        vals[sl] = 0.0;
+    }
+    __syncwarp();
+}
+
+// Phase 2 (one warp): _select_labels + _best_of_row over the distinct
+// labels in first-touch order (get(i) -> label, tally), then compare with
+// the working state; write and mark later-batch neighbours on change.
+template <class Get>
+__device__ void copra_finish(const CopraArgs& a, int32_t s, int cnt, Get get, CopraWarpSmem& sm) {
+    const int lane = threadIdx.x & 31;
+    const int32_t v = __ldg(a.svid + s);
+    const uint32_t beg = __ldg(a.soff + s);
+    const int d = (int)(__ldg(a.soff + s + 1) - beg);
+    const int K = a.K;
+    // total (copra.py:59-61): serial in touched order; the warp loads 32
+    // tallies at a time and every lane runs the same serial sum
+    double total = 0.0;
+    for (int i0 = 0; i0 < cnt; i0 += 32) {
+        double w = 0.0;
+        if (i0 + lane < cnt) {
+            int32_t l;
+            get(i0 + lane, l, w);
         }
-        __syncwarp();
-        return false;
+        const int m = min(32, cnt - i0);
+        for (int j = 0; j < m; ++j) total = __dadd_rn(total, shfl_f64(w, j));
     }
-    // ---- _select_labels (copra.py:53-108) ----
-    double total = 0.0;  // serial, touched order (:59-61)
-    if (lane == 0) {
-#pragma unroll 4
-        for (int i = 0; i < cnt; ++i) total = __dadd_rn(total, vals[tl[i]]);
-    }
-    total = shfl_f64(total, 0);
-    int kk = 0;  // kept so far (:64-71): first <= K labels with tally*K >= total, touched order
+    int kk = 0;  // (:64-71): first <= K labels with tally * K >= total, touched order
     for (int i0 = 0; i0 < cnt && kk < K; i0 += 32) {
         const int i = i0 + lane;
-        bool q = false;
+        bool qual = false;
         int32_t lab = 0;
         double w = 0.0;
         if (i < cnt) {
-            const int sl = tl[i];
-            w = vals[sl];
-            lab = keys[sl];
-            q = __dmul_rn(w, (double)K) >= total;
+            get(i, lab, w);
+            qual = __dmul_rn(w, (double)K) >= total;
         }
-        const uint32_t bal = __ballot_sync(0xffffffffu, q);
-        if (q) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, qual);
+        if (qual) {
             const int rank = kk + __popc(bal & lanemask_lt());
             if (rank < K) {
                 sm.outl[rank] = lab;
@@ -255,19 +286,26 @@ __device__ bool copra_eval(const CopraArgs& a, int32_t s, int32_t* keys, double*
         // nothing qualifies: one maximum-weight label, belonging 1 (:72-93); among
         // tied maxima the largest counter hash wins (first in touched order on equal hashes)
         double bw = -1.0;
-        for (int i = lane; i < cnt; i += 32) bw = fmax(bw, vals[tl[i]]);
+        for (int i = lane; i < cnt; i += 32) {
+            int32_t l;
+            double w;
+            get(i, l, w);
+            bw = fmax(bw, w);
+        }
 #pragma unroll
         for (int m = 16; m >= 1; m >>= 1) bw = fmax(bw, __shfl_xor_sync(0xffffffffu, bw, m));
         uint32_t bh = 0, bpos = 0xffffffffu;
         int32_t blab = kEmpty;
         for (int i = lane; i < cnt; i += 32) {
-            const int sl = tl[i];
-            if (vals[sl] != bw) continue;
-            const uint32_t h = tie_hash(a.seed, a.sweep, (uint32_t)v, (uint32_t)keys[sl]);
+            int32_t l;
+            double w;
+            get(i, l, w);
+            if (w != bw) continue;
+            const uint32_t h = tie_hash(a.seed, a.sweep, (uint32_t)v, (uint32_t)l);
             if (blab == kEmpty || h > bh || (h == bh && (uint32_t)i < bpos)) {
                 bh = h;
                 bpos = (uint32_t)i;
-                blab = keys[sl];
+                blab = l;
             }
         }
 #pragma unroll
@@ -287,12 +325,6 @@ __device__ bool copra_eval(const CopraArgs& a, int32_t s, int32_t* keys, double*
             myb = 1.0;
         }
     }
-    // restore the table
-    for (int i = lane; i < cnt; i += 32) {
-        const int sl = tl[i];
-        keys[sl] = kEmpty;
-        vals[sl] = 0.0;
-    }
     // sort the kept labels by id (:97-107): rank = number of smaller labels
     int rank = 0;
     for (int j = 0; j < kk; ++j) {
@@ -311,7 +343,7 @@ __device__ bool copra_eval(const CopraArgs& a, int32_t s, int32_t* keys, double*
             bl = ol;
         }
     }
-    // ---- commit: compare with the working state; write and mark on change ----
+    // commit: compare with the working state; write and mark on change
     const size_t row = (size_t)v * K;
     bool diff = *((volatile int32_t*)a.sizeX + v) != kk;
     if (lane < kk) {
@@ -332,62 +364,282 @@ __device__ bool copra_eval(const CopraArgs& a, int32_t s, int32_t* keys, double*
         if (a.mark) mark_row(a, beg, d, lane, 32);
     }
     if (lane == 0) a.ndist[s] = cnt;
-    return true;
 }
 
-// Warp per vertex over the dense slot range or the queue; tables in smem.
-__global__ void __launch_bounds__(kCopraWarps * 32, 3) k_copra_warp(CopraArgs a) {
+// Warp per vertex, table of 2^BITS slots in smem.  Input: `in` (slots)
+// when given, else the dense slot range / the vertex queue of the round.
+// Rows whose distinct labels may exceed 3/4 of the table go to `out`.
+template <int BITS, int NW>
+__host__ __device__ constexpr size_t copra_warp_smem_bytes() {
+    return (size_t)NW * (1 << BITS) * (sizeof(double) + 2 * sizeof(int32_t)) + NW * sizeof(CopraWarpSmem);
+}
+
+template <int BITS, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
+    k_copra_warp(CopraArgs a, const int32_t* __restrict__ in, const int32_t* __restrict__ in_len, int32_t* cursor,
+                 int32_t* out, int32_t* out_len) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int slots = 1 << BITS;
+    constexpr int limit = slots / 4 * 3;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int slots = 1 << kCopraBits;
     double* vals = (double*)smem_raw + warp * slots;
-    int32_t* keys = (int32_t*)((double*)smem_raw + kCopraWarps * slots) + warp * slots;
-    int32_t* tl = (int32_t*)((double*)smem_raw + kCopraWarps * slots) + kCopraWarps * slots + warp * slots;
-    CopraWarpSmem* sms = (CopraWarpSmem*)((int32_t*)((double*)smem_raw + kCopraWarps * slots) + 2 * kCopraWarps * slots);
+    int32_t* keys = (int32_t*)((double*)smem_raw + NW * slots) + warp * slots;
+    int32_t* tl = (int32_t*)((double*)smem_raw + NW * slots) + NW * slots + warp * slots;
+    CopraWarpSmem* sms = (CopraWarpSmem*)((int32_t*)((double*)smem_raw + NW * slots) + 2 * NW * slots);
     CopraWarpSmem& sm = sms[warp];
     for (int i = lane; i < slots; i += 32) {
         keys[i] = kEmpty;
         vals[i] = 0.0;
     }
     __syncwarp();
-    const int cnt = a.queue ? *a.queue_len : a.S;
+    const int items = in ? *in_len : (a.queue ? *a.queue_len : a.S);
     while (true) {
         int idx = 0;
-        if (lane == 0) idx = atomicAdd(a.cursor, 1);
+        if (lane == 0) idx = atomicAdd(cursor, 1);
         idx = __shfl_sync(0xffffffffu, idx, 0);
-        if (idx >= cnt) break;
-        const int32_t s = a.queue ? __ldg(a.slot_of + __ldg(a.queue + idx)) : idx;
+        if (idx >= items) break;
+        const int32_t s = in ? __ldg(in + idx) : (a.queue ? __ldg(a.slot_of + __ldg(a.queue + idx)) : idx);
         if (s < 0) continue;
         const int est = nd_count(__ldg(a.ndist + s));
-        bool done = false;
-        if (est + (est >> 2) <= kCopraLimit) done = copra_eval(a, s, keys, vals, tl, kCopraBits, kCopraLimit, sm);
-        if (!done && lane == 0) a.big[atomicAdd(a.big_len, 1)] = s;
+        int dist = -1;
+        if (est + (est >> 2) <= limit) {
+            const int d = (int)(__ldg(a.soff + s + 1) - __ldg(a.soff + s));
+            int seen = 0;
+            bool over = false;
+            for_each_contribution(a, s, 0, d, [&](int32_t lab, double val, int c, bool) {
+                if (over) return;
+                tally_chunk(lab, val, c, keys, vals, nullptr, tl, BITS, seen, sm.stage);
+                if (seen > limit) {
+                    table_restore(keys, vals, tl, seen);
+                    over = true;
+                }
+            });
+            dist = over ? -1 : seen;
+        }
+        if (dist < 0) {
+            if (lane == 0) out[atomicAdd(out_len, 1)] = s;
+            continue;
+        }
+        copra_finish(a, s, dist, [&](int i, int32_t& l, double& w) {
+            const int sl = tl[i];
+            l = keys[sl];
+            w = vals[sl];
+        }, sm);
+        table_restore(keys, vals, tl, dist);
     }
 }
 
-// Block (one warp) per big vertex; tables in per-block global scratch.
-__global__ void __launch_bounds__(32) k_copra_big(CopraArgs a) {
-    __shared__ CopraWarpSmem sm;
-    const int lane = threadIdx.x & 31;
-    const size_t slots = (size_t)1 << a.gbits;
-    int32_t* keys = a.gkeys + blockIdx.x * slots;
-    double* vals = a.gvals + blockIdx.x * slots;
-    int32_t* tl = a.gtl + blockIdx.x * slots;
-    const int cnt = *a.big_len;
-    while (true) {
-        int idx = 0;
-        if (lane == 0) idx = atomicAdd(a.big_cursor, 1);
-        idx = __shfl_sync(0xffffffffu, idx, 0);
-        if (idx >= cnt) break;
-        copra_eval(a, a.big[idx], keys, vals, tl, a.gbits, (int)(slots >> 1) + (int)(slots >> 2), sm);
-    }
+// Team path for big rows: a block of kCopraTeamWarps warps per vertex.
+// Labels are split into P hash partitions.  (1) each warp counts, for its
+// contiguous range of the row's arcs, the contributions of every partition;
+// (2) a stable scatter puts every contribution into its partition's bucket in
+// scan order (bucket q = warp ranges in order, each in scan order); (3) warp
+// w tallies buckets w, w + W, ... with its smem table -- per-label order is
+// the scan order because a label lives in one bucket; (4) the entries
+// (label, tally, first contribution) are put back into first-touch order via
+// a contribution-indexed map and one warp finishes the vertex.  A bucket
+// with more distinct labels than a warp table holds restarts the vertex with
+// twice the partitions.
+constexpr int kCopraTeamWarps = 16;
+constexpr int kCopraTeamBits = 8;      // per-warp table, 256 slots
+constexpr int kCopraTeamLimit = 192;
+constexpr int kCopraMaxParts = 4096;
+
+__host__ __device__ constexpr size_t copra_team_smem_bytes() {
+    return (size_t)kCopraTeamWarps * (1 << kCopraTeamBits) * (sizeof(double) + 3 * sizeof(int32_t)) +
+           (size_t)kCopraTeamWarps * sizeof(CopraWarpSmem) + 256;
 }
 
-__global__ void k_copra_gtab_init(int32_t* keys, double* vals, int64_t count) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(kCopraTeamWarps * 32, 2) k_copra_team(CopraArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int slots = 1 << kCopraTeamBits;
+    constexpr int W = kCopraTeamWarps;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    double* vals = (double*)smem_raw + warp * slots;
+    int32_t* ibase = (int32_t*)((double*)smem_raw + W * slots);
+    int32_t* keys = ibase + warp * slots;
+    int32_t* firsts = ibase + W * slots + warp * slots;
+    int32_t* tl = ibase + 2 * W * slots + warp * slots;
+    CopraWarpSmem* sms = (CopraWarpSmem*)(ibase + 3 * W * slots);
+    CopraWarpSmem& sm = sms[warp];
+    int32_t* ctl = (int32_t*)(sms + W);  // [0] item [1] entries [2] overflow [3] contributions [16..16+W) warp bases
+    // per-block global scratch
+    const size_t D = a.gcap_entries, Cc = a.gcap_contrib;
+    int32_t* Elab = a.gelab + blockIdx.x * D;
+    double* Eval = a.geval + blockIdx.x * D;
+    int32_t* Efirst = a.gefirst + blockIdx.x * D;
+    int32_t* Rlab = a.grlab + blockIdx.x * D;
+    double* Rval = a.grval + blockIdx.x * D;
+    int32_t* F = a.gfmap + blockIdx.x * Cc;
+    int32_t* Blab = a.gblab + blockIdx.x * Cc;
+    double* Bval = a.gbval + blockIdx.x * Cc;
+    int32_t* Bc = a.gbc + blockIdx.x * Cc;
+    int32_t* Wc = a.gwc + blockIdx.x * (size_t)(W * kCopraMaxParts);  // [W][P] counts -> offsets
+    int32_t* Qs = a.gqs + blockIdx.x * (size_t)(kCopraMaxParts + 1);  // bucket starts
+    for (int i = lane; i < slots; i += 32) {
         keys[i] = kEmpty;
         vals[i] = 0.0;
     }
+    const int nitems = *a.big_len;
+    while (true) {
+        __syncthreads();
+        if (tid == 0) ctl[0] = atomicAdd(a.big_cursor, 1);
+        __syncthreads();
+        const int idx = ctl[0];
+        if (idx >= nitems) break;
+        const int32_t s = a.big[idx];
+        const int d = (int)(__ldg(a.soff + s + 1) - __ldg(a.soff + s));
+        const int k_lo = (int)((long long)d * warp / W), k_hi = (int)((long long)d * (warp + 1) / W);
+        const int est = nd_count(__ldg(a.ndist + s));
+        int P = W;
+        while (P < kCopraMaxParts && P * kCopraTeamLimit < est + (est >> 2)) P *= 2;
+        while (true) {  // retry with more partitions on a table overflow
+            // (1) per-warp partition counts
+            for (int q = lane; q < P; q += 32) Wc[warp * P + q] = 0;
+            __syncwarp();
+            int mine = 0;
+            for_each_contribution(a, s, k_lo, k_hi, [&](int32_t lab, double, int, bool valid) {
+                const uint32_t q = valid ? part_of(lab, (uint32_t)P) : 0xffffffffu;
+                const uint32_t grp = __match_any_sync(0xffffffffu, q);
+                if (valid && (__ffs(grp) - 1) == lane) Wc[warp * P + q] += __popc(grp);
+                mine += __popc(__ballot_sync(0xffffffffu, valid));
+                __syncwarp();
+            });
+            if (lane == 0) ctl[16 + warp] = mine;
+            if (tid == 0) {
+                ctl[1] = 0;
+                ctl[2] = 0;
+            }
+            __syncthreads();
+            // bucket starts (serial over P by warp 0: P <= 4096) and per-warp offsets
+            if (warp == 0) {
+                int run = 0;
+                for (int q0 = 0; q0 < P; q0 += 32) {
+                    const int q = q0 + lane;
+                    int tot = 0;
+                    if (q < P)
+                        for (int w = 0; w < W; ++w) tot += Wc[w * P + q];
+                    int incl = tot;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += t;
+                    }
+                    if (q < P) {
+                        int off = run + incl - tot;
+                        Qs[q] = off;
+                        for (int w = 0; w < W; ++w) {
+                            const int cnum = Wc[w * P + q];
+                            Wc[w * P + q] = off;
+                            off += cnum;
+                        }
+                    }
+                    run += __shfl_sync(0xffffffffu, incl, 31);
+                }
+                if (lane == 0) {
+                    Qs[P] = run;
+                    int cb = 0;
+                    for (int w = 0; w < W; ++w) {
+                        const int m = ctl[16 + w];
+                        ctl[16 + w] = cb;
+                        cb += m;
+                    }
+                    ctl[3] = cb;
+                }
+            }
+            __syncthreads();
+            // (2) stable scatter into buckets
+            const int cb = ctl[16 + warp];
+            for_each_contribution(a, s, k_lo, k_hi, [&](int32_t lab, double val, int c, bool valid) {
+                const uint32_t q = valid ? part_of(lab, (uint32_t)P) : 0xffffffffu;
+                const uint32_t grp = __match_any_sync(0xffffffffu, q);
+                int pos = 0;
+                if (valid) pos = Wc[warp * P + q] + __popc(grp & lanemask_lt());
+                __syncwarp();
+                if (valid && (__ffs(grp) - 1) == lane) Wc[warp * P + q] += __popc(grp);
+                if (valid) {
+                    Blab[pos] = lab;
+                    Bval[pos] = val;
+                    Bc[pos] = cb + c;
+                }
+                __syncwarp();
+            });
+            __syncthreads();
+            // (3) tally the buckets
+            for (int q = warp; q < P; q += W) {
+                const int qb = Qs[q], qe = Qs[q + 1];
+                int cnt = 0;
+                bool over = false;
+                for (int i0 = qb; i0 < qe; i0 += 32) {
+                    const int i = i0 + lane;
+                    const bool valid = i < qe;
+                    tally_chunk(valid ? Blab[i] : kEmpty, valid ? Bval[i] : 0.0, valid ? Bc[i] : 0, keys, vals, firsts,
+                                tl, kCopraTeamBits, cnt, sm.stage);
+                    if (cnt > kCopraTeamLimit) {
+                        over = true;
+                        break;
+                    }
+                }
+                if (over) {
+                    table_restore(keys, vals, tl, cnt);
+                    if (lane == 0) ctl[2] = 1;
+                    break;
+                }
+                int base = 0;
+                if (lane == 0) base = atomicAdd(ctl + 1, cnt);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                for (int i = lane; i < cnt; i += 32) {
+                    const int sl = tl[i];
+                    Elab[base + i] = keys[sl];
+                    Eval[base + i] = vals[sl];
+                    Efirst[base + i] = firsts[sl];
+                    keys[sl] = kEmpty;
+                    vals[sl] = 0.0;
+                }
+                __syncwarp();
+            }
+            __syncthreads();
+            if (ctl[2] == 0) break;
+            if (P >= kCopraMaxParts) {  // cannot happen for n <= 1.5M; reported, never silent
+                if (tid == 0) atomicAdd(a.counters + kCtrCount + 1, 1ull);
+                break;
+            }
+            P *= 2;
+        }
+        // (4) first-touch order: F[first] = entry, then an ordered compaction of F
+        const int nent = ctl[1], C = ctl[3];
+        for (int e = tid; e < nent; e += blockDim.x) F[Efirst[e]] = e;
+        __syncthreads();
+        int run = 0;  // entries placed so far (block-uniform)
+        for (int c0 = 0; c0 < C; c0 += blockDim.x) {
+            const int c = c0 + tid;
+            const int e = c < C ? F[c] : -1;
+            const bool has = e >= 0;
+            const uint32_t bal = __ballot_sync(0xffffffffu, has);
+            if (lane == 0) sm.outl[0] = __popc(bal);  // per-warp count (outl reused as scratch)
+            __syncthreads();
+            int before = run;
+            for (int w = 0; w < warp; ++w) before += sms[w].outl[0];
+            if (has) {
+                const int r = before + __popc(bal & lanemask_lt());
+                Rlab[r] = Elab[e];
+                Rval[r] = Eval[e];
+                F[c] = -1;
+            }
+            for (int w = 0; w < W; ++w) run += sms[w].outl[0];
+            __syncthreads();
+        }
+        if (warp == 0)
+            copra_finish(a, s, nent, [&](int i, int32_t& l, double& w) {
+                l = Rlab[i];
+                w = Rval[i];
+            }, sm);
+    }
+}
+
+__global__ void k_fill_i32(int32_t* p, int32_t v, int64_t count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
 }
 
 // copra.py:254-258: labs[:, 0] = v, bels[:, 0] = 1, sizes = 1, best = v

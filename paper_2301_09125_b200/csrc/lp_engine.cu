@@ -130,11 +130,21 @@ struct lp_graph {
     int32_t* cbest[2] = {nullptr, nullptr};
     size_t ccap = 0;            // cells (n * K) the label-set buffers hold
     int32_t* ccur = nullptr;    // work cursors [4]
-    int32_t* cbig = nullptr;    // spill list [n]
-    int32_t* gkeys = nullptr;   // big-table scratch
-    double* gvals = nullptr;
-    int32_t* gtl = nullptr;
-    uint32_t gbits = 0;
+    int32_t* cbig = nullptr;    // team list [n]
+    int32_t* cmid = nullptr;    // tier-1 list [n]
+    // COPRA team scratch, per team block: entries [gent], contribution map [gcon]
+    int32_t* gelab = nullptr;
+    double* geval = nullptr;
+    int32_t* gefirst = nullptr;
+    int32_t* grlab = nullptr;
+    double* grval = nullptr;
+    int32_t* gfmap = nullptr;
+    int32_t* gblab = nullptr;
+    double* gbval = nullptr;
+    int32_t* gbc = nullptr;
+    int32_t* gwc = nullptr;
+    int32_t* gqs = nullptr;
+    size_t gent = 0, gcon = 0;
     int gblocks = 0;
     Routes routes;
     int64_t cap_items = 0;
@@ -628,9 +638,18 @@ static void destroy_graph(lp_graph* g) {
     }
     cudaFree(g->ccur);
     cudaFree(g->cbig);
-    cudaFree(g->gkeys);
-    cudaFree(g->gvals);
-    cudaFree(g->gtl);
+    cudaFree(g->cmid);
+    cudaFree(g->gelab);
+    cudaFree(g->geval);
+    cudaFree(g->gefirst);
+    cudaFree(g->grlab);
+    cudaFree(g->grval);
+    cudaFree(g->gfmap);
+    cudaFree(g->gblab);
+    cudaFree(g->gbval);
+    cudaFree(g->gbc);
+    cudaFree(g->gwc);
+    cudaFree(g->gqs);
     cudaFree(g->off);
     cudaFree(g->nbr);
     cudaFree(g->w);
@@ -1220,17 +1239,6 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     const size_t cells = (size_t)n * T;
     if (cells > g->slots_cap) {
         cudaFree(g->slots);
-    for (int i = 0; i < 2; ++i) {
-        cudaFree(g->clabs[i]);
-        cudaFree(g->cbels[i]);
-        cudaFree(g->csize[i]);
-        cudaFree(g->cbest[i]);
-    }
-    cudaFree(g->ccur);
-    cudaFree(g->cbig);
-    cudaFree(g->gkeys);
-    cudaFree(g->gvals);
-    cudaFree(g->gtl);
         g->slots = nullptr;
         g->slots_cap = 0;
         LP_CK(cudaMalloc(&g->slots, cells * sizeof(int32_t)));
@@ -1340,40 +1348,57 @@ static int copra_buffers(lp_graph* g, int K) {
             LP_CK(cudaMalloc(&g->csize[i], std::max<int64_t>(n, 1) * sizeof(int32_t)));
             LP_CK(cudaMalloc(&g->cbest[i], std::max<int64_t>(n, 1) * sizeof(int32_t)));
         }
-        LP_CK(cudaMalloc(&g->ccur, 4 * sizeof(int32_t)));
+        LP_CK(cudaMalloc(&g->ccur, 8 * sizeof(int32_t)));
         LP_CK(cudaMalloc(&g->cbig, std::max<int64_t>(n, 1) * sizeof(int32_t)));
+        LP_CK(cudaMalloc(&g->cmid, std::max<int64_t>(n, 1) * sizeof(int32_t)));
     }
-    // big tables: 2^gbits >= 2 * (the most distinct labels a row can see), so the
-    // big kernel never overflows; blocks bounded by a 4 GiB scratch budget
-    const double most = std::min<double>((double)n, (double)g->max_degree * K);
-    uint32_t bits = 8;
-    while ((double)(1u << bits) < 2.0 * most + 64.0) ++bits;
-    if (bits > g->gbits) {
-        cudaFree(g->gkeys);
-        cudaFree(g->gvals);
-        cudaFree(g->gtl);
-        g->gkeys = nullptr;
-        g->gvals = nullptr;
-        g->gtl = nullptr;
-        g->gbits = 0;
-        const size_t per = ((size_t)1 << bits) * (sizeof(int32_t) * 2 + sizeof(double));
-        const int blocks = (int)std::max<size_t>(1, std::min<size_t>(g->num_sms, ((size_t)4 << 30) / per));
-        const size_t slots = ((size_t)1 << bits) * blocks;
-        LP_CK(cudaMalloc(&g->gkeys, slots * sizeof(int32_t)));
-        LP_CK(cudaMalloc(&g->gvals, slots * sizeof(double)));
-        LP_CK(cudaMalloc(&g->gtl, slots * sizeof(int32_t)));
-        k_copra_gtab_init<<<g->num_sms * 8, 256, 0, g->stream>>>(g->gkeys, g->gvals, (int64_t)slots);
+    // team scratch: a row sees at most min(n, max_degree * K) distinct labels and
+    // max_degree * K contributions; blocks bounded by a 4 GiB budget
+    const size_t con = (size_t)std::max<int64_t>(1, g->max_degree) * K;
+    const size_t ent = std::min<size_t>((size_t)n, con);
+    if (ent > g->gent || con > g->gcon) {
+        cudaFree(g->gelab);
+        cudaFree(g->geval);
+        cudaFree(g->gefirst);
+        cudaFree(g->grlab);
+        cudaFree(g->grval);
+        cudaFree(g->gfmap);
+        cudaFree(g->gblab);
+        cudaFree(g->gbval);
+        cudaFree(g->gbc);
+        cudaFree(g->gwc);
+        cudaFree(g->gqs);
+        g->gelab = g->gefirst = g->grlab = g->gfmap = g->gblab = g->gbc = g->gwc = g->gqs = nullptr;
+        g->geval = g->grval = g->gbval = nullptr;
+        g->gent = g->gcon = 0;
+        const size_t parts = (size_t)kCopraTeamWarps * kCopraMaxParts + kCopraMaxParts + 1;
+        const size_t per = ent * (3 * sizeof(int32_t) + 2 * sizeof(double)) +
+                           con * (3 * sizeof(int32_t) + sizeof(double)) + parts * sizeof(int32_t);
+        const int blocks = (int)std::max<size_t>(1, std::min<size_t>(2 * g->num_sms, ((size_t)6 << 30) / per));
+        LP_CK(cudaMalloc(&g->gelab, ent * blocks * sizeof(int32_t)));
+        LP_CK(cudaMalloc(&g->geval, ent * blocks * sizeof(double)));
+        LP_CK(cudaMalloc(&g->gefirst, ent * blocks * sizeof(int32_t)));
+        LP_CK(cudaMalloc(&g->grlab, ent * blocks * sizeof(int32_t)));
+        LP_CK(cudaMalloc(&g->grval, ent * blocks * sizeof(double)));
+        LP_CK(cudaMalloc(&g->gfmap, con * blocks * sizeof(int32_t)));
+        LP_CK(cudaMalloc(&g->gblab, con * blocks * sizeof(int32_t)));
+        LP_CK(cudaMalloc(&g->gbval, con * blocks * sizeof(double)));
+        LP_CK(cudaMalloc(&g->gbc, con * blocks * sizeof(int32_t)));
+        LP_CK(cudaMalloc(&g->gwc, (size_t)kCopraTeamWarps * kCopraMaxParts * blocks * sizeof(int32_t)));
+        LP_CK(cudaMalloc(&g->gqs, (size_t)(kCopraMaxParts + 1) * blocks * sizeof(int32_t)));
+        k_fill_i32<<<g->num_sms * 8, 256, 0, g->stream>>>(g->gfmap, -1, (int64_t)(con * blocks));
         LP_CK(cudaGetLastError());
-        g->gbits = bits;
+        g->gent = ent;
+        g->gcon = con;
         g->gblocks = blocks;
     }
     return LP_OK;
 }
 
-static size_t copra_smem_bytes() {
-    return (size_t)kCopraWarps * (1 << kCopraBits) * (sizeof(double) + 2 * sizeof(int32_t)) +
-           kCopraWarps * sizeof(CopraWarpSmem);
-}
+// COPRA tiers: warp + 512-slot table (8 warps/block), warp + 4096-slot
+// table (1 warp/block), team (16 warps, partitioned; lp_copra_kernels.cuh)
+#define COPRA_T0 kCopraBits, kCopraWarps, 3
+#define COPRA_T1 11, 2, 3
 
 extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_out, double* bels_out,
                             int64_t* sizes_out, int64_t* best_out, int64_t* changed_per_iter, lp_run_stats* stats) {
@@ -1406,12 +1431,21 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
     cudaStream_t st = g->stream;
     static int smem_set_device = -1;
     if (smem_set_device != g->device) {
-        LP_CK(cudaFuncSetAttribute(k_copra_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)copra_smem_bytes()));
+        LP_CK(cudaFuncSetAttribute(k_copra_warp<COPRA_T0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)copra_warp_smem_bytes<kCopraBits, kCopraWarps>()));
+        LP_CK(cudaFuncSetAttribute(k_copra_warp<COPRA_T1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)copra_warp_smem_bytes<11, 2>()));
+        LP_CK(cudaFuncSetAttribute(k_copra_team, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)copra_team_smem_bytes()));
         smem_set_device = g->device;
     }
-    int occ = 1;
-    LP_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_copra_warp, kCopraWarps * 32, copra_smem_bytes()));
+    int occ = 1, occ1 = 1;
+    LP_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_copra_warp<COPRA_T0>, kCopraWarps * 32,
+                                                        copra_warp_smem_bytes<kCopraBits, kCopraWarps>()));
+    LP_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_copra_warp<COPRA_T1>, 64,
+                                                        copra_warp_smem_bytes<11, 2>()));
     occ = std::max(occ, 1);
+    occ1 = std::max(occ1, 1);
     int c0 = 0, c1 = 1;  // L0 / X buffer index
     k_copra_init<<<g->num_sms * 8, 256, 0, st>>>(g->clabs[c0], g->cbels[c0], g->csize[c0], g->cbest[c0], n, K);
     if (P.S > 0) k_reset_ndist<<<g->num_sms * 8, 256, 0, st>>>(P.soff, P.ndist, P.S);
@@ -1433,25 +1467,41 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
     a.big_len = g->ccur + 1;
     a.big_cursor = g->ccur + 2;
     a.big = g->cbig;
-    a.gkeys = g->gkeys;
-    a.gvals = g->gvals;
-    a.gtl = g->gtl;
-    a.gbits = g->gbits;
+    a.gelab = g->gelab;
+    a.geval = g->geval;
+    a.gefirst = g->gefirst;
+    a.grlab = g->grlab;
+    a.grval = g->grval;
+    a.gfmap = g->gfmap;
+    a.gblab = g->gblab;
+    a.gbval = g->gbval;
+    a.gbc = g->gbc;
+    a.gwc = g->gwc;
+    a.gqs = g->gqs;
+    a.gcap_entries = g->gent;
+    a.gcap_contrib = g->gcon;
     a.counters = g->counters;
     a.seed = o->seed;
     Prof prof;
     prof.on = (o->flags & LP_RAK_PROFILE) != 0;
     prof.pool = &g->event_pool;
-    LP_CK(cudaMemsetAsync(g->counters, 0, kCtrCount * sizeof(unsigned long long), st));
+    LP_CK(cudaMemsetAsync(g->counters, 0, (kCtrCount + 2) * sizeof(unsigned long long), st));
     LP_CK(cudaEventRecord(g->ev0, st));
     int it = 0, rounds = 0;
     auto launch = [&](int64_t work) -> int {
-        LP_CK(cudaMemsetAsync(g->ccur, 0, 4 * sizeof(int32_t), st));
+        LP_CK(cudaMemsetAsync(g->ccur, 0, 8 * sizeof(int32_t), st));
+        // ccur: [0] tier-0 cursor [1] big length [2] big cursor [3] mid length [4] mid cursor
         prof.begin(st, kKWarp);
-        k_copra_warp<<<grid_for(work, kCopraWarps, g->num_sms * occ), kCopraWarps * 32, copra_smem_bytes(), st>>>(a);
+        k_copra_warp<COPRA_T0><<<grid_for(work, kCopraWarps, g->num_sms * occ), kCopraWarps * 32,
+                                 copra_warp_smem_bytes<kCopraBits, kCopraWarps>(), st>>>(
+            a, nullptr, nullptr, g->ccur, g->cmid, g->ccur + 3);
+        prof.end(st);
+        prof.begin(st, kKTeam);
+        k_copra_warp<COPRA_T1><<<g->num_sms * occ1, 64, copra_warp_smem_bytes<11, 2>(), st>>>(
+            a, g->cmid, g->ccur + 3, g->ccur + 4, g->cbig, g->ccur + 1);
         prof.end(st);
         prof.begin(st, kKHub);
-        k_copra_big<<<g->gblocks, 32, 0, st>>>(a);
+        k_copra_team<<<g->gblocks, kCopraTeamWarps * 32, copra_team_smem_bytes(), st>>>(a);  // gblocks <= 2 / SM
         prof.end(st);
         ++rounds;
         return LP_OK;
@@ -1498,10 +1548,12 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
         }
         LP_CK(cudaMemsetAsync(g->counters + kCtrChanged, 0, sizeof(unsigned long long), st));
         k_count_changed<<<g->num_sms * 8, 256, 0, st>>>(g->cbest[c0], g->cbest[c1], n, g->counters + kCtrChanged);
-        LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, kCtrCount * sizeof(unsigned long long),
+        LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, (kCtrCount + 2) * sizeof(unsigned long long),
                               cudaMemcpyDeviceToHost, st));
         LP_CK(cudaStreamSynchronize(st));
         LP_CK(cudaGetLastError());
+        if (g->h_counters[kCtrCount + 1])
+            return lp_fail(LP_ERR_UNSUPPORTED, "a row has more distinct labels than the team tables hold");
         const int64_t changed = (int64_t)g->h_counters[kCtrChanged];
         if (changed_per_iter) changed_per_iter[it - 1] = changed;
         std::swap(c0, c1);  // c0 = this sweep's state
