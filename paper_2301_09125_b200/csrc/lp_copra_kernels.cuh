@@ -54,7 +54,7 @@ struct CopraArgs {
     int32_t* bestX;
     int32_t* ndist;                     // per-slot distinct count of the last evaluation
     // frontier
-    int32_t* mark;
+    unsigned long long* mark;
     int32_t* mq_out;
     int32_t* mq_len;
     // work: dense slot range or a vertex queue; spill list for big tables
@@ -656,9 +656,10 @@ __global__ void k_copra_init(int32_t* __restrict__ labs, double* __restrict__ be
 }
 
 // frontier: clear the marks of the queued vertices before the round evaluates any
-__global__ void k_clear_marks(const int32_t* __restrict__ q, const int32_t* __restrict__ qlen, int32_t* mark) {
+__global__ void k_clear_marks(const int32_t* __restrict__ q, const int32_t* __restrict__ qlen,
+                              unsigned long long* mark) {
     const int cnt = *qlen;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) mark[q[i]] = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) mark[q[i]] = 0ull;
 }
 
 // copra.py:171-173: vertices whose best label changed this sweep

@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -89,6 +90,10 @@ struct Plan {
     int64_t flags_bs = -1;           // batch size the snbr flags were computed for
     int32_t bin_beg[kNumBins + 1] = {0, 0, 0, 0, 0, 0};  // slot range of each bin (idle: [.., n))
     int32_t big_end = 0;             // slots [0, big_end) are big rows, [big_end, S) small
+    // visit order (position -> vertex) and the dense-wave lengths
+    int32_t* vorder = nullptr;
+    int32_t* wave_len = nullptr;     // [kMaxWaves] device
+    int waves = 0;                   // waves wave_len was built for
     // every active row as phase-1 pieces (INDEX plans: SLPA's dense rounds)
     int32_t* dslot = nullptr;
     int32_t* dk0 = nullptr;
@@ -104,6 +109,7 @@ struct lp_graph {
     int64_t n = 0, m = 0;
     int64_t max_degree = 0;
     int64_t sliceable = 0;  // rows long enough to be cut into slices
+    int64_t slice_slots = 0;  // their largest global tables, summed
     int wmode = kUnit;
     int fixed_shift = 0;
     int64_t bytes = 0;
@@ -118,7 +124,8 @@ struct lp_graph {
     int32_t* labA = nullptr;
     int32_t* labB = nullptr;
     int32_t* cur = nullptr;  // the buffer holding the latest labels
-    int32_t* mark = nullptr;    // frontier marks by vertex id
+    unsigned long long* mark = nullptr;  // frontier marks by vertex id (changed weight since routing)
+    unsigned long long* gap = nullptr;   // per slot: winner margin lower bound at the last evaluation
     int32_t* mq[2] = {nullptr, nullptr};  // mark queues (alternate per round)
     int32_t* mq_len = nullptr;  // their lengths [2]
     int32_t* slots = nullptr;   // SLPA memories [n x T]
@@ -155,6 +162,9 @@ struct lp_graph {
     void* cub_tmp = nullptr;
     size_t cub_tmp_bytes = 0;
     int num_sms = 148;
+    int waves = 1;  // dense waves of the cross-batch schedules (LP_WAVES overrides)
+    bool margin_skip = true;  // frontier margin test (LP_MARGIN=0 disables)
+    bool debug_rounds = false;  // LP_DEBUG_ROUNDS=1: per-round route sizes on stderr
     bool labels_valid = false;
     std::vector<cudaEvent_t> event_pool;
 };
@@ -213,16 +223,23 @@ __global__ void k_weight_convert(const double* __restrict__ w, uint32_t* __restr
     }
 }
 
-// [0] max degree, [1] rows longer than two slices
+// [0] max degree, [1] rows longer than two slices, [2] their largest
+// global slice tables (slots), summed
 __global__ void k_degree_stats(const uint32_t* __restrict__ off, int64_t n, unsigned long long* out) {
-    unsigned long long mx = 0, sl = 0;
+    unsigned long long mx = 0, sl = 0, slots = 0;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long d = off[v + 1] - off[v];
         mx = max(mx, d);
-        sl += d > 2ull * kSliceArcs;
+        if (d > 2ull * kSliceArcs) {
+            ++sl;
+            unsigned long long t = 1ull << kGlobalBits;
+            while (t < 2 * d + 64) t <<= 1;
+            slots += t;
+        }
     }
     atomicMax(out, mx);
     if (sl) atomicAdd(out + 1, sl);
+    if (slots) atomicAdd(out + 2, slots);
 }
 
 __global__ void k_plan_pos(const int64_t* __restrict__ order, int32_t* __restrict__ pos, int64_t n,
@@ -283,6 +300,11 @@ __global__ void k_plan_keys(const uint32_t* __restrict__ off, const int32_t* __r
     }
     __syncthreads();
     if (threadIdx.x < kNumBins && sc[threadIdx.x]) atomicAdd(counts + threadIdx.x, sc[threadIdx.x]);
+}
+
+__global__ void k_plan_vorder(const int32_t* __restrict__ pos, int32_t* __restrict__ vorder, int64_t n) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        vorder[pos[v]] = (int32_t)v;
 }
 
 __global__ void k_iota(int32_t* a, int64_t n) {
@@ -598,6 +620,8 @@ static void free_plan(Plan& P) {
     cudaFree(P.swsum);
     cudaFree(P.ndist);
     cudaFree(P.lbuf);
+    cudaFree(P.vorder);
+    cudaFree(P.wave_len);
     cudaFree(P.dslot);
     cudaFree(P.dk0);
     cudaFree(P.dcount);
@@ -614,6 +638,7 @@ static void free_routes(Routes& r) {
     cudaFree(r.cand);
     cudaFree(r.cand_done);
     cudaFree(r.gkeys);
+    cudaFree(r.gtl);
     cudaFree(r.gfirst);
     cudaFree(r.gacc);
     cudaFree(r.gcount);
@@ -656,6 +681,7 @@ static void destroy_graph(lp_graph* g) {
     cudaFree(g->labA);
     cudaFree(g->labB);
     cudaFree(g->mark);
+    cudaFree(g->gap);
     cudaFree(g->counters);
     cudaFree(g->out64);
     cudaFree(g->cub_tmp);
@@ -757,6 +783,8 @@ static int build_plan(lp_graph* g, int kind, const int64_t* order_host, uint32_t
         free_plan(P);
         return lp_fail(LP_ERR_INVALID, "order is not a permutation of range(n)");
     }
+    LP_CK(dalloc(&P.vorder, n, &bytes));
+    k_plan_vorder<<<G, 256, 0, st>>>(P.pos, P.vorder, n);
     k_plan_keys<<<G, 256, 0, st>>>(g->off, g->nbr, t.key, n, g->counters + 1, t.deg, index ? 1 : 0);
     k_iota<<<G, 256, 0, st>>>(t.iota, n);
     size_t need = 0, need2 = 0;
@@ -848,7 +876,9 @@ static cudaError_t alloc_routes(lp_graph* g) {
     const int64_t n = std::max<int64_t>(g->n, 1);
     // hub items: one per partition (<= est / kHubPlan + 1) or per slice
     g->cap_items = n + g->m / (kHubPlan / 2) + g->m / kSliceArcs + 1024;
-    const int64_t gpool = std::max<int64_t>(g->sliceable, 1) << kGlobalBits;
+    // slice-table pool: every sliceable row at its largest table (2^bits >= 2 d + 64)
+    const int64_t gpool = std::max<int64_t>(g->slice_slots, (int64_t)1 << kGlobalBits);
+    r.gcap = gpool;
     cudaError_t e;
     for (int c = 0; c < 3; ++c)
         if ((e = dalloc(&r.small[c], n, &g->bytes))) return e;
@@ -861,6 +891,7 @@ static cudaError_t alloc_routes(lp_graph* g) {
     if ((e = dalloc(&r.cand_done, g->cap_items, &g->bytes))) return e;
     if ((e = dalloc(&r.gcount, g->cap_items, &g->bytes))) return e;
     if ((e = dalloc(&r.gkeys, gpool, &g->bytes))) return e;
+    if ((e = dalloc(&r.gtl, gpool, &g->bytes))) return e;
     if ((e = dalloc(&r.gfirst, gpool, &g->bytes))) return e;
     if ((e = dalloc(&r.gacc, gpool, &g->bytes))) return e;
     // phase-1 pieces: one per row plus one per extra kPieceArcs arcs
@@ -897,6 +928,9 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     };
     if (cudaGetDevice(&g->device) != cudaSuccess) return fail(lp_fail(LP_ERR_CUDA, "cudaGetDevice failed"));
     cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device);
+    if (const char* ev = getenv("LP_WAVES")) g->waves = std::max(1, std::min(1024, atoi(ev)));
+    if (const char* ev = getenv("LP_MARGIN")) g->margin_skip = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_DEBUG_ROUNDS")) g->debug_rounds = atoi(ev) != 0;
     g->n = n;
     g->m = m;
 #define G_CK(call)                                                                                      \
@@ -915,6 +949,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     G_CK(dalloc(&g->labA, n, &g->bytes));
     G_CK(dalloc(&g->labB, n, &g->bytes));
     G_CK(dalloc(&g->mark, n + 4, &g->bytes));
+    G_CK(dalloc(&g->gap, n + 4, &g->bytes));
     G_CK(dalloc(&g->mq[0], n + 4, &g->bytes));
     G_CK(dalloc(&g->mq[1], n + 4, &g->bytes));
     G_CK(dalloc(&g->mq_len, 4, &g->bytes));
@@ -922,7 +957,8 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     G_CK(dalloc(&g->out64, n, &g->bytes));
     G_CK(cudaMallocHost((void**)&g->h_len, kLenCount * sizeof(int32_t)));
     G_CK(cudaMallocHost((void**)&g->h_counters, 32 * sizeof(unsigned long long)));
-    G_CK(cudaMemsetAsync(g->mark, 0, (n + 4) * sizeof(int32_t), st));
+    G_CK(cudaMemsetAsync(g->mark, 0, (n + 4) * sizeof(unsigned long long), st));
+    G_CK(cudaMemsetAsync(g->gap, 0, (n + 4) * sizeof(unsigned long long), st));
     G_CK(cudaMemsetAsync(g->counters, 0, 32 * sizeof(unsigned long long), st));
     {
         int64_t* tmp = nullptr;
@@ -949,6 +985,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
         }
         g->max_degree = (int64_t)g->h_counters[8];
         g->sliceable = (int64_t)g->h_counters[9];
+        g->slice_slots = (int64_t)g->h_counters[10];
         g->wmode = kUnit;
         if (weights && m > 0 && g->h_counters[4 + 0] != 0) {
             const unsigned long long bad = g->h_counters[4 + 1];
@@ -999,6 +1036,21 @@ extern "C" int lp_graph_get_info(const lp_graph* g, lp_graph_info* info) {
 
 extern "C" void* lp_graph_stream(lp_graph* g) { return g ? (void*)g->stream : nullptr; }
 
+// Device lengths of the W dense waves (positions [w*ws, (w+1)*ws) of the order).
+static int ensure_waves(lp_graph* g, int W) {
+    Plan& P = g->plan();
+    if (P.waves == W && P.wave_len) return LP_OK;
+    cudaFree(P.wave_len);
+    P.wave_len = nullptr;
+    LP_CK(cudaMalloc(&P.wave_len, W * sizeof(int32_t)));
+    std::vector<int32_t> h((size_t)W);
+    const int64_t ws = (g->n + W - 1) / W;
+    for (int w = 0; w < W; ++w) h[(size_t)w] = (int32_t)std::max<int64_t>(0, std::min<int64_t>(ws, g->n - w * ws));
+    LP_CK(cudaMemcpy(P.wave_len, h.data(), W * sizeof(int32_t), cudaMemcpyHostToDevice));
+    P.waves = W;
+    return LP_OK;
+}
+
 // One sweep (RAK) or speaking round (SLPA): the dense round over every
 // active row, then frontier rounds over the mark queue until a round marks
 // nothing.  One host sync per frontier round (route sizes).
@@ -1010,19 +1062,49 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
     int q = 0;  // this round's writes queue into mq[q]
     a.mq_out = g->mq[q];
     a.mq_len = g->mq_len + q;
+    a.horizon = INT32_MAX;
     LP_CK(cudaMemsetAsync(g->mq_len, 0, 2 * sizeof(int32_t), st));
-    run_round(g, a, true, g->h_len, prof, alg);
-    if (alg == kGatherRak) *gathered += P.m_active;  // (piece gathers count themselves)
-    ++*rounds;
+    const int W = cross ? g->waves : 1;
+    if (W <= 1) {
+        run_round(g, a, true, g->h_len, prof, alg);
+        if (alg == kGatherRak) *gathered += P.m_active;  // (piece gathers count themselves)
+        ++*rounds;
+    } else {
+        // Dense waves: the visit order in W consecutive position ranges, each
+        // routed and evaluated after the previous one, so a wave reads the
+        // current-sweep labels of all earlier waves; a changed label marks only
+        // the later neighbours in positions already evaluated (its own wave).
+        if (int rc = ensure_waves(g, W)) return rc;
+        const int64_t ws = (g->n + W - 1) / W;
+        for (int w = 0; w < W; ++w) {
+            if (w > 0) LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
+            prof->begin(st, -1);
+            k_route_queue<<<g->num_sms * 4, 256, 0, st>>>(a, P.vorder + w * ws, P.wave_len + w, P.slot_of, 0);
+            prof->end(st);
+            LP_CK(cudaMemcpyAsync(g->h_len, g->routes.len, kLenCount * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            LP_CK(cudaStreamSynchronize(st));
+            a.horizon = (int32_t)std::min<int64_t>(g->n, (w + 1) * ws);
+            if (g->h_len[kLenGather] > 0) run_round(g, a, false, g->h_len, prof, alg);
+            ++*rounds;
+        }
+        a.horizon = INT32_MAX;
+    }
     while (cross) {
         // route last round's queue; this round's writes queue into the other one
         LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
         LP_CK(cudaMemsetAsync(g->mq_len + (q ^ 1), 0, sizeof(int32_t), st));
         prof->begin(st, -1);
-        k_route_queue<<<g->num_sms * 4, 256, 0, st>>>(a, g->mq[q], g->mq_len + q, P.slot_of);
+        k_route_queue<<<g->num_sms * 4, 256, 0, st>>>(a, g->mq[q], g->mq_len + q, P.slot_of, 1);
         prof->end(st);
         LP_CK(cudaMemcpyAsync(g->h_len, g->routes.len, kLenCount * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         LP_CK(cudaStreamSynchronize(st));
+        if (g->debug_rounds) {
+            int32_t ql = 0;
+            cudaMemcpy(&ql, g->mq_len + q, sizeof(int32_t), cudaMemcpyDeviceToHost);
+            fprintf(stderr, "[lp] round %d: queue %d small %d/%d/%d warp %d warpbig %d team %d hub-items %d pieces %d\n",
+                    *rounds, ql, g->h_len[kLenS16], g->h_len[kLenS16 - 1], g->h_len[kLenS16 - 2], g->h_len[kLenWarp],
+                    g->h_len[kLenWarpBig], g->h_len[kLenTeam], g->h_len[kLenHub], g->h_len[kLenGather]);
+        }
         if (g->h_len[kLenGather] == 0) break;
         q ^= 1;
         a.mq_out = g->mq[q];
@@ -1129,6 +1211,9 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.svid = P.svid;
     a.lbuf = P.lbuf;
     a.mark = cross ? g->mark : nullptr;
+    a.gap = (cross && g->wmode != kFloat && g->margin_skip) ? g->gap : nullptr;
+    a.pos = P.pos;
+    a.horizon = INT32_MAX;
     a.mq_out = nullptr;
     a.mq_len = nullptr;
     a.ndist = P.ndist;
@@ -1259,6 +1344,9 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     a.svid = P.svid;
     a.lbuf = P.lbuf;
     a.mark = cross ? g->mark : nullptr;
+    a.gap = (cross && g->wmode != kFloat && g->margin_skip) ? g->gap : nullptr;
+    a.pos = P.pos;
+    a.horizon = INT32_MAX;
     a.ndist = P.ndist;
     a.counters = g->counters;
     a.r = g->routes;

@@ -61,7 +61,7 @@ struct Item {
     int32_t R;   // slices
     int32_t cb;  // merge state base (cand[cb..cb+P), cand_done[cb]); -1 when P = R = 1
     int32_t gt;  // global slice-table base (entries), R > 1
-    int32_t pad;
+    int32_t gbits;  // global slice table of 2^gbits slots, R > 1
 };
 
 // route-list lengths / cursors (device ints)
@@ -91,6 +91,8 @@ struct Routes {
     int32_t* len;  // kLen*
     HubCand* cand;
     int32_t* cand_done;
+    int64_t gcap;    // slots in the global slice-table pool
+    int32_t* gtl;    // per slice table: slots of its entries in insertion order (same indexing)
     int32_t* gkeys;  // global slice tables (SoA)
     uint32_t* gfirst;
     unsigned long long* gacc;
@@ -108,7 +110,14 @@ struct EvalArgs {
     const int32_t* __restrict__ L0;     // labels at sweep start, by vertex id (read-only in a sweep)
     int32_t* x;                         // working labels, by vertex id
     int32_t* lbuf;                      // phase 1 output: label of every arc's neighbour
-    int32_t* mark;                      // next-round marks by vertex id, null = no cross-batch deps
+    unsigned long long* mark;           // next-round marks by vertex id: weight of the changed earlier
+                                        // neighbours since the last routing (0 = unmarked); null = no
+                                        // cross-batch deps
+    unsigned long long* gap;            // per slot: lower bound of (winner - runner-up) weight at the
+                                        // last evaluation (0 = unknown); null = no margin skipping
+    const int32_t* __restrict__ pos;    // vertex -> visit position (wave horizon test)
+    int32_t horizon;                    // dense waves: only positions < horizon have been evaluated
+                                        // this sweep and need marks; INT32_MAX = all
     int32_t* mq_out;                    // queue of newly marked vertices (this round's writes)
     int32_t* mq_len;                    // its length
     int32_t* ndist;                     // per-slot distinct-label count of the last evaluation
@@ -197,6 +206,18 @@ __device__ __forceinline__ void flush_counters(const EvalArgs& a, long long dchg
     }
 }
 
+// Record the winner's margin over the rest of the row (lower bound
+// 2 * winner - total, useful when the winner holds a strict majority).
+template <typename A> __device__ __forceinline__ void store_gap(const EvalArgs& a, int32_t s, A win, A total) {
+    if (a.gap) {
+        if constexpr (std::is_same<A, float>::value) {
+            a.gap[s] = 0ull;
+        } else {
+            a.gap[s] = (win + win > total) ? (unsigned long long)(win + win - total) : 0ull;
+        }
+    }
+}
+
 // Write a vertex's new label (one thread).  Returns true when it changed.
 __device__ __forceinline__ bool commit_label(const EvalArgs& a, int32_t v, int32_t lab, long long& dchg,
                                              long long& writes) {
@@ -222,13 +243,31 @@ __device__ __forceinline__ bool commit_label_known(const EvalArgs& a, int32_t v,
 // Mark the later-batch neighbours of a vertex whose label changed; a vertex
 // marked for the first time this round joins the mark queue (warp-aggregated
 // append), so the next round routes only the queue instead of scanning n.
+// A later-batch neighbour needs a mark only if it may already have read this
+// vertex's label this sweep: during the dense waves, only positions below the
+// horizon have been evaluated (a later wave reads the new label anyway).
+__device__ __forceinline__ bool needs_mark(const EvalArgs& a, int32_t u) {
+    return a.horizon == INT32_MAX || __ldg(a.pos + u) < a.horizon;
+}
+template <typename Args> __device__ __forceinline__ bool needs_mark(const Args&, int32_t) { return true; }
+
+// weight a change adds to a neighbour's mark (margin units: counts, or the
+// fixed-point weights; 1 when margins are not tracked)
+__device__ __forceinline__ unsigned long long mark_weight(const EvalArgs& a, uint32_t e) {
+    return (a.gap && a.sw) ? (unsigned long long)__ldg(a.sw + e) : 1ull;
+}
+template <typename Args> __device__ __forceinline__ unsigned long long mark_weight(const Args&, uint32_t) {
+    return 1ull;
+}
+
 template <typename Args>
 __device__ __forceinline__ void mark_row(const Args& a, uint32_t beg, int d, int from, int step) {
     const int lane = threadIdx.x & 31;
     for (int k = from; k < d; k += step) {
         const uint32_t nb = __ldg(a.snbr + beg + k);
         const int32_t u = (int32_t)(nb >> 2);
-        const bool win = (nb & kLater) && atomicExch(a.mark + u, 1) == 0;
+        const bool win =
+            (nb & kLater) && needs_mark(a, u) && atomicAdd(a.mark + u, mark_weight(a, beg + k)) == 0ull;
         const uint32_t act = __activemask();
         const uint32_t bal = __ballot_sync(act, win);
         if (bal) {
@@ -394,13 +433,24 @@ __device__ __forceinline__ void route_append(const EvalArgs& a, int cls, int32_t
         }
     }
     if (cls == 5) {
+        // rows long enough to slice: R arc slices fold into one L2-resident
+        // global table sized for the estimate (2^bits >= 2 est + 64), so the
+        // row is read once whatever its label count; else label partitions
+        int gbits = kGlobalBits;
+        while ((1 << gbits) < 2 * est + 64 && gbits < 28) ++gbits;
+        int gt = -1;
+        // slices when the labels are few (a small L2 table); with many labels the
+        // smem label partitions are faster than global-table atomics (measured)
         if (d > kSliceArcs * 2 && est <= kSliceEst) {
+            gt = atomicAdd(a.r.len + kGtabCursor, 1 << gbits);
+            if ((int64_t)gt + (1 << gbits) > a.r.gcap) gt = -1;  // pool exhausted: partitions
+        }
+        if (gt >= 0) {
             const int R = (d + kSliceArcs - 1) / kSliceArcs;
             const int base = atomicAdd(a.r.len + kLenHub, R);
             const int cb = atomicAdd(a.r.len + kCandCursor, 1);
-            const int gt = atomicAdd(a.r.len + kGtabCursor, 1 << kGlobalBits);
             for (int r = 0; r < R; ++r) {
-                Item t = {s, 0, 1, r, R, cb, gt, 0};
+                Item t = {s, 0, 1, r, R, cb, gt, gbits};
                 a.r.hub[base + r] = t;
             }
         } else {
@@ -430,7 +480,7 @@ __global__ void k_route_dense(EvalArgs a, int32_t s_beg, int32_t s_end) {
 // Frontier round: the queued (marked) vertices -> route lists + phase-1
 // pieces; marks are cleared so this round's writes can queue them again.
 __global__ void k_route_queue(EvalArgs a, const int32_t* __restrict__ mq_in, const int32_t* __restrict__ mq_in_len,
-                              const int32_t* __restrict__ slot_of) {
+                              const int32_t* __restrict__ slot_of, int clear_marks) {
     const int lane = threadIdx.x & 31;
     const int cnt = *mq_in_len;
     for (int base = blockIdx.x * blockDim.x; base < cnt; base += gridDim.x * blockDim.x) {
@@ -439,8 +489,22 @@ __global__ void k_route_queue(EvalArgs a, const int32_t* __restrict__ mq_in, con
         int32_t s = -1;
         if (i < cnt) {
             const int32_t v = mq_in[i];
-            a.mark[v] = 0;
             s = slot_of[v];
+            if (clear_marks) {
+                // Margin test: the labels that changed since v's last evaluation
+                // moved at most `delta` weight, so if the winner led the runner-up
+                // by more than 2 * delta it still wins: v is not re-evaluated.
+                // (Skipping consumes margin: gap -= 2 * delta keeps it a valid bound.)
+                if (a.gap && s >= 0) {
+                    const unsigned long long delta = a.mark[v];
+                    const unsigned long long gp = a.gap[s];
+                    if (gp > 2ull * delta) {
+                        a.gap[s] = gp - 2ull * delta;
+                        s = -1;
+                    }
+                }
+                a.mark[v] = 0ull;
+            }
             if (s >= 0) cls = route_class(a, s, est, d);
         }
         route_append(a, cls, s, est, d);
@@ -509,7 +573,10 @@ __global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, i
 #pragma unroll
             for (int k = 0; k < MAXD; ++k)
                 if (lab[k] == cand) cw += w[k];
-            if (cw + cw > total) continue;  // strict majority: label unchanged
+            if (cw + cw > total) {  // strict majority: label unchanged
+                store_gap<A>(a, s, cw, total);
+                continue;
+            }
         }
         const uint32_t vtx = (uint32_t)p;
         Cand<A> best = none_cand<A>();
@@ -533,6 +600,7 @@ __global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, i
         }
         const int32_t nd_new = (best.w + best.w > total) ? kMajBit : 0;
         if (nd_new != nd) a.ndist[s] = nd_new;
+        store_gap<A>(a, s, best.w, total);
         if (commit_label_known(a, p, best.lab, xv, l0v, dchg, writes) && a.mark) mark_row(a, beg, d, 0, 1);
     }
     flush_counters(a, dchg, arcs, writes, verts);
@@ -971,6 +1039,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                     if (lane == 0) {
                         arcs += d;
                         ++verts;
+                        store_gap<A>(a, s, cw, total);
                     }
                     continue;
                 }
@@ -1135,6 +1204,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                 ++verts;
                 const bool maj = WM != kFloat && wbest + wbest > total;
                 a.ndist[s] = (hashed ? ntouched : K) | (maj ? kMajBit : 0);
+                store_gap<A>(a, s, wbest, total);
                 changed = commit_label_known(a, p, winner, xv, l0v, dchg, writes);
             }
             changed = __shfl_sync(0xffffffffu, changed, 0);
@@ -1386,6 +1456,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
                 if (tid == 0) {
                     arcs += d;
                     ++verts;
+                    store_gap<A>(a, s, tot_cw, total);
                 }
                 if (!DYNAMIC) it += gridDim.x;
                 continue;
@@ -1444,6 +1515,9 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
             int32_t* gkeys = a.r.gkeys + item.gt;
             uint32_t* gfirst = a.r.gfirst + item.gt;
             unsigned long long* gacc = a.r.gacc + item.gt;
+            int32_t* gtl = a.r.gtl + item.gt;
+            const int gbits = item.gbits;
+            const int gcapv = (1 << gbits) / 4 * 3;
             if (tid == 0) s_gnew = 0;
             __syncthreads();
             for (int base = k_lo + warp * 32; base < k_hi; base += NT) {
@@ -1459,14 +1533,22 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
                 int g = -1;
                 bool isnew = false;
                 if (lab != kEmpty && lane == leader) {
-                    g = table_slot(gkeys, lab, kGlobalBits, isnew);
+                    g = table_slot(gkeys, lab, gbits, isnew);
                     if (g >= 0) {
                         atomicMin(gfirst + g, (uint32_t)k);
                         if constexpr (WM == kUnit) gacc_add<A>(gacc + g, (A)__popc(grp));
                     } else {
-                        atomicAdd(&s_gnew, 1 << 20);  // table full
+                        atomicAdd(&s_gnew, 1);  // table full
                     }
-                    if (isnew) atomicAdd(&s_gnew, 1);
+                }
+                // new entries join the table's list: one counter atomic per warp chunk
+                const uint32_t nbal = __ballot_sync(0xffffffffu, isnew);
+                if (nbal) {
+                    int t0 = 0;
+                    if (lane == __ffs(nbal) - 1) t0 = atomicAdd(a.r.gcount + item.cb, __popc(nbal));
+                    t0 = __shfl_sync(0xffffffffu, t0, __ffs(nbal) - 1);
+                    const int ti = t0 + __popc(nbal & lanemask_lt());
+                    if (isnew && ti < gcapv) gtl[ti] = g;
                 }
                 if constexpr (WM != kUnit) {
                     const int gb = __shfl_sync(0xffffffffu, g, leader);
@@ -1475,7 +1557,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
             }
             __syncthreads();
             if (tid == 0) {
-                if (s_gnew) atomicAdd(a.r.gcount + item.cb, s_gnew);
+                if (s_gnew) atomicAdd(a.r.gcount + item.cb, 1 << 28);  // table full: slow path
                 __threadfence();
                 s_last = atomicAdd(a.r.cand_done + item.cb, 1) == item.R - 1;
                 if (s_last) __threadfence();
@@ -1484,11 +1566,12 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
             last = s_last;
             if (last) {
                 const int gcount = __ldcg(a.r.gcount + item.cb);
+                const bool ok = gcount <= gcapv;
                 Best<A> b = none_best<A>();
-                if (gcount <= kGlobalCap) {
-                    for (int g = tid; g < GHB; g += NT) {
+                if (ok) {
+                    for (int i = tid; i < gcount; i += NT) {
+                        const int g = __ldcg(gtl + i);
                         const int32_t key = __ldcg(gkeys + g);
-                        if (key == kEmpty) continue;
                         Best<A> c;
                         c.w = gacc_read<A>(gacc + g);
                         c.lab = key;
@@ -1497,11 +1580,18 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
                         c.mult = 1;
                         merge_best(b, c);
                     }
-                }
-                for (int g = tid; g < GHB; g += NT) {
-                    gkeys[g] = kEmpty;
-                    gfirst[g] = 0xffffffffu;
-                    gacc[g] = 0ull;
+                    for (int i = tid; i < gcount; i += NT) {
+                        const int g = __ldcg(gtl + i);
+                        gkeys[g] = kEmpty;
+                        gfirst[g] = 0xffffffffu;
+                        gacc[g] = 0ull;
+                    }
+                } else {
+                    for (int g = tid; g < (1 << gbits); g += NT) {
+                        gkeys[g] = kEmpty;
+                        gfirst[g] = 0xffffffffu;
+                        gacc[g] = 0ull;
+                    }
                 }
                 best = block_merge(b);
                 distinct = gcount;
@@ -1509,7 +1599,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
                     a.r.cand_done[item.cb] = 0;
                     a.r.gcount[item.cb] = 0;
                 }
-                if (gcount > kGlobalCap) {
+                if (!ok) {
                     // rare slow path: labels were underestimated; this block
                     // redoes the whole row in four label partitions (or more)
                     if (tid == 0) {
@@ -1531,6 +1621,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
                 ++verts;
                 const bool maj = WM != kFloat && best.w + best.w > total;
                 a.ndist[s] = distinct | (maj ? kMajBit : 0);
+                store_gap<A>(a, s, best.w, total);
                 s_flag = commit_label(a, p, best.lab, dchg, writes) ? 1 : 0;
             }
         }
