@@ -581,6 +581,12 @@ template <int WM, int TIE> struct Launcher {
                 <<<grid, kHubThreads, team_smem_bytes<WM, kHubBits>(), st>>>(a, kLenHub);
             prof->end(st);
         }
+        // deferred marks of the rows that changed this round
+        if (a.mark) {
+            prof->begin(st, -1);
+            k_mark_pieces<<<sms * 16, 256, 0, st>>>(a);
+            prof->end(st);
+        }
     }
 };
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_warp[2] = {1, 1};
@@ -644,6 +650,8 @@ static void free_routes(Routes& r) {
     cudaFree(r.gcount);
     cudaFree(r.gslot);
     cudaFree(r.gk0);
+    cudaFree(r.cslot);
+    cudaFree(r.ck0);
     r = Routes();
 }
 
@@ -898,6 +906,8 @@ static cudaError_t alloc_routes(lp_graph* g) {
     const int64_t pieces = n + g->m / kPieceArcs + 1;
     if ((e = dalloc(&r.gslot, pieces, &g->bytes))) return e;
     if ((e = dalloc(&r.gk0, pieces, &g->bytes))) return e;
+    if ((e = dalloc(&r.cslot, pieces, &g->bytes))) return e;
+    if ((e = dalloc(&r.ck0, pieces, &g->bytes))) return e;
     if ((e = cudaMemsetAsync(r.cand_done, 0, g->cap_items * sizeof(int32_t), g->stream))) return e;
     if ((e = cudaMemsetAsync(r.gcount, 0, g->cap_items * sizeof(int32_t), g->stream))) return e;
     k_gtab_init<<<g->num_sms * 4, 256, 0, g->stream>>>(r.gkeys, r.gfirst, r.gacc, gpool);

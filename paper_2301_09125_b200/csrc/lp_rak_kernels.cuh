@@ -80,7 +80,9 @@ enum {
     kWarpCursor = 11,  // + warp class (0 / 1)
     kLenGather = 13,   // phase-1 pieces (row, arc range) of frontier rounds
     kGatherCursor = 14,
-    kLenCount = 16
+    kLenChg = 15,      // pieces of the rows whose label changed this round (deferred marks)
+    kChgCursor = 16,
+    kLenCount = 20
 };
 
 struct Routes {
@@ -99,6 +101,8 @@ struct Routes {
     int32_t* gcount;  // distinct count per slice table (indexed by cb)
     int32_t* gslot;   // frontier rounds: phase-1 pieces: slot ...
     int32_t* gk0;     // ... and first arc of the piece within the row (<= kPieceArcs arcs)
+    int32_t* cslot;   // changed rows as pieces: slot ...
+    int32_t* ck0;     // ... and first arc
 };
 
 struct EvalArgs {
@@ -385,6 +389,125 @@ __global__ void __launch_bounds__(256) k_gather_pieces(EvalArgs a, const int32_t
 }
 
 // ---------------------------------------------------------------------------
+// deferred marks
+// ---------------------------------------------------------------------------
+// A vertex whose label changed does not walk its row inline (a dependent
+// row load plus one returning atomic per 32 arcs, fully exposed in the tally
+// kernels); it appends its row, as pieces, to the changed list, and
+// k_mark_pieces walks all changed rows after the round's tally kernels with
+// eight loads in flight per lane.
+
+// one thread: push row s (d arcs)
+__device__ __forceinline__ void push_changed(const EvalArgs& a, int32_t s, int d) {
+    const int np = (d + kPieceArcs - 1) / kPieceArcs;
+    const int b0 = atomicAdd(a.r.len + kLenChg, np);
+    for (int q = 0; q < np; ++q) {
+        a.r.cslot[b0 + q] = s;
+        a.r.ck0[b0 + q] = q * kPieceArcs;
+    }
+}
+
+// active lanes of a warp, rows of <= kPieceArcs arcs: one atomic per warp
+__device__ __forceinline__ void push_changed_small(const EvalArgs& a, bool ch, int32_t s) {
+    const uint32_t act = __activemask();
+    const uint32_t bal = __ballot_sync(act, ch);
+    if (!bal) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(bal) - 1;
+    int b0 = 0;
+    if (lane == leader) b0 = atomicAdd(a.r.len + kLenChg, __popc(bal));
+    b0 = __shfl_sync(act, b0, leader);
+    if (ch) {
+        const int idx = b0 + __popc(bal & lanemask_lt());
+        a.r.cslot[idx] = s;
+        a.r.ck0[idx] = 0;
+    }
+}
+
+// whole warp: lane v pushes row (s, d) when bit v of `chm` is set
+__device__ __forceinline__ void push_changed_batch(const EvalArgs& a, uint32_t chm, int32_t s, int d) {
+    const int lane = threadIdx.x & 31;
+    const int np = ((chm >> lane) & 1u) ? (d + kPieceArcs - 1) / kPieceArcs : 0;
+    int incl = np;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    int b0 = 0;
+    if (lane == 31 && tot) b0 = atomicAdd(a.r.len + kLenChg, tot);
+    b0 = __shfl_sync(0xffffffffu, b0, 31);
+    for (int q = 0; q < np; ++q) {
+        a.r.cslot[b0 + incl - np + q] = s;
+        a.r.ck0[b0 + incl - np + q] = q * kPieceArcs;
+    }
+}
+
+// Mark the later-batch neighbours of every changed row (see mark_row); warp
+// batches of 32 pieces, flattened, eight arcs in flight per lane.
+__global__ void __launch_bounds__(256) k_mark_pieces(EvalArgs a) {
+    constexpr int J = 8;
+    const int lane = threadIdx.x & 31;
+    const int cnt = a.r.len[kLenChg];
+    while (true) {
+        int b0 = 0;
+        if (lane == 0) b0 = atomicAdd(a.r.len + kChgCursor, 32);
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (b0 >= cnt) break;
+        uint32_t pbeg = 0, plen = 0;
+        if (b0 + lane < cnt) {
+            const int32_t s = a.r.cslot[b0 + lane];
+            const uint32_t rb = __ldg(a.soff + s), re = __ldg(a.soff + s + 1);
+            pbeg = rb + (uint32_t)a.r.ck0[b0 + lane];
+            plen = min((uint32_t)kPieceArcs, re - pbeg);
+        }
+        uint32_t incl = plen;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t excl = incl - plen;
+        for (uint32_t base = 0; base < total; base += 32 * J) {
+            uint32_t e[J];
+            uint32_t nb[J];
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const uint32_t i = base + j * 32 + lane;
+                int r = 0;
+#pragma unroll
+                for (int step = 16; step >= 1; step >>= 1) {
+                    const uint32_t ex = __shfl_sync(0xffffffffu, excl, r + step);
+                    if (r + step < 32 && ex <= i) r += step;
+                }
+                const uint32_t pb = __shfl_sync(0xffffffffu, pbeg, r);
+                const uint32_t pe = __shfl_sync(0xffffffffu, excl, r);
+                e[j] = i < total ? pb + (i - pe) : 0xffffffffu;
+                nb[j] = i < total ? __ldg(a.snbr + e[j]) : 0u;
+            }
+            bool win[J];
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const int32_t u = (int32_t)(nb[j] >> 2);
+                win[j] = e[j] != 0xffffffffu && (nb[j] & kLater) && needs_mark(a, u) &&
+                         atomicAdd(a.mark + u, mark_weight(a, e[j])) == 0ull;
+            }
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, win[j]);
+                if (!bal) continue;
+                int q0 = 0;
+                if (lane == 0) q0 = atomicAdd(a.mq_len, __popc(bal));
+                q0 = __shfl_sync(0xffffffffu, q0, 0);
+                if (win[j]) a.mq_out[q0 + __popc(bal & lanemask_lt())] = (int32_t)(nb[j] >> 2);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // routing
 // ---------------------------------------------------------------------------
 // cls: 0/1/2 small (d <= 4 / 8 / 16), 3 warp, 6 big-table warp, 4 team, 5 hub
@@ -601,7 +724,8 @@ __global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, i
         const int32_t nd_new = (best.w + best.w > total) ? kMajBit : 0;
         if (nd_new != nd) a.ndist[s] = nd_new;
         store_gap<A>(a, s, best.w, total);
-        if (commit_label_known(a, p, best.lab, xv, l0v, dchg, writes) && a.mark) mark_row(a, beg, d, 0, 1);
+        const bool ch = commit_label_known(a, p, best.lab, xv, l0v, dchg, writes);
+        if (a.mark) push_changed_small(a, ch, s);
     }
     flush_counters(a, dchg, arcs, writes, verts);
 }
@@ -983,6 +1107,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                 nbr_next[c] = (k < d0) ? a.lbuf[beg0 + k] : kEmpty;
             }
         }
+        uint32_t chm = 0;  // batch vertices whose label changed (deferred marks)
         for (int v = 0; v < nv; ++v) {
             const int32_t s = __shfl_sync(0xffffffffu, ms, v);
             const int32_t p = __shfl_sync(0xffffffffu, mp, v);
@@ -1208,8 +1333,9 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                 changed = commit_label_known(a, p, winner, xv, l0v, dchg, writes);
             }
             changed = __shfl_sync(0xffffffffu, changed, 0);
-            if (changed && a.mark) mark_row(a, beg, d, lane, 32);
+            if (changed) chm |= 1u << v;
         }
+        if (a.mark) push_changed_batch(a, chm, ms, (int)(mend - mbeg));
     }
     flush_counters(a, dchg, arcs, writes, verts);
 }
@@ -1625,8 +1751,8 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int 
                 s_flag = commit_label(a, p, best.lab, dchg, writes) ? 1 : 0;
             }
         }
+        if (tid == 0 && s_flag && a.mark) push_changed(a, s, d);
         __syncthreads();
-        if (s_flag && a.mark) mark_row(a, beg, d, tid, NT);
         if (!DYNAMIC) it += gridDim.x;
     }
     flush_counters(a, dchg, arcs, writes, verts);

@@ -7,7 +7,7 @@ import sys
 rep = sys.argv[1]
 idx = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass,cuda"],
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 blocks = out.split('"Kernel Name"')
 blk = blocks[idx + 1] if len(blocks) > idx + 1 else blocks[-1]
