@@ -300,12 +300,28 @@ def run_ours(args, world, rank, local):
         "kernel_share": {k: v["ms"] / max(total_kernel_ms, 1e-9) for k, v in kernels.items()},
     }
 
-    # modularity of the final labels (untimed, the reference's parity metric)
-    from oracle import oracle as O
+    # modularity of the final labels (untimed, the reference's parity metric), on the device
+    from paper_2301_09125_b200 import quality
 
-    labels = np.empty(g.vertex_count, dtype=np.int64)
-    _lib.check(L.lp_labels_download(dg.handle, _lib.ptr(labels)))
-    q_ours = O.modularity(g, labels)
+    q_ours = quality.modularity_gpu(g, None, device_graph=dg)
+
+    # the other schedules / tie rules on the same graph (device time, inputs resident)
+    modes = {}
+    if not args.no_modes:
+        for name, kw in (("synchronous_strict", dict(batches=1, strict=True)),
+                         ("exact_nonstrict", dict(batches=0, strict=False))):
+            mp = lp.RakParams(seed=args.seed, tolerance=cfg["tolerance"], max_iterations=cfg["max_iterations"], **kw)
+            mo = lp.rak._opts(mp)
+            st = _lib.RunStats()
+            _lib.check(L.lp_rak_run_resident(dg.handle, C.byref(mo), None, C.byref(st)))  # warm
+            tms, arcs_m = 0.0, 0
+            for _ in range(3):
+                st = _lib.RunStats()
+                _lib.check(L.lp_rak_run_resident(dg.handle, C.byref(mo), None, C.byref(st)))
+                tms += st.kernel_ms
+                arcs_m += g.edge_count * st.iterations
+            modes[name] = {"gteps": arcs_m / (tms * 1e-3) / 1e9, "ms_per_run": tms / 3, "iterations": int(st.iterations),
+                           "modularity": quality.modularity_gpu(g, None, device_graph=dg)}
 
     line = {
         "metric": "RAK GTEPS on R-MAT-22 (dense-equivalent: edge_count x sweeps / time)",
@@ -325,6 +341,7 @@ def run_ours(args, world, rank, local):
         "gpu_launches": int(sum(p["launches"] for p in per)),
         "roofline": roofline,
         "modularity": q_ours,
+        "modes": modes,
         "graph_gen_s": t_gen,
     }
 
@@ -412,6 +429,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-modes", action="store_true", help="skip the secondary schedule / tie-rule timings")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -184,6 +184,13 @@ int lp_slpa_run(lp_graph* g, const lp_slpa_opts* opts, int64_t* labels_out, int6
 int lp_copra_run(lp_graph* g, const lp_copra_opts* opts, int64_t* labs_out, double* bels_out, int64_t* sizes_out,
                  int64_t* best_out, int64_t* changed_per_iter, lp_run_stats* stats);
 
+/* Modularity (quality.py:10-42) on the device, float64 accumulators:
+ * labels[n] host int64, or NULL for the labels of the last RAK run on this
+ * handle; total_weight = Graph.total_weight.  Equals the reference's value
+ * up to float64 summation order (exactly, for integer weights, up to the
+ * final sum of squares). */
+int lp_modularity(lp_graph* g, const int64_t* labels, double total_weight, double* q_out);
+
 /* Calibration (device time per pass, ms): mode 0 streams the neighbour
  * indices of the active rows once; mode 1 also gathers every neighbour's
  * label (the sweep's memory traffic without the tally).  Needs a plan

@@ -130,6 +130,7 @@ EXPORTS = (
     "lp_labels_download",
     "lp_slpa_run",
     "lp_copra_run",
+    "lp_modularity",
     "lp_calibrate",
     "lp_shuffled_indices",
     "lp_gen_rmat",
@@ -173,6 +174,7 @@ def lib():
     L.lp_rak_run.argtypes = [vp, C.POINTER(RakOpts), vp, vp, vp, vp, C.POINTER(RunStats)]
     L.lp_rak_run_resident.argtypes = [vp, C.POINTER(RakOpts), vp, C.POINTER(RunStats)]
     L.lp_labels_download.argtypes = [vp, vp]
+    L.lp_modularity.argtypes = [vp, vp, C.c_double, C.POINTER(C.c_double)]
     L.lp_copra_run.argtypes = [vp, C.POINTER(CopraOpts), vp, vp, vp, vp, vp, C.POINTER(RunStats)]
     L.lp_slpa_run.argtypes = [vp, C.POINTER(SlpaOpts), vp, vp, vp, C.POINTER(RunStats)]
     L.lp_calibrate.argtypes = [vp, C.c_int32, C.c_int32, C.POINTER(C.c_double)]

@@ -28,7 +28,7 @@ import numpy as np
 from . import _lib
 from .graph import Graph, check_symmetric
 from .prng import XorShift32, draw_bounded
-from .quality import modularity
+from .quality import score
 from .result import DetectionResult
 
 CHUNK = 1024  # the reference's parallel work unit (copra.py:31); no CUDA counterpart
@@ -132,7 +132,7 @@ def copra_detect(graph: Graph, params: CopraParams | None = None) -> DetectionRe
     best, it, _, _, _, st, changed = copra_run(graph, params, want_sets=False)
     elapsed = time.perf_counter() - start
     st["changed"] = changed
-    return DetectionResult(best, it, elapsed, modularity(graph, best), st)
+    return DetectionResult(best, it, elapsed, score(graph, best), st)
 
 
 def _select_labels(touched, tally, max_labels, rng):

@@ -1690,6 +1690,93 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
     return LP_OK;
 }
 
+// ---------------------------------------------------------------------------
+// modularity (quality.py:10-42) on the device, float64 accumulators
+// ---------------------------------------------------------------------------
+// warp per row of the input CSR: internal weight (self-loops twice) and the
+// community degrees d_c (self-loops twice, graph.degree_weights)
+__global__ void k_mod_arcs(const uint32_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                           const uint32_t* __restrict__ w, int wmode, int shift, const int32_t* __restrict__ lab,
+                           int64_t n, double* __restrict__ dc, double* internal) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
+    double in_sum = 0.0;
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; v < n; v += warps) {
+        const int32_t lv = lab[v];
+        double deg = 0.0;
+        for (uint32_t e = off[v] + lane; e < off[v + 1]; e += 32) {
+            const int32_t u = nbr[e];
+            double we = 1.0;
+            if (w) we = wmode == kFixed ? ldexp((double)w[e], -shift) : (double)__uint_as_float(w[e]);
+            if (u == (int32_t)v) we *= 2.0;
+            deg += we;
+            if (lab[u] == lv) in_sum += we;
+        }
+        for (int o = 16; o >= 1; o >>= 1) deg += __shfl_xor_sync(0xffffffffu, deg, o);
+        if (lane == 0 && deg != 0.0) atomicAdd(dc + lv, deg);
+    }
+    for (int o = 16; o >= 1; o >>= 1) in_sum += __shfl_xor_sync(0xffffffffu, in_sum, o);
+    if (lane == 0 && in_sum != 0.0) atomicAdd(internal, in_sum);
+}
+
+__global__ void k_mod_squares(const double* __restrict__ dc, int64_t n, double inv_total, double* out) {
+    double acc = 0.0;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        const double x = dc[c] * inv_total;
+        acc += x * x;
+    }
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc != 0.0) atomicAdd(out, acc);
+}
+
+__global__ void k_labels_from64(const int64_t* __restrict__ in, int32_t* __restrict__ out, int64_t n) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        out[v] = (int32_t)in[v];
+}
+
+extern "C" int lp_modularity(lp_graph* g, const int64_t* labels, double total_weight, double* q_out) {
+    if (!g || !q_out) return lp_fail(LP_ERR_INVALID, "NULL argument");
+    *q_out = 0.0;
+    if (g->n == 0 || !(total_weight > 0.0)) return LP_OK;
+    LP_CK(cudaSetDevice(g->device));
+    cudaStream_t st = g->stream;
+    const int64_t n = g->n;
+    const int32_t* lab = nullptr;
+    int32_t* tmp = nullptr;
+    if (labels) {
+        LP_CK(cudaMemcpyAsync(g->out64, labels, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        LP_CK(cudaMemsetAsync(g->counters, 0, sizeof(unsigned long long), st));
+        k_check_labels<<<g->num_sms * 4, 256, 0, st>>>(g->out64, n, g->counters);
+        unsigned long long bad = 0;
+        LP_CK(cudaMemcpyAsync(&bad, g->counters, sizeof(bad), cudaMemcpyDeviceToHost, st));
+        LP_CK(cudaStreamSynchronize(st));
+        if (bad) return lp_fail(LP_ERR_INVALID, "community labels must lie in [0, vertex_count)");
+        LP_CK(cudaMalloc(&tmp, n * sizeof(int32_t)));
+        k_labels_from64<<<g->num_sms * 8, 256, 0, st>>>(g->out64, tmp, n);
+        lab = tmp;
+    } else {
+        if (!g->labels_valid) return lp_fail(LP_ERR_INVALID, "no labels: run a detection first");
+        lab = g->cur;
+    }
+    double* dc = nullptr;
+    cudaError_t e = cudaMalloc(&dc, (n + 2) * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemsetAsync(dc, 0, (n + 2) * sizeof(double), st);
+    if (e == cudaSuccess) {
+        k_mod_arcs<<<g->num_sms * 16, 256, 0, st>>>(g->off, g->nbr, g->w, g->wmode, g->fixed_shift, lab, n, dc,
+                                                    dc + n);
+        k_mod_squares<<<g->num_sms * 8, 256, 0, st>>>(dc, n, 1.0 / total_weight, dc + n + 1);
+        e = cudaGetLastError();
+    }
+    double h[2] = {0.0, 0.0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, dc + n, 2 * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(dc);
+    cudaFree(tmp);
+    LP_CK(e);
+    *q_out = h[0] / total_weight - h[1];
+    return LP_OK;
+}
+
 extern "C" int lp_device_count(int32_t* count) {
     int c = 0;
     cudaError_t e = cudaGetDeviceCount(&c);

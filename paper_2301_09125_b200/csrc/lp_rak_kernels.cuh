@@ -169,8 +169,8 @@ constexpr int kWarpEst = WarpClass<0>::kEst;
 constexpr int kTeamEst = 2048;    // 8-warp team: 4096-slot table
 constexpr int kTeamMaxDeg = 16384;
 constexpr int kTeamBits = 12, kTeamThreads = 256;
-constexpr int kHubBits = 13, kHubThreads = 512;  // 16-warp team: 8192 slots
-constexpr int kHubPlan = 4096;     // distinct labels planned per hub partition
+constexpr int kHubBits = 14, kHubThreads = 1024;  // 32-warp team: 16384 slots
+constexpr int kHubPlan = 8192;     // distinct labels planned per hub partition
 constexpr int kSliceArcs = 8192;   // arcs per slice
 constexpr int kSliceEst = 1024;    // slicing only when distinct labels are few
 constexpr int kGlobalBits = 11;    // per-vertex global slice table: 2048 slots
@@ -1377,7 +1377,7 @@ template <typename A> __device__ __forceinline__ A gacc_read(const unsigned long
 }
 
 template <int WM, int TIE, int NT, int TBITS, bool DYNAMIC>
-__global__ void __launch_bounds__(NT, NT == 512 ? 2 : 3) k_team(EvalArgs a, int which) {
+__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_team(EvalArgs a, int which) {
     using A = typename Acc<WM>::T;
     using Tab = TeamTable<WM, TBITS>;
     constexpr int HB = Tab::HB;

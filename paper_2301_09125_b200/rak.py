@@ -44,7 +44,7 @@ import numpy as np
 from . import _lib
 from .graph import Graph, check_symmetric
 from .prng import XorShift32, draw_bounded
-from .quality import modularity
+from .quality import score
 from .result import DetectionResult
 
 # Vertices per parallel work unit in the reference's _rak_par (rak.py:36-37);
@@ -146,7 +146,7 @@ def rak_detect(graph: Graph, params: RakParams | None = None, *, order=None, lab
     elapsed = time.perf_counter() - start
     if changed_history:
         st["changed"] = changed
-    return DetectionResult(out, iterations, elapsed, modularity(graph, out), st)
+    return DetectionResult(out, iterations, elapsed, score(graph, out), st)
 
 
 def _pick_from_tally(labels_in_order, weights_by_label, strict, states, slot):

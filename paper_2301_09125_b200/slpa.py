@@ -34,7 +34,7 @@ import numpy as np
 
 from . import _lib
 from .graph import Graph, check_symmetric
-from .quality import modularity
+from .quality import score
 from .result import DetectionResult
 
 CHUNK = 1024  # the reference's parallel work unit (slpa.py:31); no CUDA counterpart
@@ -135,7 +135,7 @@ def slpa_detect(graph: Graph, params: SlpaParams | None = None) -> DetectionResu
     labels, it, _, _, st, repeats = slpa_run(graph, params, want_slots=False)
     elapsed = time.perf_counter() - start
     st["repeats"] = repeats
-    return DetectionResult(labels, it, elapsed, modularity(graph, labels), st)
+    return DetectionResult(labels, it, elapsed, score(graph, labels), st)
 
 
 def _modal(arr: np.ndarray) -> int:

@@ -7,7 +7,7 @@ TAG=${1:-r01}; shift
 set -x
 mkdir -p gpurun_out
 make -s -C paper_2301_09125_b200/csrc && make -s -C oracle
-B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline $*"
+B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-modes $*"
 $B > gpurun_out/${TAG}_bench_plain.json 2> gpurun_out/${TAG}_bench_plain.err || exit 1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct \
     --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv $B > gpurun_out/${TAG}_ncu_launches.log 2>&1

@@ -192,3 +192,45 @@ class TestEdgeCases:
                 want, it, _ = oracle.rak(g, batches=batches, tie=otie, tolerance=1e-4, max_iterations=6)
                 res = lp.rak_detect(g, lp.RakParams(tie=tie, tolerance=1e-4, max_iterations=6, batches=batches))
                 assert np.array_equal(res.assignment, want) and res.iterations == it, (tie, batches)
+
+
+def test_gpu_modularity_matches_numpy(gpu, golden_rak):
+    """quality.modularity_gpu (lp_modularity) vs the numpy restatement of
+    quality.py:10-42: same value up to float64 summation order."""
+    from paper_2301_09125_b200 import quality
+
+    rng = np.random.default_rng(3)
+    for name in ("gnp_1000", "planted_4000", "rmat_12", "rmat_12_w", "star_50", "grid_64", "isolated_12"):
+        g = load_graph(golden_rak, name)
+        n = g.vertex_count
+        for lab in (np.arange(n), np.zeros(n, dtype=np.int64), rng.integers(0, max(1, n // 7), n),
+                    lp.rak_detect(g, lp.RakParams(strict=True)).assignment):
+            q_cpu = quality.modularity(g, lab)
+            q_gpu = quality.modularity_gpu(g, lab)
+            assert q_gpu == pytest.approx(q_cpu, abs=1e-12), name
+    g = lp.rmat(16, seed=5)
+    res = lp.rak_detect(g, lp.RakParams(strict=True))
+    dg = lp._lib.device_graph(g)
+    assert quality.modularity_gpu(g, None, device_graph=dg) == pytest.approx(quality.modularity(g, res.assignment),
+                                                                             abs=1e-12)
+    with pytest.raises(ValueError):
+        quality.modularity_gpu(g, np.full(g.vertex_count, g.vertex_count))
+
+
+def test_exact_schedule_full_size_rmat20(gpu, oracle):
+    """The reference's in-place strict sweep on R-MAT-20 (1M vertices, 32M arcs):
+    labels after the run and per-sweep changed counts bit-exact to the
+    oracle's sequential restatement (which is pinned to the reference)."""
+    g = lp.rmat(20, seed=1)
+    want, it, changed = oracle.rak(g, batches=0, tie=0, seed=1, tolerance=0.05, max_iterations=20)
+    res = lp.rak_detect(g, lp.RakParams(strict=True, seed=1, tolerance=0.05, max_iterations=20),
+                        changed_history=True)
+    assert res.iterations == it
+    assert np.array_equal(res.stats["changed"], changed)
+    assert np.array_equal(res.assignment, want)
+    # and the synchronous / batched schedules against their restatements
+    for batches, tie in ((1, 0), (64, 1)):
+        want, it, changed = oracle.rak(g, batches=batches, tie=tie, seed=2, tolerance=0.05, max_iterations=20)
+        res = lp.rak_detect(g, lp.RakParams(seed=2, tolerance=0.05, max_iterations=20, batches=batches,
+                                            tie=["scan-first", "random"][tie]), changed_history=True)
+        assert res.iterations == it and np.array_equal(res.assignment, want), batches
