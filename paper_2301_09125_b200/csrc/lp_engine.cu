@@ -30,6 +30,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "../../include/labelprop_cuda.h"
@@ -59,9 +60,43 @@ enum KernelSlot : int { kKHub = 0, kKTeam = 1, kKWarp = 2, kKSmall = 3, kKSlots 
         }                                                                                            \
     } while (0)
 
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync
+// on the handle's stream, release threshold raised once): a fresh handle or
+// plan reuses the memory of earlier ones instead of paying cudaMalloc /
+// cudaFree (tens of ms for the GB-sized CSR buffers).  tl_stream is the
+// stream of the handle the calling API function works on.
+static thread_local cudaStream_t tl_stream = nullptr;
+
+struct StreamScope {
+    cudaStream_t saved;
+    explicit StreamScope(cudaStream_t s) : saved(tl_stream) { tl_stream = s; }
+    ~StreamScope() { tl_stream = saved; }
+};
+
+static cudaError_t pool_alloc(void** p, size_t bytes) {
+    return cudaMallocAsync(p, std::max<size_t>(bytes, 1), tl_stream);
+}
+template <typename T> static cudaError_t pool_alloc(T** p, size_t bytes) { return pool_alloc((void**)p, bytes); }
+
+static void dfree(void* p) {
+    if (p) cudaFreeAsync(p, tl_stream);
+}
+
 template <typename T> static cudaError_t dalloc(T** p, size_t count, int64_t* bytes) {
     *bytes += (int64_t)(count * sizeof(T));
-    return cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
+    return pool_alloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
+}
+
+// keep freed pool memory for reuse instead of returning it to the driver
+static void pool_keep(int device) {
+    static int done = -1;
+    if (done == device) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done = device;
 }
 
 // Plan kinds: RAK (seeded/custom visit order, self-loop arcs kept: the
@@ -175,6 +210,14 @@ struct lp_graph {
 __global__ void k_i64_to_u32(const int64_t* __restrict__ in, uint32_t* __restrict__ out, int64_t count) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = (uint32_t)in[i];
+}
+
+// bad[0] counts decreasing offsets
+__global__ void k_offsets_check(const int64_t* __restrict__ off, int64_t n, unsigned long long* bad) {
+    unsigned long long b = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        b += off[v + 1] < off[v];
+    if (b) atomicAdd(bad, b);
 }
 
 // neighbours -> int32 with range check; bad[0] counts out-of-range ids
@@ -305,6 +348,11 @@ __global__ void k_plan_keys(const uint32_t* __restrict__ off, const int32_t* __r
 __global__ void k_plan_vorder(const int32_t* __restrict__ pos, int32_t* __restrict__ vorder, int64_t n) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
         vorder[pos[v]] = (int32_t)v;
+}
+
+__global__ void k_iota64(int64_t* a, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = i;
 }
 
 __global__ void k_iota(int32_t* a, int64_t n) {
@@ -617,97 +665,101 @@ template <int WM> static void pick_fns(int tie, round_fn* r, setup_fn* s) {
 // graph handle
 // ---------------------------------------------------------------------------
 static void free_plan(Plan& P) {
-    cudaFree(P.pos);
-    cudaFree(P.svid);
-    cudaFree(P.slot_of);
-    cudaFree(P.soff);
-    cudaFree(P.snbr);
-    cudaFree(P.sw);
-    cudaFree(P.swsum);
-    cudaFree(P.ndist);
-    cudaFree(P.lbuf);
-    cudaFree(P.vorder);
-    cudaFree(P.wave_len);
-    cudaFree(P.dslot);
-    cudaFree(P.dk0);
-    cudaFree(P.dcount);
+    dfree(P.pos);
+    dfree(P.svid);
+    dfree(P.slot_of);
+    dfree(P.soff);
+    dfree(P.snbr);
+    dfree(P.sw);
+    dfree(P.swsum);
+    dfree(P.ndist);
+    dfree(P.lbuf);
+    dfree(P.vorder);
+    dfree(P.wave_len);
+    dfree(P.dslot);
+    dfree(P.dk0);
+    dfree(P.dcount);
     P = Plan();
 }
 
 static void free_routes(Routes& r) {
-    for (int c = 0; c < 3; ++c) cudaFree(r.small[c]);
-    cudaFree(r.warp[0]);
-    cudaFree(r.warp[1]);
-    cudaFree(r.team);
-    cudaFree(r.hub);
-    cudaFree(r.len);
-    cudaFree(r.cand);
-    cudaFree(r.cand_done);
-    cudaFree(r.gkeys);
-    cudaFree(r.gtl);
-    cudaFree(r.gfirst);
-    cudaFree(r.gacc);
-    cudaFree(r.gcount);
-    cudaFree(r.gslot);
-    cudaFree(r.gk0);
-    cudaFree(r.cslot);
-    cudaFree(r.ck0);
+    for (int c = 0; c < 3; ++c) dfree(r.small[c]);
+    dfree(r.warp[0]);
+    dfree(r.warp[1]);
+    dfree(r.team);
+    dfree(r.hub);
+    dfree(r.len);
+    dfree(r.cand);
+    dfree(r.cand_done);
+    dfree(r.gkeys);
+    dfree(r.gtl);
+    dfree(r.gfirst);
+    dfree(r.gacc);
+    dfree(r.gcount);
+    dfree(r.gslot);
+    dfree(r.gk0);
+    dfree(r.cslot);
+    dfree(r.ck0);
     r = Routes();
 }
 
 static void destroy_graph(lp_graph* g) {
     if (!g) return;
+    StreamScope ss(g->stream);
     for (Plan& P : g->plans) free_plan(P);
     free_routes(g->routes);
-    cudaFree(g->mq[0]);
-    cudaFree(g->mq[1]);
-    cudaFree(g->mq_len);
-    cudaFree(g->slots);
+    dfree(g->mq[0]);
+    dfree(g->mq[1]);
+    dfree(g->mq_len);
+    dfree(g->slots);
     for (int i = 0; i < 2; ++i) {
-        cudaFree(g->clabs[i]);
-        cudaFree(g->cbels[i]);
-        cudaFree(g->csize[i]);
-        cudaFree(g->cbest[i]);
+        dfree(g->clabs[i]);
+        dfree(g->cbels[i]);
+        dfree(g->csize[i]);
+        dfree(g->cbest[i]);
     }
-    cudaFree(g->ccur);
-    cudaFree(g->cbig);
-    cudaFree(g->cmid);
-    cudaFree(g->gelab);
-    cudaFree(g->geval);
-    cudaFree(g->gefirst);
-    cudaFree(g->grlab);
-    cudaFree(g->grval);
-    cudaFree(g->gfmap);
-    cudaFree(g->gblab);
-    cudaFree(g->gbval);
-    cudaFree(g->gbc);
-    cudaFree(g->gwc);
-    cudaFree(g->gqs);
-    cudaFree(g->off);
-    cudaFree(g->nbr);
-    cudaFree(g->w);
-    cudaFree(g->labA);
-    cudaFree(g->labB);
-    cudaFree(g->mark);
-    cudaFree(g->gap);
-    cudaFree(g->counters);
-    cudaFree(g->out64);
-    cudaFree(g->cub_tmp);
+    dfree(g->ccur);
+    dfree(g->cbig);
+    dfree(g->cmid);
+    dfree(g->gelab);
+    dfree(g->geval);
+    dfree(g->gefirst);
+    dfree(g->grlab);
+    dfree(g->grval);
+    dfree(g->gfmap);
+    dfree(g->gblab);
+    dfree(g->gbval);
+    dfree(g->gbc);
+    dfree(g->gwc);
+    dfree(g->gqs);
+    dfree(g->off);
+    dfree(g->nbr);
+    dfree(g->w);
+    dfree(g->labA);
+    dfree(g->labB);
+    dfree(g->mark);
+    dfree(g->gap);
+    dfree(g->counters);
+    dfree(g->out64);
+    dfree(g->cub_tmp);
     if (g->h_len) cudaFreeHost(g->h_len);
     if (g->h_counters) cudaFreeHost(g->h_counters);
     for (cudaEvent_t e : g->event_pool) cudaEventDestroy(e);
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
-    if (g->stream) cudaStreamDestroy(g->stream);
+    if (g->stream) {
+        cudaStreamSynchronize(g->stream);  // the pool frees above are ordered on it
+        cudaStreamDestroy(g->stream);
+    }
     delete g;
 }
 
 static int ensure_cub_tmp(lp_graph* g, size_t bytes) {
     if (bytes <= g->cub_tmp_bytes) return LP_OK;
-    cudaFree(g->cub_tmp);
+    dfree(g->cub_tmp);
     g->cub_tmp = nullptr;
     g->cub_tmp_bytes = 0;
-    LP_CK(cudaMalloc(&g->cub_tmp, bytes));
+    LP_CK(pool_alloc(&g->cub_tmp, bytes));
     g->cub_tmp_bytes = bytes;
     return LP_OK;
 }
@@ -729,14 +781,62 @@ struct TmpBufs {
     uint32_t* sdeg = nullptr;
     uint32_t* deg = nullptr;
     ~TmpBufs() {
-        cudaFree(deg);
-        cudaFree(order);
-        cudaFree(key);
-        cudaFree(key_sorted);
-        cudaFree(iota);
-        cudaFree(sdeg);
+        dfree(deg);
+        dfree(order);
+        dfree(key);
+        dfree(key_sorted);
+        dfree(iota);
+        dfree(sdeg);
     }
 };
+
+// shuffled_indices(n, seed) is a sequential Fisher-Yates pass (~17 ms for
+// n = 2^22); the last (n, seed) result is kept process-wide, so fresh graph
+// handles of the same size and seed (e.g. a re-uploaded graph) skip it.
+static void cached_shuffle(int64_t n, uint32_t seed, int64_t* out) {
+    static std::mutex mu;
+    static int64_t c_n = -1;
+    static uint32_t c_seed = 0;
+    static std::vector<int64_t> c_order;
+    std::lock_guard<std::mutex> lock(mu);
+    if (c_n != n || c_seed != seed) {
+        c_order.resize((size_t)n);
+        lp_host_shuffled_indices(n, seed, c_order.data());
+        c_n = n;
+        c_seed = seed;
+    }
+    std::memcpy(out, c_order.data(), (size_t)n * sizeof(int64_t));
+}
+
+// Device copy of the last shuffled order per device (kept for the process).
+static int device_shuffle(lp_graph* g, int64_t n, uint32_t seed, const int64_t** out) {
+    struct Entry {
+        int64_t n = -1;
+        uint32_t seed = 0;
+        int64_t* d = nullptr;
+        size_t cap = 0;
+    };
+    static std::mutex mu;
+    static Entry cache[64];
+    std::lock_guard<std::mutex> lock(mu);
+    Entry& e = cache[g->device & 63];
+    if (e.n != n || e.seed != seed) {
+        std::vector<int64_t> h((size_t)n);
+        cached_shuffle(n, seed, h.data());
+        if ((size_t)n > e.cap) {
+            if (e.d) cudaFree(e.d);
+            e.d = nullptr;
+            e.cap = 0;
+            LP_CK(cudaMalloc((void**)&e.d, std::max<size_t>((size_t)n, 1) * sizeof(int64_t)));
+            e.cap = (size_t)n;
+        }
+        LP_CK(cudaMemcpy(e.d, h.data(), (size_t)n * sizeof(int64_t), cudaMemcpyHostToDevice));
+        e.n = n;
+        e.seed = seed;
+    }
+    *out = e.d;
+    return LP_OK;
+}
 
 // Build (or reuse) the plan of a kind and visit order: positions, the
 // degree-binned storage CSR (neighbour ids), the phase-1 label buffer.
@@ -755,14 +855,13 @@ static int build_plan(lp_graph* g, int kind, const int64_t* order_host, uint32_t
         return LP_OK;
     g->bytes -= P.bytes;
     free_plan(P);
-    std::vector<int64_t> own;
-    if (!custom) {
-        own.resize((size_t)n);
-        if (index)
-            for (int64_t i = 0; i < n; ++i) own[(size_t)i] = i;
-        else
-            lp_host_shuffled_indices(n, seed, own.data());
-        order_host = own.data();
+    // the visit order on the device: identity (INDEX), the caller's, or
+    // shuffled_indices(n, seed) from the process-wide device cache
+    const int64_t* order_dev = nullptr;
+    if (index) {
+        order_dev = nullptr;  // generated on the device below
+    } else if (!custom) {
+        if (int rc = device_shuffle(g, n, seed, &order_dev)) return rc;
     }
     cudaStream_t st = g->stream;
     LP_CK(cudaEventRecord(g->ev0, st));
@@ -779,7 +878,12 @@ static int build_plan(lp_graph* g, int kind, const int64_t* order_host, uint32_t
     LP_CK(dalloc(&t.iota, n, &tmpb));
     LP_CK(dalloc(&t.sdeg, n + 1, &tmpb));
     LP_CK(dalloc(&t.deg, n, &tmpb));
-    LP_CK(cudaMemcpyAsync(t.order, order_host, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    if (custom)
+        LP_CK(cudaMemcpyAsync(t.order, order_host, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    else if (order_dev)
+        LP_CK(cudaMemcpyAsync(t.order, order_dev, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    else
+        k_iota64<<<g->num_sms * 8, 256, 0, st>>>(t.order, n);
     LP_CK(cudaMemsetAsync(g->counters, 0, 8 * sizeof(unsigned long long), st));
     LP_CK(cudaMemsetAsync(P.pos, 0xff, n * sizeof(int32_t), st));
     const int G = g->num_sms * 8;
@@ -925,8 +1029,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (m > 0 && !neighbors) return lp_fail(LP_ERR_INVALID, "neighbors is NULL");
     if (n > 0 && (offsets[0] != 0 || offsets[n] != m))
         return lp_fail(LP_ERR_INVALID, "offsets must start at 0 and end at edge_count");
-    for (int64_t v = 0; v < n; ++v)
-        if (offsets[v + 1] < offsets[v]) return lp_fail(LP_ERR_INVALID, "offsets must be non-decreasing");
+    // (monotonicity of offsets is checked on the device after the upload)
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return lp_fail(LP_ERR_CUDA, "no CUDA device available (liblabelprop_cuda needs a B200)");
@@ -951,6 +1054,8 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
                                 "CUDA error %s at %s:%d", cudaGetErrorName(_e), __FILE__, __LINE__)); \
     } while (0)
     G_CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    StreamScope ss(g->stream);
+    pool_keep(g->device);
     G_CK(cudaEventCreate(&g->ev0));
     G_CK(cudaEventCreate(&g->ev1));
     cudaStream_t st = g->stream;
@@ -976,6 +1081,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
         G_CK(dalloc(&tmp, std::max(n + 1, m), &tb));
         G_CK(cudaMemcpyAsync(tmp, offsets, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
         k_i64_to_u32<<<g->num_sms * 8, 256, 0, st>>>(tmp, g->off, n + 1);
+        k_offsets_check<<<g->num_sms * 8, 256, 0, st>>>(tmp, n, g->counters + 11);
         if (m > 0) {
             G_CK(cudaMemcpyAsync(tmp, neighbors, m * sizeof(int64_t), cudaMemcpyHostToDevice, st));
             k_nbr_convert<<<g->num_sms * 8, 256, 0, st>>>(tmp, g->nbr, m, n, g->counters);
@@ -989,8 +1095,12 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
         k_degree_stats<<<g->num_sms * 8, 256, 0, st>>>(g->off, n, g->counters + 8);
         G_CK(cudaMemcpyAsync(g->h_counters, g->counters, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         G_CK(cudaStreamSynchronize(st));
+        if (g->h_counters[11]) {
+            dfree(tmp);
+            return fail(lp_fail(LP_ERR_INVALID, "offsets must be non-decreasing"));
+        }
         if (g->h_counters[0]) {
-            cudaFree(tmp);
+            dfree(tmp);
             return fail(lp_fail(LP_ERR_INVALID, "neighbor ids must lie in [0, vertex_count)"));
         }
         g->max_degree = (int64_t)g->h_counters[8];
@@ -1014,7 +1124,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
             k_weight_convert<<<g->num_sms * 8, 256, 0, st>>>((const double*)tmp, g->w, m, g->wmode, g->fixed_shift);
         }
         G_CK(cudaStreamSynchronize(st));
-        cudaFree(tmp);
+        dfree(tmp);
     }
     G_CK(alloc_routes(g));
     G_CK(cudaStreamSynchronize(st));
@@ -1050,13 +1160,14 @@ extern "C" void* lp_graph_stream(lp_graph* g) { return g ? (void*)g->stream : nu
 static int ensure_waves(lp_graph* g, int W) {
     Plan& P = g->plan();
     if (P.waves == W && P.wave_len) return LP_OK;
-    cudaFree(P.wave_len);
+    dfree(P.wave_len);
     P.wave_len = nullptr;
-    LP_CK(cudaMalloc(&P.wave_len, W * sizeof(int32_t)));
+    LP_CK(pool_alloc(&P.wave_len, W * sizeof(int32_t)));
     std::vector<int32_t> h((size_t)W);
     const int64_t ws = (g->n + W - 1) / W;
     for (int w = 0; w < W; ++w) h[(size_t)w] = (int32_t)std::max<int64_t>(0, std::min<int64_t>(ws, g->n - w * ws));
-    LP_CK(cudaMemcpy(P.wave_len, h.data(), W * sizeof(int32_t), cudaMemcpyHostToDevice));
+    LP_CK(cudaMemcpyAsync(P.wave_len, h.data(), W * sizeof(int32_t), cudaMemcpyHostToDevice, g->stream));
+    LP_CK(cudaStreamSynchronize(g->stream));
     P.waves = W;
     return LP_OK;
 }
@@ -1167,6 +1278,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     if (o->tie < 0 || o->tie > 2) return lp_fail(LP_ERR_INVALID, "unknown tie rule");
     if (o->batches < 0) return lp_fail(LP_ERR_INVALID, "batches must be >= 0");
     LP_CK(cudaSetDevice(g->device));
+    StreamScope ss(g->stream);
     lp_run_stats st_local;
     lp_run_stats* S = stats ? stats : &st_local;
     memset(S, 0, sizeof(*S));
@@ -1305,6 +1417,7 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     if (o->tie < 0 || o->tie > 2) return lp_fail(LP_ERR_INVALID, "unknown tie rule");
     if (o->batches < 0) return lp_fail(LP_ERR_INVALID, "batches must be >= 0");
     LP_CK(cudaSetDevice(g->device));
+    StreamScope ss(g->stream);
     lp_run_stats st_local;
     lp_run_stats* S = stats ? stats : &st_local;
     memset(S, 0, sizeof(*S));
@@ -1333,10 +1446,10 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     LP_CK(setup(g->device));
     const size_t cells = (size_t)n * T;
     if (cells > g->slots_cap) {
-        cudaFree(g->slots);
+        dfree(g->slots);
         g->slots = nullptr;
         g->slots_cap = 0;
-        LP_CK(cudaMalloc(&g->slots, cells * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->slots, cells * sizeof(int32_t)));
         g->slots_cap = cells;
     }
     int32_t* A = g->labA;  // previous appends (round 1: own ids, the guess)
@@ -1411,11 +1524,11 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     }
     if (slots_out) {
         int64_t* tmp = nullptr;
-        LP_CK(cudaMalloc(&tmp, cells * sizeof(int64_t)));
+        LP_CK(pool_alloc(&tmp, cells * sizeof(int64_t)));
         k_slots_to64<<<g->num_sms * 8, 256, 0, st>>>(g->slots, tmp, (int64_t)cells);
         cudaError_t e = cudaMemcpyAsync(slots_out, tmp, cells * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        cudaFree(tmp);
+        dfree(tmp);
         LP_CK(e);
     }
     return LP_OK;
@@ -1429,43 +1542,43 @@ static int copra_buffers(lp_graph* g, int K) {
     const size_t cells = (size_t)n * K;
     if (cells > g->ccap) {
         for (int i = 0; i < 2; ++i) {
-            cudaFree(g->clabs[i]);
-            cudaFree(g->cbels[i]);
+            dfree(g->clabs[i]);
+            dfree(g->cbels[i]);
             g->clabs[i] = nullptr;
             g->cbels[i] = nullptr;
         }
         g->ccap = 0;
         for (int i = 0; i < 2; ++i) {
-            LP_CK(cudaMalloc(&g->clabs[i], cells * sizeof(int32_t)));
-            LP_CK(cudaMalloc(&g->cbels[i], cells * sizeof(double)));
+            LP_CK(pool_alloc(&g->clabs[i], cells * sizeof(int32_t)));
+            LP_CK(pool_alloc(&g->cbels[i], cells * sizeof(double)));
         }
         g->ccap = cells;
     }
     if (!g->csize[0]) {
         for (int i = 0; i < 2; ++i) {
-            LP_CK(cudaMalloc(&g->csize[i], std::max<int64_t>(n, 1) * sizeof(int32_t)));
-            LP_CK(cudaMalloc(&g->cbest[i], std::max<int64_t>(n, 1) * sizeof(int32_t)));
+            LP_CK(pool_alloc(&g->csize[i], std::max<int64_t>(n, 1) * sizeof(int32_t)));
+            LP_CK(pool_alloc(&g->cbest[i], std::max<int64_t>(n, 1) * sizeof(int32_t)));
         }
-        LP_CK(cudaMalloc(&g->ccur, 8 * sizeof(int32_t)));
-        LP_CK(cudaMalloc(&g->cbig, std::max<int64_t>(n, 1) * sizeof(int32_t)));
-        LP_CK(cudaMalloc(&g->cmid, std::max<int64_t>(n, 1) * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->ccur, 8 * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->cbig, std::max<int64_t>(n, 1) * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->cmid, std::max<int64_t>(n, 1) * sizeof(int32_t)));
     }
     // team scratch: a row sees at most min(n, max_degree * K) distinct labels and
     // max_degree * K contributions; blocks bounded by a 4 GiB budget
     const size_t con = (size_t)std::max<int64_t>(1, g->max_degree) * K;
     const size_t ent = std::min<size_t>((size_t)n, con);
     if (ent > g->gent || con > g->gcon) {
-        cudaFree(g->gelab);
-        cudaFree(g->geval);
-        cudaFree(g->gefirst);
-        cudaFree(g->grlab);
-        cudaFree(g->grval);
-        cudaFree(g->gfmap);
-        cudaFree(g->gblab);
-        cudaFree(g->gbval);
-        cudaFree(g->gbc);
-        cudaFree(g->gwc);
-        cudaFree(g->gqs);
+        dfree(g->gelab);
+        dfree(g->geval);
+        dfree(g->gefirst);
+        dfree(g->grlab);
+        dfree(g->grval);
+        dfree(g->gfmap);
+        dfree(g->gblab);
+        dfree(g->gbval);
+        dfree(g->gbc);
+        dfree(g->gwc);
+        dfree(g->gqs);
         g->gelab = g->gefirst = g->grlab = g->gfmap = g->gblab = g->gbc = g->gwc = g->gqs = nullptr;
         g->geval = g->grval = g->gbval = nullptr;
         g->gent = g->gcon = 0;
@@ -1473,17 +1586,17 @@ static int copra_buffers(lp_graph* g, int K) {
         const size_t per = ent * (3 * sizeof(int32_t) + 2 * sizeof(double)) +
                            con * (3 * sizeof(int32_t) + sizeof(double)) + parts * sizeof(int32_t);
         const int blocks = (int)std::max<size_t>(1, std::min<size_t>(2 * g->num_sms, ((size_t)6 << 30) / per));
-        LP_CK(cudaMalloc(&g->gelab, ent * blocks * sizeof(int32_t)));
-        LP_CK(cudaMalloc(&g->geval, ent * blocks * sizeof(double)));
-        LP_CK(cudaMalloc(&g->gefirst, ent * blocks * sizeof(int32_t)));
-        LP_CK(cudaMalloc(&g->grlab, ent * blocks * sizeof(int32_t)));
-        LP_CK(cudaMalloc(&g->grval, ent * blocks * sizeof(double)));
-        LP_CK(cudaMalloc(&g->gfmap, con * blocks * sizeof(int32_t)));
-        LP_CK(cudaMalloc(&g->gblab, con * blocks * sizeof(int32_t)));
-        LP_CK(cudaMalloc(&g->gbval, con * blocks * sizeof(double)));
-        LP_CK(cudaMalloc(&g->gbc, con * blocks * sizeof(int32_t)));
-        LP_CK(cudaMalloc(&g->gwc, (size_t)kCopraTeamWarps * kCopraMaxParts * blocks * sizeof(int32_t)));
-        LP_CK(cudaMalloc(&g->gqs, (size_t)(kCopraMaxParts + 1) * blocks * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->gelab, ent * blocks * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->geval, ent * blocks * sizeof(double)));
+        LP_CK(pool_alloc(&g->gefirst, ent * blocks * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->grlab, ent * blocks * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->grval, ent * blocks * sizeof(double)));
+        LP_CK(pool_alloc(&g->gfmap, con * blocks * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->gblab, con * blocks * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->gbval, con * blocks * sizeof(double)));
+        LP_CK(pool_alloc(&g->gbc, con * blocks * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->gwc, (size_t)kCopraTeamWarps * kCopraMaxParts * blocks * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->gqs, (size_t)(kCopraMaxParts + 1) * blocks * sizeof(int32_t)));
         k_fill_i32<<<g->num_sms * 8, 256, 0, g->stream>>>(g->gfmap, -1, (int64_t)(con * blocks));
         LP_CK(cudaGetLastError());
         g->gent = ent;
@@ -1509,6 +1622,7 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
     if (!best_out) return lp_fail(LP_ERR_INVALID, "best_out is NULL");
     if ((labs_out == nullptr) != (bels_out == nullptr)) return lp_fail(LP_ERR_INVALID, "labs_out and bels_out go together");
     LP_CK(cudaSetDevice(g->device));
+    StreamScope ss(g->stream);
     lp_run_stats st_local;
     lp_run_stats* S = stats ? stats : &st_local;
     memset(S, 0, sizeof(*S));
@@ -1669,10 +1783,10 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
     int64_t* best64 = g->out64;
     cudaError_t e = cudaSuccess;
     if (labs_out) {
-        e = cudaMalloc(&l64, cells * sizeof(int64_t));
-        if (e == cudaSuccess) e = cudaMalloc(&b64, cells * sizeof(double));
+        e = pool_alloc(&l64, cells * sizeof(int64_t));
+        if (e == cudaSuccess) e = pool_alloc(&b64, cells * sizeof(double));
     }
-    if (e == cudaSuccess && sizes_out) e = cudaMalloc(&s64, n * sizeof(int64_t));
+    if (e == cudaSuccess && sizes_out) e = pool_alloc(&s64, n * sizeof(int64_t));
     if (e == cudaSuccess) {
         k_copra_download<<<g->num_sms * 8, 256, 0, st>>>(g->clabs[c0], g->cbels[c0], g->csize[c0], g->cbest[c0], l64,
                                                         b64, s64, best64, n, K, K);
@@ -1683,9 +1797,9 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
     if (e == cudaSuccess && labs_out) e = cudaMemcpyAsync(bels_out, b64, cells * sizeof(double), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess && sizes_out) e = cudaMemcpyAsync(sizes_out, s64, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    cudaFree(l64);
-    cudaFree(b64);
-    cudaFree(s64);
+    dfree(l64);
+    dfree(b64);
+    dfree(s64);
     LP_CK(e);
     return LP_OK;
 }
@@ -1739,6 +1853,7 @@ extern "C" int lp_modularity(lp_graph* g, const int64_t* labels, double total_we
     *q_out = 0.0;
     if (g->n == 0 || !(total_weight > 0.0)) return LP_OK;
     LP_CK(cudaSetDevice(g->device));
+    StreamScope ss(g->stream);
     cudaStream_t st = g->stream;
     const int64_t n = g->n;
     const int32_t* lab = nullptr;
@@ -1751,7 +1866,7 @@ extern "C" int lp_modularity(lp_graph* g, const int64_t* labels, double total_we
         LP_CK(cudaMemcpyAsync(&bad, g->counters, sizeof(bad), cudaMemcpyDeviceToHost, st));
         LP_CK(cudaStreamSynchronize(st));
         if (bad) return lp_fail(LP_ERR_INVALID, "community labels must lie in [0, vertex_count)");
-        LP_CK(cudaMalloc(&tmp, n * sizeof(int32_t)));
+        LP_CK(pool_alloc(&tmp, n * sizeof(int32_t)));
         k_labels_from64<<<g->num_sms * 8, 256, 0, st>>>(g->out64, tmp, n);
         lab = tmp;
     } else {
@@ -1759,7 +1874,7 @@ extern "C" int lp_modularity(lp_graph* g, const int64_t* labels, double total_we
         lab = g->cur;
     }
     double* dc = nullptr;
-    cudaError_t e = cudaMalloc(&dc, (n + 2) * sizeof(double));
+    cudaError_t e = pool_alloc(&dc, (n + 2) * sizeof(double));
     if (e == cudaSuccess) e = cudaMemsetAsync(dc, 0, (n + 2) * sizeof(double), st);
     if (e == cudaSuccess) {
         k_mod_arcs<<<g->num_sms * 16, 256, 0, st>>>(g->off, g->nbr, g->w, g->wmode, g->fixed_shift, lab, n, dc,
@@ -1770,8 +1885,8 @@ extern "C" int lp_modularity(lp_graph* g, const int64_t* labels, double total_we
     double h[2] = {0.0, 0.0};
     if (e == cudaSuccess) e = cudaMemcpyAsync(h, dc + n, 2 * sizeof(double), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    cudaFree(dc);
-    cudaFree(tmp);
+    dfree(dc);
+    dfree(tmp);
     LP_CK(e);
     *q_out = h[0] / total_weight - h[1];
     return LP_OK;

@@ -106,9 +106,9 @@ def rak_labels(graph: Graph, params: RakParams | None = None, *, order=None, lab
     if params is None:
         params = RakParams()
     n = graph.vertex_count
-    out = np.arange(n, dtype=np.int64)
     if n == 0:
-        return out, 0, {}, np.zeros(0, dtype=np.int64)
+        return np.zeros(0, dtype=np.int64), 0, {}, np.zeros(0, dtype=np.int64)
+    out = np.empty(n, dtype=np.int64)  # written by lp_rak_run
     dg = device_graph if device_graph is not None else _lib.device_graph(graph)
     opts = _opts(params)
     if profile:

@@ -234,3 +234,16 @@ def test_exact_schedule_full_size_rmat20(gpu, oracle):
         res = lp.rak_detect(g, lp.RakParams(seed=2, tolerance=0.05, max_iterations=20, batches=batches,
                                             tie=["scan-first", "random"][tie]), changed_history=True)
         assert res.iterations == it and np.array_equal(res.assignment, want), batches
+
+
+def test_malformed_csr_rejected_on_upload(gpu):
+    from paper_2301_09125_b200 import _lib
+
+    off = np.array([0, 2, 1, 3], dtype=np.int64)  # decreasing
+    nbr = np.array([0, 1, 2], dtype=np.int64)
+    g = lp.Graph(3, 3, off, nbr, np.ones(3), 3.0)
+    with pytest.raises(ValueError, match="non-decreasing"):
+        _lib.DeviceGraph(g)
+    g = lp.Graph(3, 3, np.array([0, 1, 2, 3]), np.array([0, 1, 7]), np.ones(3), 3.0)
+    with pytest.raises(ValueError, match="neighbor ids"):
+        _lib.DeviceGraph(g)
