@@ -4,10 +4,10 @@ Drop-in for the reference's ``labelprop.copra`` (`pkg/src/labelprop/
 copra.py`): ``CopraParams`` keeps the reference's fields, defaults and
 validation (`copra.py:34-50`) plus defaulted ``batches`` / ``backend``;
 ``copra_detect`` keeps the signature and result contract
-(`copra.py:286-292`); ``collect_and_threshold`` and ``best_label`` keep the
-helper semantics (`copra.py:295-336`).
+(`copra.py:292-297`); ``collect_and_threshold`` and ``best_label`` keep the
+helper semantics (`copra.py:300-338`).
 
-The sweeps (`copra.py:124-237`) run in one call into
+The sweeps (`copra.py:124-238`) run in one call into
 ``liblabelprop_cuda.so`` (``lp_copra_run``, kernels in
 ``csrc/lp_copra_kernels.cuh``).  Belongings are float64 and every
 arithmetic step follows the reference's order, so label sets match the CPU
@@ -103,7 +103,7 @@ def copra_run(graph: Graph, params: CopraParams | None = None, *, want_sets: boo
 
 
 def _detect_full(graph: Graph, params: CopraParams, check_invariants: bool = False):
-    """Run COPRA and return the full final state (ref `copra.py:240-283`):
+    """Run COPRA and return the full final state (ref `copra.py:241-289`):
     ``(best, iterations, elapsed, stats, labs, bels, sizes)``; ``stats`` =
     [max |sum(bels) - 1|, min size, max size] (computed on the host here)."""
     if __debug__:
@@ -121,7 +121,7 @@ def _detect_full(graph: Graph, params: CopraParams, check_invariants: bool = Fal
 
 
 def copra_detect(graph: Graph, params: CopraParams | None = None) -> DetectionResult:
-    """Run COPRA on a preprocessed graph; the assignment is each best label (ref `copra.py:286-292`)."""
+    """Run COPRA on a preprocessed graph; the assignment is each best label (ref `copra.py:292-297`)."""
     if params is None:
         params = CopraParams()
     if __debug__:
@@ -161,7 +161,7 @@ def _select_labels(touched, tally, max_labels, rng):
 
 def collect_and_threshold(labels, weights, max_labels: int, rng: XorShift32):
     """Apply the normalize/threshold/fallback/renormalize step to one tally
-    (ref `copra.py:295-322`).  Returns (labels, belongings) sorted by label id."""
+    (ref `copra.py:300-324`).  Returns (labels, belongings) sorted by label id."""
     labs = np.asarray(labels, dtype=np.int64)
     wts = np.asarray(weights, dtype=np.float64)
     if labs.size == 0:
@@ -178,7 +178,7 @@ def collect_and_threshold(labels, weights, max_labels: int, rng: XorShift32):
 
 
 def best_label(labels, belongings) -> int:
-    """Maximum-belonging label; ties break to the smallest label id (ref `copra.py:325-336`)."""
+    """Maximum-belonging label; ties break to the smallest label id (ref `copra.py:327-338`)."""
     labs = np.asarray(labels, dtype=np.int64)
     bels = np.asarray(belongings, dtype=np.float64)
     if labs.size == 0:

@@ -4,8 +4,8 @@ Drop-in for the reference's ``labelprop.slpa`` (`pkg/src/labelprop/
 slpa.py`): ``SlpaParams`` keeps the reference's fields, defaults and
 validation (`slpa.py:34-48`) and adds defaulted ``batches`` / ``tie`` /
 ``backend`` fields; ``slpa_detect`` keeps the signature and result contract
-(`slpa.py:196-201`); ``most_popular_label`` keeps the helper
-(`slpa.py:204-209`).
+(`slpa.py:189-194`); ``most_popular_label`` keeps the helper
+(`slpa.py:197-202`).
 
 The speaking rounds and the projection (`slpa.py:91-150`) run in one call
 into ``liblabelprop_cuda.so`` (``lp_slpa_run``): each round is the RAK
@@ -89,7 +89,7 @@ def slpa_run(graph: Graph, params: SlpaParams | None = None, *, want_slots: bool
 
     Returns ``(labels, iterations, slots, filled, stats, repeats_per_round)``
     -- ``slots``/``filled`` as the reference's ``_detect_full`` returns them
-    (`slpa.py:164-193`; ``slots`` is None without ``want_slots``).
+    (`slpa.py:154-186`; ``slots`` is None without ``want_slots``).
     """
     if params is None:
         params = SlpaParams()
@@ -114,7 +114,7 @@ def slpa_run(graph: Graph, params: SlpaParams | None = None, *, want_slots: bool
 
 
 def _detect_full(graph: Graph, params: SlpaParams):
-    """Run SLPA and return (labels, iterations, elapsed, slots, filled) (ref `slpa.py:164-193`)."""
+    """Run SLPA and return (labels, iterations, elapsed, slots, filled) (ref `slpa.py:154-186`)."""
     if __debug__:
         check_symmetric(graph)
     start = time.perf_counter()
@@ -124,7 +124,7 @@ def _detect_full(graph: Graph, params: SlpaParams):
 
 
 def slpa_detect(graph: Graph, params: SlpaParams | None = None) -> DetectionResult:
-    """Run SLPA on a preprocessed graph; the assignment is each modal label (ref `slpa.py:196-201`)."""
+    """Run SLPA on a preprocessed graph; the assignment is each modal label (ref `slpa.py:189-194`)."""
     if params is None:
         params = SlpaParams()
     if __debug__:
@@ -145,7 +145,7 @@ def _modal(arr: np.ndarray) -> int:
 
 
 def most_popular_label(memory) -> int:
-    """Modal label of a memory; frequency ties break to the smallest id (ref `slpa.py:204-209`)."""
+    """Modal label of a memory; frequency ties break to the smallest id (ref `slpa.py:197-202`)."""
     arr = np.asarray(memory, dtype=np.int64)
     if arr.size == 0:
         raise ValueError("empty memory")
