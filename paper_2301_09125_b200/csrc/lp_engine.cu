@@ -522,7 +522,7 @@ struct Prof {
 
 template <int WM, int TIE> struct Launcher {
     using A = typename Acc<WM>::T;
-    static int occ_warp[2], occ_team, occ_hub, done_device;
+    static int occ_warp[2], occ_team, occ_team2, occ_hub, done_device;
     template <int WC> static cudaError_t setup_warp() {
         cudaError_t e = cudaFuncSetAttribute(k_warp<WM, TIE, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)warp_smem_bytes<WM, WC>());
@@ -540,6 +540,13 @@ template <int WM, int TIE> struct Launcher {
         e = cudaFuncSetAttribute(k_team<WM, TIE, kTeamThreads, kTeamBits, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)team_smem_bytes<WM, kTeamBits>());
         if (e) return e;
+        e = cudaFuncSetAttribute(k_team<WM, TIE, kTeam2Threads, kTeam2Bits, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)team_smem_bytes<WM, kTeam2Bits>());
+        if (e) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_team2, k_team<WM, TIE, kTeam2Threads, kTeam2Bits, true>,
+                                                          kTeam2Threads, team_smem_bytes<WM, kTeam2Bits>());
+        if (e) return e;
+        occ_team2 = std::max(occ_team2, 1);
         e = cudaFuncSetAttribute(k_team<WM, TIE, kHubThreads, kHubBits, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)team_smem_bytes<WM, kHubBits>());
         if (e) return e;
@@ -621,6 +628,14 @@ template <int WM, int TIE> struct Launcher {
                 <<<sms * occ_team, kTeamThreads, team_smem_bytes<WM, kTeamBits>(), st>>>(a, kLenTeam);
             prof->end(st);
         }
+        if (big || h_len[kLenTeam2] > 0) {
+            a.bin = kKTeam;
+            prof->begin(st, kKTeam);
+            const int grid = dense ? sms * occ_team2 : grid_for(h_len[kLenTeam2], 1, sms * occ_team2);
+            k_team<WM, TIE, kTeam2Threads, kTeam2Bits, true>
+                <<<grid, kTeam2Threads, team_smem_bytes<WM, kTeam2Bits>(), st>>>(a, kLenTeam2);
+            prof->end(st);
+        }
         if (big || h_len[kLenHub] > 0) {
             a.bin = kKHub;
             prof->begin(st, kKHub);
@@ -639,6 +654,7 @@ template <int WM, int TIE> struct Launcher {
 };
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_warp[2] = {1, 1};
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_team = 1;
+template <int WM, int TIE> int Launcher<WM, TIE>::occ_team2 = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_hub = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::done_device = -1;
 
@@ -687,6 +703,7 @@ static void free_routes(Routes& r) {
     dfree(r.warp[0]);
     dfree(r.warp[1]);
     dfree(r.team);
+    dfree(r.team2);
     dfree(r.hub);
     dfree(r.len);
     dfree(r.cand);
@@ -997,6 +1014,7 @@ static cudaError_t alloc_routes(lp_graph* g) {
     if ((e = dalloc(&r.warp[0], n, &g->bytes))) return e;
     if ((e = dalloc(&r.warp[1], n, &g->bytes))) return e;
     if ((e = dalloc(&r.team, 2 * n, &g->bytes))) return e;
+    if ((e = dalloc(&r.team2, n, &g->bytes))) return e;
     if ((e = dalloc(&r.hub, g->cap_items, &g->bytes))) return e;
     if ((e = dalloc(&r.len, kLenCount, &g->bytes))) return e;
     if ((e = dalloc(&r.cand, g->cap_items, &g->bytes))) return e;
@@ -1222,9 +1240,9 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         if (g->debug_rounds) {
             int32_t ql = 0;
             cudaMemcpy(&ql, g->mq_len + q, sizeof(int32_t), cudaMemcpyDeviceToHost);
-            fprintf(stderr, "[lp] round %d: queue %d small %d/%d/%d warp %d warpbig %d team %d hub-items %d pieces %d\n",
+            fprintf(stderr, "[lp] round %d: queue %d small %d/%d/%d warp %d warpbig %d team %d team2 %d hub-items %d pieces %d\n",
                     *rounds, ql, g->h_len[kLenS16], g->h_len[kLenS16 - 1], g->h_len[kLenS16 - 2], g->h_len[kLenWarp],
-                    g->h_len[kLenWarpBig], g->h_len[kLenTeam], g->h_len[kLenHub], g->h_len[kLenGather]);
+                    g->h_len[kLenWarpBig], g->h_len[kLenTeam], g->h_len[kLenTeam2], g->h_len[kLenHub], g->h_len[kLenGather]);
         }
         if (g->h_len[kLenGather] == 0) break;
         q ^= 1;

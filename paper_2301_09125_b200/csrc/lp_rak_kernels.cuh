@@ -82,6 +82,8 @@ enum {
     kGatherCursor = 14,
     kLenChg = 15,      // pieces of the rows whose label changed this round (deferred marks)
     kChgCursor = 16,
+    kLenTeam2 = 17,    // 16-warp team, 8192-slot table (est <= kTeam2Est, d <= kTeamMaxDeg)
+    kTeam2Cursor = 18,
     kLenCount = 20
 };
 
@@ -89,6 +91,7 @@ struct Routes {
     int32_t* small[3];  // slot lists by small degree class (4, 8, 16)
     int32_t* warp[2];   // slot lists of the two warp classes
     Item* team;
+    Item* team2;
     Item* hub;
     int32_t* len;  // kLen*
     HubCand* cand;
@@ -169,6 +172,8 @@ constexpr int kWarpEst = WarpClass<0>::kEst;
 constexpr int kTeamEst = 2048;    // 8-warp team: 4096-slot table
 constexpr int kTeamMaxDeg = 16384;
 constexpr int kTeamBits = 12, kTeamThreads = 256;
+constexpr int kTeam2Bits = 13, kTeam2Threads = 512;  // 16-warp team: 8192 slots
+constexpr int kTeam2Est = 6144;
 constexpr int kHubBits = 14, kHubThreads = 1024;  // 32-warp team: 16384 slots
 constexpr int kHubPlan = 8192;     // distinct labels planned per hub partition
 constexpr int kSliceArcs = 8192;   // arcs per slice
@@ -524,6 +529,7 @@ __device__ __forceinline__ int route_class(const EvalArgs& a, int32_t s, int& es
     if (est <= WarpClass<0>::kEst && d <= WarpClass<0>::kMaxDeg) return 3;
     if (est <= WarpClass<1>::kEst && d <= WarpClass<1>::kMaxDeg) return 6;
     if (est <= kTeamEst && d <= kTeamMaxDeg) return 4;
+    if (est <= kTeam2Est && d <= kTeamMaxDeg) return 7;
     return 5;
 }
 
@@ -533,13 +539,13 @@ __device__ __forceinline__ void route_append(const EvalArgs& a, int cls, int32_t
     const int lane = threadIdx.x & 31;
     const uint32_t act = __activemask();
 #pragma unroll
-    for (int c = 0; c < 7; ++c) {
+    for (int c = 0; c < 8; ++c) {
         if (c == 5) continue;  // hubs below
         const uint32_t m = __ballot_sync(act, cls == c);
         if (!m) continue;
         const int leader = __ffs(m) - 1;
         int base = 0;
-        if (lane == leader) base = atomicAdd(a.r.len + c, __popc(m));
+        if (lane == leader) base = atomicAdd(a.r.len + (c == 7 ? kLenTeam2 : c), __popc(m));
         base = __shfl_sync(act, base, leader);
         if (cls == c) {
             const int idx = base + __popc(m & lanemask_lt());
@@ -551,7 +557,7 @@ __device__ __forceinline__ void route_append(const EvalArgs& a, int cls, int32_t
                 a.r.warp[1][idx] = s;
             } else {
                 Item t = {s, 0, 1, 0, 1, -1, 0, 0};
-                a.r.team[idx] = t;
+                (c == 7 ? a.r.team2 : a.r.team)[idx] = t;
             }
         }
     }
@@ -1405,8 +1411,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
     const int lane = tid & 31;
     const int warp = tid >> 5;
     for (int h = tid; h < HB; h += NT) tab->t.init(h);
-    const Item* items = which == kLenHub ? a.r.hub : a.r.team;
-    const int cursor = which == kLenHub ? kHubCursor : kTeamCursor;
+    const Item* items = which == kLenHub ? a.r.hub : (which == kLenTeam2 ? a.r.team2 : a.r.team);
+    const int cursor = which == kLenHub ? kHubCursor : (which == kLenTeam2 ? kTeam2Cursor : kTeamCursor);
     long long dchg = 0, arcs = 0, writes = 0, verts = 0;
     int32_t it = blockIdx.x;
     __syncthreads();
