@@ -200,6 +200,8 @@ struct lp_graph {
     int waves = 1;  // dense waves of the cross-batch schedules (LP_WAVES overrides)
     bool margin_skip = true;  // frontier margin test (LP_MARGIN=0 disables)
     bool debug_rounds = false;  // LP_DEBUG_ROUNDS=1: per-round route sizes on stderr
+    double dense_frac = 0.35;   // a round that changed >= this share of the active rows is followed by a
+                                // full round instead of marks + frontier (LP_DENSE_FRAC; >= 1 disables)
     bool labels_valid = false;
     std::vector<cudaEvent_t> event_pool;
 };
@@ -644,12 +646,8 @@ template <int WM, int TIE> struct Launcher {
                 <<<grid, kHubThreads, team_smem_bytes<WM, kHubBits>(), st>>>(a, kLenHub);
             prof->end(st);
         }
-        // deferred marks of the rows that changed this round
-        if (a.mark) {
-            prof->begin(st, -1);
-            k_mark_pieces<<<sms * 16, 256, 0, st>>>(a);
-            prof->end(st);
-        }
+        // (the deferred marks of the rows that changed this round are launched
+        // by the sweep driver: mark_pass)
     }
 };
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_warp[2] = {1, 1};
@@ -1062,6 +1060,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_WAVES")) g->waves = std::max(1, std::min(1024, atoi(ev)));
     if (const char* ev = getenv("LP_MARGIN")) g->margin_skip = atoi(ev) != 0;
     if (const char* ev = getenv("LP_DEBUG_ROUNDS")) g->debug_rounds = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_DENSE_FRAC")) g->dense_frac = atof(ev);
     g->n = n;
     g->m = m;
 #define G_CK(call)                                                                                      \
@@ -1204,10 +1203,35 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
     a.horizon = INT32_MAX;
     LP_CK(cudaMemsetAsync(g->mq_len, 0, 2 * sizeof(int32_t), st));
     const int W = cross ? g->waves : 1;
+    auto mark_pass = [&]() {
+        prof->begin(st, -1);
+        k_mark_pieces<<<g->num_sms * 16, 256, 0, st>>>(a);
+        prof->end(st);
+    };
+    // writes of the round just run (label changes); one sync
+    auto round_writes = [&](int64_t* w) -> int {
+        LP_CK(cudaMemcpyAsync(g->h_counters + kCtrWrites, g->counters + kCtrWrites, sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, st));
+        LP_CK(cudaStreamSynchronize(st));
+        *w = (int64_t)g->h_counters[kCtrWrites];
+        return LP_OK;
+    };
+    const int64_t dense_at = (int64_t)(g->dense_frac * (double)P.S);
+    bool dense_next = false;
     if (W <= 1) {
+        LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
         run_round(g, a, true, g->h_len, prof, alg);
         if (alg == kGatherRak) *gathered += P.m_active;  // (piece gathers count themselves)
         ++*rounds;
+        if (cross) {
+            int64_t w = 0;
+            if (g->dense_frac < 1.0) {
+                if (int rc = round_writes(&w)) return rc;
+            }
+            if (w == 0 && g->dense_frac < 1.0) return LP_OK;  // nothing changed: the sweep is solved
+            dense_next = g->dense_frac < 1.0 && w >= dense_at;
+            if (!dense_next) mark_pass();
+        }
     } else {
         // Dense waves: the visit order in W consecutive position ranges, each
         // routed and evaluated after the previous one, so a wave reads the
@@ -1223,12 +1247,34 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
             LP_CK(cudaMemcpyAsync(g->h_len, g->routes.len, kLenCount * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
             LP_CK(cudaStreamSynchronize(st));
             a.horizon = (int32_t)std::min<int64_t>(g->n, (w + 1) * ws);
-            if (g->h_len[kLenGather] > 0) run_round(g, a, false, g->h_len, prof, alg);
+            if (g->h_len[kLenGather] > 0) {
+                run_round(g, a, false, g->h_len, prof, alg);
+                if (a.mark) mark_pass();
+            }
             ++*rounds;
         }
         a.horizon = INT32_MAX;
     }
     while (cross) {
+        if (dense_next) {
+            // most labels moved last round: re-evaluate every vertex (a full
+            // round costs less than marking and routing nearly all of them);
+            // vertices whose inputs did not change recompute the same label
+            LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
+            LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
+            a.mq_out = g->mq[q];
+            a.mq_len = g->mq_len + q;
+            LP_CK(cudaMemsetAsync(g->mq_len + q, 0, sizeof(int32_t), st));
+            run_round(g, a, true, g->h_len, prof, alg);  // (refreshes every margin)
+            if (alg == kGatherRak) *gathered += P.m_active;
+            ++*rounds;
+            int64_t w = 0;
+            if (int rc = round_writes(&w)) return rc;
+            if (w == 0) break;
+            dense_next = w >= dense_at;
+            if (!dense_next) mark_pass();
+            continue;
+        }
         // route last round's queue; this round's writes queue into the other one
         LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
         LP_CK(cudaMemsetAsync(g->mq_len + (q ^ 1), 0, sizeof(int32_t), st));
@@ -1251,6 +1297,15 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
         run_round(g, a, false, g->h_len, prof, alg);
         ++*rounds;
+        if (g->dense_frac < 1.0) {
+            int64_t w = 0;
+            if (int rc = round_writes(&w)) return rc;
+            if (w == 0) break;
+            dense_next = w >= dense_at;
+            if (!dense_next) mark_pass();
+        } else {
+            mark_pass();
+        }
     }
     return LP_OK;
 }
