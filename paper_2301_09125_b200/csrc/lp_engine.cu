@@ -200,6 +200,8 @@ struct lp_graph {
     int waves = 1;  // dense waves of the cross-batch schedules (LP_WAVES overrides)
     bool margin_skip = true;  // frontier margin test (LP_MARGIN=0 disables)
     bool debug_rounds = false;  // LP_DEBUG_ROUNDS=1: per-round route sizes on stderr
+    bool rows_sorted = false;  // every row strictly increasing (duplicate-free), checked at upload
+    bool first_round_shortcut = true;  // LP_FIRST_ROUND=0 disables k_first_round
     double dense_frac = 0.35;   // a round that changed >= this share of the active rows is followed by a
                                 // full round instead of marks + frontier (LP_DENSE_FRAC; >= 1 disables)
     bool labels_valid = false;
@@ -212,6 +214,17 @@ struct lp_graph {
 __global__ void k_i64_to_u32(const int64_t* __restrict__ in, uint32_t* __restrict__ out, int64_t count) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = (uint32_t)in[i];
+}
+
+// bad[0] counts arcs not strictly above their predecessor in the row
+__global__ void k_rows_sorted(const uint32_t* __restrict__ off, const int32_t* __restrict__ nbr, int64_t n,
+                              unsigned long long* bad) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
+    unsigned long long b = 0;
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; v < n; v += warps)
+        for (uint32_t e = off[v] + 1 + lane; e < off[v + 1]; e += 32) b += nbr[e] <= nbr[e - 1];
+    if (b) atomicAdd(bad, b);
 }
 
 // bad[0] counts decreasing offsets
@@ -1061,6 +1074,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_MARGIN")) g->margin_skip = atoi(ev) != 0;
     if (const char* ev = getenv("LP_DEBUG_ROUNDS")) g->debug_rounds = atoi(ev) != 0;
     if (const char* ev = getenv("LP_DENSE_FRAC")) g->dense_frac = atof(ev);
+    if (const char* ev = getenv("LP_FIRST_ROUND")) g->first_round_shortcut = atoi(ev) != 0;
     g->n = n;
     g->m = m;
 #define G_CK(call)                                                                                      \
@@ -1110,6 +1124,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
             k_weight_scan<<<g->num_sms * 8, 256, 0, st>>>((const double*)tmp, m, g->counters + 4);
         }
         k_degree_stats<<<g->num_sms * 8, 256, 0, st>>>(g->off, n, g->counters + 8);
+        k_rows_sorted<<<g->num_sms * 16, 256, 0, st>>>(g->off, g->nbr, n, g->counters + 12);
         G_CK(cudaMemcpyAsync(g->h_counters, g->counters, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         G_CK(cudaStreamSynchronize(st));
         if (g->h_counters[11]) {
@@ -1121,6 +1136,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
             return fail(lp_fail(LP_ERR_INVALID, "neighbor ids must lie in [0, vertex_count)"));
         }
         g->max_degree = (int64_t)g->h_counters[8];
+        g->rows_sorted = g->h_counters[12] == 0;
         g->sliceable = (int64_t)g->h_counters[9];
         g->slice_slots = (int64_t)g->h_counters[10];
         g->wmode = kUnit;
@@ -1193,7 +1209,7 @@ static int ensure_waves(lp_graph* g, int W) {
 // active row, then frontier rounds over the mark queue until a round marks
 // nothing.  One host sync per frontier round (route sizes).
 static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round, int alg, Prof* prof, int* rounds,
-                       int64_t* gathered) {
+                       int64_t* gathered, bool first_ids = false) {
     const Plan& P = g->plan();
     cudaStream_t st = g->stream;
     LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
@@ -1220,8 +1236,16 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
     bool dense_next = false;
     if (W <= 1) {
         LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
-        run_round(g, a, true, g->h_len, prof, alg);
-        if (alg == kGatherRak) *gathered += P.m_active;  // (piece gathers count themselves)
+        if (first_ids) {
+            // labels are still the vertex ids: the round is one neighbour read per row
+            a.bin = kKSmall;
+            prof->begin(st, kKSmall);
+            k_first_round<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S);
+            prof->end(st);
+        } else {
+            run_round(g, a, true, g->h_len, prof, alg);
+            if (alg == kGatherRak) *gathered += P.m_active;  // (piece gathers count themselves)
+        }
         ++*rounds;
         if (cross) {
             int64_t w = 0;
@@ -1432,7 +1456,11 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         a.x = X;
         LP_CK(cudaMemcpyAsync(X, L0, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
         LP_CK(cudaMemsetAsync(g->counters + kCtrChanged, 0, 2 * sizeof(unsigned long long), st));
-        if (int rc = solve_sweep(g, a, cross, run_round, kGatherRak, &prof, &rounds, &gathered)) return rc;
+        // first sweep from labels = ids: the dense round is trivial for unit
+        // weights and scan-first / min-label ties on duplicate-free sorted rows
+        const bool first_ids = it == 1 && !labels_init && g->wmode == kUnit && g->rows_sorted &&
+                               (o->tie == kScanFirst || o->tie == kMinLabel) && g->first_round_shortcut;
+        if (int rc = solve_sweep(g, a, cross, run_round, kGatherRak, &prof, &rounds, &gathered, first_ids)) return rc;
         LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, kCtrCount * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                               st));
         LP_CK(cudaStreamSynchronize(st));

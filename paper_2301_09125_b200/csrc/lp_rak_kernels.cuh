@@ -159,6 +159,9 @@ constexpr int32_t kMajBit = 1 << 30;
 __host__ __device__ __forceinline__ int32_t nd_count(int32_t v) { return v & (kMajBit - 1); }
 
 constexpr int kSmallMax = 16;     // thread-per-vertex bound (degree)
+#ifndef LP_WARP_REG_EST
+#define LP_WARP_REG_EST 32  // rows estimated to hold more labels skip the warp register table
+#endif
 // warp classes: 0 = 512-slot table (est <= 256, d <= 2048, 8 warps/block),
 // 1 = 1024-slot table (est <= 512, d <= 8192, 8 warps/block)
 template <int WC> struct WarpClass;
@@ -655,6 +658,35 @@ __global__ void k_route_queue(EvalArgs a, const int32_t* __restrict__ mq_in, con
             a.r.gk0[b0 + incl - np + q] = q * kPieceArcs;
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// first dense round of a run that starts from labels = vertex ids
+// ---------------------------------------------------------------------------
+// rak.py:168 starts every vertex with its own id.  In the first round of the
+// first sweep every read returns the initial label (nothing is written
+// before the round's gathers), so the labels of a row are its neighbour ids:
+// all distinct (rows are duplicate-free), each with count 1.  With unit
+// weights the argmax is then the first arc for scan-first ties and the
+// smallest neighbour id for min-label ties -- the same arc when rows are
+// sorted -- so the round needs no gather and no tally: one thread per row
+// reads one neighbour id.  Everything the tally kernels record is recorded
+// (label, changed count, distinct count, majority flag, margin, changed row).
+__global__ void __launch_bounds__(256) k_first_round(EvalArgs a, int32_t S) {
+    long long dchg = 0, arcs = 0, writes = 0, verts = 0;
+    for (int32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
+        const int32_t p = __ldg(a.svid + s);
+        const uint32_t beg = __ldg(a.soff + s);
+        const int d = (int)(__ldg(a.soff + s + 1) - beg);
+        const int32_t lab = (int32_t)(__ldg(a.snbr + beg) >> 2);
+        arcs += d;
+        ++verts;
+        a.ndist[s] = d | (2 > d ? kMajBit : 0);
+        store_gap<uint32_t>(a, s, 1u, (uint32_t)d);
+        const bool ch = commit_label_known(a, p, lab, p, p, dchg, writes);
+        if (a.mark) push_changed_small(a, ch, s);
+    }
+    flush_counters(a, dchg, arcs, writes, verts);
 }
 
 // ---------------------------------------------------------------------------
@@ -1188,7 +1220,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
             A tacc = A(0);
             uint32_t tfirst = 0;
             int K = 0;                  // register entries in use (warp-uniform)
-            bool hashed = est > 32;     // use the shared hash
+            bool hashed = est > LP_WARP_REG_EST;  // use the shared hash
             int ntouched = 0;
             bool overflow = false;
             for (int base = 0; base < d && !overflow; base += 32 * U) {
