@@ -202,6 +202,8 @@ struct lp_graph {
     bool debug_rounds = false;  // LP_DEBUG_ROUNDS=1: per-round route sizes on stderr
     bool rows_sorted = false;  // every row strictly increasing (duplicate-free), checked at upload
     bool first_round_shortcut = true;  // LP_FIRST_ROUND=0 disables k_first_round
+    bool sweep_frontier = true;        // active frontier across sweeps (LP_SWEEP_FRONTIER=0 disables)
+    double carry_frac = 0.1;           // ... after sweeps that changed <= this share of the rows (LP_CARRY_FRAC)
     double dense_frac = 0.35;   // a round that changed >= this share of the active rows is followed by a
                                 // full round instead of marks + frontier (LP_DENSE_FRAC; >= 1 disables)
     bool labels_valid = false;
@@ -1075,6 +1077,8 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_DEBUG_ROUNDS")) g->debug_rounds = atoi(ev) != 0;
     if (const char* ev = getenv("LP_DENSE_FRAC")) g->dense_frac = atof(ev);
     if (const char* ev = getenv("LP_FIRST_ROUND")) g->first_round_shortcut = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_SWEEP_FRONTIER")) g->sweep_frontier = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_CARRY_FRAC")) g->carry_frac = atof(ev);
     g->n = n;
     g->m = m;
 #define G_CK(call)                                                                                      \
@@ -1209,16 +1213,18 @@ static int ensure_waves(lp_graph* g, int W) {
 // active row, then frontier rounds over the mark queue until a round marks
 // nothing.  One host sync per frontier round (route sizes).
 static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round, int alg, Prof* prof, int* rounds,
-                       int64_t* gathered, bool first_ids = false) {
+                       int64_t* gathered, bool first_ids = false, bool carry = false) {
     const Plan& P = g->plan();
     cudaStream_t st = g->stream;
     LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
-    int q = 0;  // this round's writes queue into mq[q]
+    int q = 0;  // the queue routed next / this round's writes queue into mq[q]
     a.mq_out = g->mq[q];
     a.mq_len = g->mq_len + q;
     a.horizon = INT32_MAX;
-    LP_CK(cudaMemsetAsync(g->mq_len, 0, 2 * sizeof(int32_t), st));
-    const int W = cross ? g->waves : 1;
+    a.mark_all = 0;
+    // carry: mq[0] already holds the vertices whose inputs changed since their
+    // last evaluation (built at the sweep boundary); keep it
+    LP_CK(cudaMemsetAsync(g->mq_len + (carry ? 1 : 0), 0, (carry ? 1 : 2) * sizeof(int32_t), st));
     auto mark_pass = [&]() {
         prof->begin(st, -1);
         k_mark_pieces<<<g->num_sms * 16, 256, 0, st>>>(a);
@@ -1233,30 +1239,24 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         return LP_OK;
     };
     const int64_t dense_at = (int64_t)(g->dense_frac * (double)P.S);
-    bool dense_next = false;
-    if (W <= 1) {
-        LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
-        if (first_ids) {
-            // labels are still the vertex ids: the round is one neighbour read per row
-            a.bin = kKSmall;
-            prof->begin(st, kKSmall);
-            k_first_round<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S);
-            prof->end(st);
+    enum { kNextDense, kNextFirst, kNextQueue };
+    int next = first_ids ? kNextFirst : kNextDense;
+    if (carry) {
+        int32_t ql = 0;
+        LP_CK(cudaMemcpyAsync(g->h_len, g->mq_len, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        LP_CK(cudaStreamSynchronize(st));
+        ql = g->h_len[0];
+        if (ql == 0) return LP_OK;  // no vertex saw a neighbour change: the sweep changes nothing
+        if (ql >= dense_at) {
+            // most vertices are queued: one full round is cheaper; drop their marks
+            k_clear_marks<<<g->num_sms * 4, 256, 0, st>>>(g->mq[0], g->mq_len, g->mark);
+            next = kNextDense;
         } else {
-            run_round(g, a, true, g->h_len, prof, alg);
-            if (alg == kGatherRak) *gathered += P.m_active;  // (piece gathers count themselves)
+            next = kNextQueue;
         }
-        ++*rounds;
-        if (cross) {
-            int64_t w = 0;
-            if (g->dense_frac < 1.0) {
-                if (int rc = round_writes(&w)) return rc;
-            }
-            if (w == 0 && g->dense_frac < 1.0) return LP_OK;  // nothing changed: the sweep is solved
-            dense_next = g->dense_frac < 1.0 && w >= dense_at;
-            if (!dense_next) mark_pass();
-        }
-    } else {
+    }
+    const int W = (cross && !carry && !first_ids) ? g->waves : 1;
+    if (W > 1) {
         // Dense waves: the visit order in W consecutive position ranges, each
         // routed and evaluated after the previous one, so a wave reads the
         // current-sweep labels of all earlier waves; a changed label marks only
@@ -1278,57 +1278,60 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
             ++*rounds;
         }
         a.horizon = INT32_MAX;
+        next = kNextQueue;
     }
-    while (cross) {
-        if (dense_next) {
-            // most labels moved last round: re-evaluate every vertex (a full
-            // round costs less than marking and routing nearly all of them);
-            // vertices whose inputs did not change recompute the same label
+    while (true) {
+        if (next == kNextQueue) {
+            // route the queue (margin test); this round's writes queue into the other one
+            LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
+            LP_CK(cudaMemsetAsync(g->mq_len + (q ^ 1), 0, sizeof(int32_t), st));
+            prof->begin(st, -1);
+            k_route_queue<<<g->num_sms * 4, 256, 0, st>>>(a, g->mq[q], g->mq_len + q, P.slot_of, 1);
+            prof->end(st);
+            LP_CK(cudaMemcpyAsync(g->h_len, g->routes.len, kLenCount * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            LP_CK(cudaStreamSynchronize(st));
+            if (g->debug_rounds) {
+                int32_t ql = 0;
+                cudaMemcpy(&ql, g->mq_len + q, sizeof(int32_t), cudaMemcpyDeviceToHost);
+                fprintf(stderr, "[lp] round %d: queue %d small %d/%d/%d warp %d warpbig %d team %d team2 %d hub-items %d pieces %d\n",
+                        *rounds, ql, g->h_len[kLenS16], g->h_len[kLenS16 - 1], g->h_len[kLenS16 - 2],
+                        g->h_len[kLenWarp], g->h_len[kLenWarpBig], g->h_len[kLenTeam], g->h_len[kLenTeam2],
+                        g->h_len[kLenHub], g->h_len[kLenGather]);
+            }
+            if (g->h_len[kLenGather] == 0) break;  // everything queued passed the margin test
+            q ^= 1;
+            a.mq_out = g->mq[q];
+            a.mq_len = g->mq_len + q;
+            LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
+            run_round(g, a, false, g->h_len, prof, alg);
+        } else {
+            // every active row (dense), or the trivial first round from labels = ids
             LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
             LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
             a.mq_out = g->mq[q];
             a.mq_len = g->mq_len + q;
             LP_CK(cudaMemsetAsync(g->mq_len + q, 0, sizeof(int32_t), st));
-            run_round(g, a, true, g->h_len, prof, alg);  // (refreshes every margin)
-            if (alg == kGatherRak) *gathered += P.m_active;
-            ++*rounds;
-            int64_t w = 0;
-            if (int rc = round_writes(&w)) return rc;
-            if (w == 0) break;
-            dense_next = w >= dense_at;
-            if (!dense_next) mark_pass();
-            continue;
+            if (next == kNextFirst) {
+                a.bin = kKSmall;
+                prof->begin(st, kKSmall);
+                k_first_round<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S);
+                prof->end(st);
+            } else {
+                run_round(g, a, true, g->h_len, prof, alg);  // (refreshes every margin)
+                if (alg == kGatherRak) *gathered += P.m_active;  // (piece gathers count themselves)
+            }
         }
-        // route last round's queue; this round's writes queue into the other one
-        LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
-        LP_CK(cudaMemsetAsync(g->mq_len + (q ^ 1), 0, sizeof(int32_t), st));
-        prof->begin(st, -1);
-        k_route_queue<<<g->num_sms * 4, 256, 0, st>>>(a, g->mq[q], g->mq_len + q, P.slot_of, 1);
-        prof->end(st);
-        LP_CK(cudaMemcpyAsync(g->h_len, g->routes.len, kLenCount * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        LP_CK(cudaStreamSynchronize(st));
-        if (g->debug_rounds) {
-            int32_t ql = 0;
-            cudaMemcpy(&ql, g->mq_len + q, sizeof(int32_t), cudaMemcpyDeviceToHost);
-            fprintf(stderr, "[lp] round %d: queue %d small %d/%d/%d warp %d warpbig %d team %d team2 %d hub-items %d pieces %d\n",
-                    *rounds, ql, g->h_len[kLenS16], g->h_len[kLenS16 - 1], g->h_len[kLenS16 - 2], g->h_len[kLenWarp],
-                    g->h_len[kLenWarpBig], g->h_len[kLenTeam], g->h_len[kLenTeam2], g->h_len[kLenHub], g->h_len[kLenGather]);
-        }
-        if (g->h_len[kLenGather] == 0) break;
-        q ^= 1;
-        a.mq_out = g->mq[q];
-        a.mq_len = g->mq_len + q;
-        LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
-        run_round(g, a, false, g->h_len, prof, alg);
         ++*rounds;
-        if (g->dense_frac < 1.0) {
-            int64_t w = 0;
-            if (int rc = round_writes(&w)) return rc;
-            if (w == 0) break;
-            dense_next = w >= dense_at;
-            if (!dense_next) mark_pass();
+        if (!cross) break;  // no cross-batch reads: one round solves the sweep
+        int64_t w = 0;
+        if (int rc = round_writes(&w)) return rc;
+        if (w == 0) break;  // nothing changed: every read is final
+        if (w >= dense_at) {
+            // most labels moved: a full round costs less than marking and routing them
+            next = kNextDense;
         } else {
             mark_pass();
+            next = kNextQueue;
         }
     }
     return LP_OK;
@@ -1429,8 +1432,15 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.swsum = P.swsum;
     a.svid = P.svid;
     a.lbuf = P.lbuf;
-    a.mark = cross ? g->mark : nullptr;
-    a.gap = (cross && g->wmode != kFloat && g->margin_skip) ? g->gap : nullptr;
+    // marks: cross-batch dependencies inside a sweep, and (track) the active
+    // frontier across sweeps: a sweep re-evaluates only vertices with a
+    // neighbour that changed since their last evaluation
+    // (not with random ties: tie_hash is keyed by the sweep, so an unchanged
+    // neighbourhood can still produce a different winner)
+    const bool track = g->sweep_frontier && o->tie != kRandom;
+    a.mark = (cross || track) ? g->mark : nullptr;
+    a.gap = ((cross || track) && g->wmode != kFloat && g->margin_skip) ? g->gap : nullptr;
+    a.mark_all = 0;
     a.pos = P.pos;
     a.horizon = INT32_MAX;
     a.mq_out = nullptr;
@@ -1449,24 +1459,45 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     int it = 0;
     int rounds = 0;
     int64_t gathered = 0;
+    int64_t last_changed = n;
     while (it < o->max_iterations) {
         ++it;
         a.sweep = (uint32_t)it;
         a.L0 = L0;
         a.x = X;
+        // (only after a sweep that changed few labels: marking the neighbours of
+        // many changed rows costs more than one full round)
+        const bool carry = track && it > 1 && last_changed <= (int64_t)(g->carry_frac * (double)P.S);
+        if (carry) {
+            // sweep boundary: every neighbour of a vertex whose label changed in the
+            // last sweep is queued (with the changed weight, for the margin test);
+            // only queued vertices can change in this sweep's first round
+            LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
+            LP_CK(cudaMemsetAsync(g->mq_len, 0, sizeof(int32_t), st));
+            k_sweep_changes<<<g->num_sms * 8, 256, 0, st>>>(a, L0, X, (int32_t)P.S);  // L0 = last result, X = older
+            a.mq_out = g->mq[0];
+            a.mq_len = g->mq_len;
+            a.mark_all = 1;
+            prof.begin(st, -1);
+            k_mark_pieces<<<g->num_sms * 16, 256, 0, st>>>(a);
+            prof.end(st);
+            a.mark_all = 0;
+        }
         LP_CK(cudaMemcpyAsync(X, L0, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
         LP_CK(cudaMemsetAsync(g->counters + kCtrChanged, 0, 2 * sizeof(unsigned long long), st));
         // first sweep from labels = ids: the dense round is trivial for unit
         // weights and scan-first / min-label ties on duplicate-free sorted rows
         const bool first_ids = it == 1 && !labels_init && g->wmode == kUnit && g->rows_sorted &&
                                (o->tie == kScanFirst || o->tie == kMinLabel) && g->first_round_shortcut;
-        if (int rc = solve_sweep(g, a, cross, run_round, kGatherRak, &prof, &rounds, &gathered, first_ids)) return rc;
+        if (int rc = solve_sweep(g, a, cross, run_round, kGatherRak, &prof, &rounds, &gathered, first_ids, carry))
+            return rc;
         LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, kCtrCount * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                               st));
         LP_CK(cudaStreamSynchronize(st));
         LP_CK(cudaGetLastError());
         const int64_t changed = (int64_t)g->h_counters[kCtrChanged];
         if (changed_per_iter) changed_per_iter[it - 1] = changed;
+        last_changed = changed;
         std::swap(L0, X);  // L0 now holds this sweep's labels
         if ((double)changed <= o->tolerance * (double)n) break;  // rak.py:114-115
     }

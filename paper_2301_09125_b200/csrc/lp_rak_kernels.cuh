@@ -123,6 +123,7 @@ struct EvalArgs {
     unsigned long long* gap;            // per slot: lower bound of (winner - runner-up) weight at the
                                         // last evaluation (0 = unknown); null = no margin skipping
     const int32_t* __restrict__ pos;    // vertex -> visit position (wave horizon test)
+    int32_t mark_all;                   // mark every neighbour (sweep boundary), not only later-batch ones
     int32_t horizon;                    // dense waves: only positions < horizon have been evaluated
                                         // this sweep and need marks; INT32_MAX = all
     int32_t* mq_out;                    // queue of newly marked vertices (this round's writes)
@@ -452,6 +453,24 @@ __device__ __forceinline__ void push_changed_batch(const EvalArgs& a, uint32_t c
     }
 }
 
+// Sweep boundary: the rows whose label differs between two label arrays
+// (this sweep's result vs the previous one) join the changed list, so that
+// k_mark_pieces (mark_all) can queue every neighbour for the next sweep.
+__global__ void k_sweep_changes(EvalArgs a, const int32_t* __restrict__ lnew, const int32_t* __restrict__ lold,
+                                int32_t S) {
+    for (int32_t base = blockIdx.x * blockDim.x; base < S; base += gridDim.x * blockDim.x) {
+        const int32_t s = base + threadIdx.x;
+        bool ch = false;
+        int d = 0;
+        if (s < S) {
+            const int32_t v = __ldg(a.svid + s);
+            ch = lnew[v] != lold[v];
+            d = (int)(__ldg(a.soff + s + 1) - __ldg(a.soff + s));
+        }
+        push_changed_batch(a, __ballot_sync(0xffffffffu, ch), s, d);
+    }
+}
+
 // Mark the later-batch neighbours of every changed row (see mark_row); warp
 // batches of 32 pieces, flattened, eight arcs in flight per lane.
 __global__ void __launch_bounds__(256) k_mark_pieces(EvalArgs a) {
@@ -499,7 +518,7 @@ __global__ void __launch_bounds__(256) k_mark_pieces(EvalArgs a) {
 #pragma unroll
             for (int j = 0; j < J; ++j) {
                 const int32_t u = (int32_t)(nb[j] >> 2);
-                win[j] = e[j] != 0xffffffffu && (nb[j] & kLater) && needs_mark(a, u) &&
+                win[j] = e[j] != 0xffffffffu && (a.mark_all || (nb[j] & kLater)) && needs_mark(a, u) &&
                          atomicAdd(a.mark + u, mark_weight(a, e[j])) == 0ull;
             }
 #pragma unroll
