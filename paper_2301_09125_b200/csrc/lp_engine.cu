@@ -161,6 +161,7 @@ struct lp_graph {
     int32_t* cur = nullptr;  // the buffer holding the latest labels
     unsigned long long* mark = nullptr;  // frontier marks by vertex id (changed weight since routing)
     unsigned long long* gap = nullptr;   // per slot: winner margin lower bound at the last evaluation
+    uint8_t* chg = nullptr;              // sweep boundary: label changed in the last sweep
     int32_t* mq[2] = {nullptr, nullptr};  // mark queues (alternate per round)
     int32_t* mq_len = nullptr;  // their lengths [2]
     int32_t* slots = nullptr;   // SLPA memories [n x T]
@@ -203,7 +204,7 @@ struct lp_graph {
     bool rows_sorted = false;  // every row strictly increasing (duplicate-free), checked at upload
     bool first_round_shortcut = true;  // LP_FIRST_ROUND=0 disables k_first_round
     bool sweep_frontier = true;        // active frontier across sweeps (LP_SWEEP_FRONTIER=0 disables)
-    double carry_frac = 0.1;           // ... after sweeps that changed <= this share of the rows (LP_CARRY_FRAC)
+    double carry_frac = 0.5;           // ... after sweeps that changed <= this share of the rows (LP_CARRY_FRAC)
     double dense_frac = 0.35;   // a round that changed >= this share of the active rows is followed by a
                                 // full round instead of marks + frontier (LP_DENSE_FRAC; >= 1 disables)
     bool labels_valid = false;
@@ -769,6 +770,7 @@ static void destroy_graph(lp_graph* g) {
     dfree(g->labB);
     dfree(g->mark);
     dfree(g->gap);
+    dfree(g->chg);
     dfree(g->counters);
     dfree(g->out64);
     dfree(g->cub_tmp);
@@ -958,8 +960,9 @@ static int build_plan(lp_graph* g, int kind, const int64_t* order_host, uint32_t
     if (g->w) LP_CK(dalloc(&P.sw, P.m_active, &bytes));
     k_plan_rows<<<g->num_sms * 16, 256, 0, st>>>(P.svid, g->off, g->nbr, g->w, P.soff, P.snbr, P.sw, P.S,
                                                  index ? 1 : 0);
-    if (index) {
-        // dense piece list (reuses t.sdeg as the per-slot piece counts / offsets)
+    {
+        // dense piece list (reuses t.sdeg as the per-slot piece counts / offsets):
+        // SLPA's dense gathers, the pull marks at sweep boundaries
         k_plan_piece_counts<<<G, 256, 0, st>>>(P.soff, t.sdeg, P.S);
         LP_CK(cub::DeviceScan::ExclusiveSum(g->cub_tmp, need2, t.sdeg, t.sdeg, (int)(P.S + 1), st));
         uint32_t np = 0;
@@ -1100,6 +1103,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     G_CK(dalloc(&g->labB, n, &g->bytes));
     G_CK(dalloc(&g->mark, n + 4, &g->bytes));
     G_CK(dalloc(&g->gap, n + 4, &g->bytes));
+    G_CK(dalloc(&g->chg, n + 4, &g->bytes));
     G_CK(dalloc(&g->mq[0], n + 4, &g->bytes));
     G_CK(dalloc(&g->mq[1], n + 4, &g->bytes));
     G_CK(dalloc(&g->mq_len, 4, &g->bytes));
@@ -1246,14 +1250,9 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         LP_CK(cudaMemcpyAsync(g->h_len, g->mq_len, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         LP_CK(cudaStreamSynchronize(st));
         ql = g->h_len[0];
+        if (g->debug_rounds) fprintf(stderr, "[lp] sweep start: carried queue %d (dense at %lld)\n", ql, (long long)dense_at);
         if (ql == 0) return LP_OK;  // no vertex saw a neighbour change: the sweep changes nothing
-        if (ql >= dense_at) {
-            // most vertices are queued: one full round is cheaper; drop their marks
-            k_clear_marks<<<g->num_sms * 4, 256, 0, st>>>(g->mq[0], g->mq_len, g->mark);
-            next = kNextDense;
-        } else {
-            next = kNextQueue;
-        }
+        next = kNextQueue;  // (the margin test filters the queue; see the switch below)
     }
     const int W = (cross && !carry && !first_ids) ? g->waves : 1;
     if (W > 1) {
@@ -1303,7 +1302,16 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
             a.mq_out = g->mq[q];
             a.mq_len = g->mq_len + q;
             LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
-            run_round(g, a, false, g->h_len, prof, alg);
+            if ((double)g->h_len[kLenGather] >= g->dense_frac * (double)P.npieces) {
+                // most rows survived the margin test: a full round is cheaper than the
+                // routed frontier (the routes are dropped; every margin is refreshed)
+                LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
+                LP_CK(cudaMemsetAsync(g->mq_len + q, 0, sizeof(int32_t), st));
+                run_round(g, a, true, g->h_len, prof, alg);
+                if (alg == kGatherRak) *gathered += P.m_active;
+            } else {
+                run_round(g, a, false, g->h_len, prof, alg);
+            }
         } else {
             // every active row (dense), or the trivial first round from labels = ids
             LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
@@ -1474,14 +1482,23 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
             // only queued vertices can change in this sweep's first round
             LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
             LP_CK(cudaMemsetAsync(g->mq_len, 0, sizeof(int32_t), st));
-            k_sweep_changes<<<g->num_sms * 8, 256, 0, st>>>(a, L0, X, (int32_t)P.S);  // L0 = last result, X = older
             a.mq_out = g->mq[0];
             a.mq_len = g->mq_len;
-            a.mark_all = 1;
             prof.begin(st, -1);
-            k_mark_pieces<<<g->num_sms * 16, 256, 0, st>>>(a);
+            if (last_changed * 50 <= P.S) {
+                // few changed rows: push from them (one atomic per neighbour)
+                k_sweep_changes<<<g->num_sms * 8, 256, 0, st>>>(a, L0, X, (int32_t)P.S);  // L0 = last result
+                a.mark_all = 1;
+                k_mark_pieces<<<g->num_sms * 16, 256, 0, st>>>(a);
+                a.mark_all = 0;
+            } else {
+                // many: every row pulls the changed flags of its neighbours (one flat
+                // pass, one atomic per row piece with a changed neighbour)
+                k_changed_flags<<<g->num_sms * 8, 256, 0, st>>>(L0, X, g->chg, n);
+                k_pull_marks<<<g->num_sms * 16, 256, 0, st>>>(a, g->chg, P.dslot, P.dk0, P.dcount,
+                                                             g->routes.len + kGatherCursor);
+            }
             prof.end(st);
-            a.mark_all = 0;
         }
         LP_CK(cudaMemcpyAsync(X, L0, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
         LP_CK(cudaMemsetAsync(g->counters + kCtrChanged, 0, 2 * sizeof(unsigned long long), st));

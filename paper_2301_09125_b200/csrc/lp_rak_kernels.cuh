@@ -231,6 +231,17 @@ template <typename A> __device__ __forceinline__ void store_gap(const EvalArgs& 
     }
 }
 
+// Record the exact lead of the winner (largest label weight w1) over the
+// runner-up (w2).
+template <typename A> __device__ __forceinline__ void store_lead(const EvalArgs& a, int32_t s, A w1, A w2) {
+    if (a.gap) {
+        if constexpr (std::is_same<A, float>::value)
+            a.gap[s] = 0ull;
+        else
+            a.gap[s] = (unsigned long long)(w1 - w2);
+    }
+}
+
 // Write a vertex's new label (one thread).  Returns true when it changed.
 __device__ __forceinline__ bool commit_label(const EvalArgs& a, int32_t v, int32_t lab, long long& dchg,
                                              long long& writes) {
@@ -468,6 +479,89 @@ __global__ void k_sweep_changes(EvalArgs a, const int32_t* __restrict__ lnew, co
             d = (int)(__ldg(a.soff + s + 1) - __ldg(a.soff + s));
         }
         push_changed_batch(a, __ballot_sync(0xffffffffu, ch), s, d);
+    }
+}
+
+__global__ void k_changed_flags(const int32_t* __restrict__ lnew, const int32_t* __restrict__ lold,
+                                uint8_t* __restrict__ chg, int64_t n) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        chg[v] = lnew[v] != lold[v];
+}
+
+// Sweep boundary, pull form: warps take 32 row pieces (the plan's dense
+// piece list), sum the weights of arcs whose neighbour changed (shared-memory
+// atomics per piece), and add each nonzero sum to the row's mark -- the first
+// mark queues the vertex, as in k_mark_pieces.
+__global__ void __launch_bounds__(256) k_pull_marks(EvalArgs a, const uint8_t* __restrict__ chg,
+                                                    const int32_t* __restrict__ dslot,
+                                                    const int32_t* __restrict__ dk0,
+                                                    const int32_t* __restrict__ dcount, int32_t* cursor) {
+    constexpr int J = 8;
+    __shared__ unsigned long long sums[8][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int cnt = *dcount;
+    while (true) {
+        int b0 = 0;
+        if (lane == 0) b0 = atomicAdd(cursor, 32);
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (b0 >= cnt) break;
+        uint32_t pbeg = 0, plen = 0;
+        int32_t ps = -1;
+        if (b0 + lane < cnt) {
+            ps = dslot[b0 + lane];
+            const uint32_t rb = __ldg(a.soff + ps), re = __ldg(a.soff + ps + 1);
+            pbeg = rb + (uint32_t)dk0[b0 + lane];
+            plen = min((uint32_t)kPieceArcs, re - pbeg);
+        }
+        sums[wib][lane] = 0ull;
+        __syncwarp();
+        uint32_t incl = plen;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t excl = incl - plen;
+        for (uint32_t base = 0; base < total; base += 32 * J) {
+            uint32_t e[J];
+            int rr[J];
+            uint32_t nb[J];
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const uint32_t i = base + j * 32 + lane;
+                int r = 0;
+#pragma unroll
+                for (int step = 16; step >= 1; step >>= 1) {
+                    const uint32_t ex = __shfl_sync(0xffffffffu, excl, r + step);
+                    if (r + step < 32 && ex <= i) r += step;
+                }
+                const uint32_t pb = __shfl_sync(0xffffffffu, pbeg, r);
+                const uint32_t pe = __shfl_sync(0xffffffffu, excl, r);
+                rr[j] = r;
+                e[j] = i < total ? pb + (i - pe) : 0xffffffffu;
+                nb[j] = i < total ? __ldg(a.snbr + e[j]) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < J; ++j)
+                if (e[j] != 0xffffffffu && __ldg(chg + (nb[j] >> 2))) atomicAdd(&sums[wib][rr[j]], mark_weight(a, e[j]));
+        }
+        __syncwarp();
+        const unsigned long long sm = sums[wib][lane];
+        bool win = false;
+        int32_t v = -1;
+        if (sm) {
+            v = __ldg(a.svid + ps);
+            win = atomicAdd(a.mark + v, sm) == 0ull;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, win);
+        if (bal) {
+            int q0 = 0;
+            if (lane == 0) q0 = atomicAdd(a.mq_len, __popc(bal));
+            q0 = __shfl_sync(0xffffffffu, q0, 0);
+            if (win) a.mq_out[q0 + __popc(bal & lanemask_lt())] = v;
+        }
+        __syncwarp();
     }
 }
 
@@ -760,6 +854,7 @@ __global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, i
         }
         const uint32_t vtx = (uint32_t)p;
         Cand<A> best = none_cand<A>();
+        A w1 = A(0), w2 = A(0);
 #pragma unroll
         for (int i2 = 0; i2 < MAXD; ++i2) {
             if (i2 < d) {
@@ -775,12 +870,19 @@ __global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, i
                 if (!dup) {
                     Cand<A> c = make_cand<TIE, A>(sum, lab[i2], (uint32_t)i2, a.seed, a.sweep, vtx);
                     if (better(c, best)) best = c;
+                    // the two largest label weights: the winner's exact lead
+                    if (sum > w1) {
+                        w2 = w1;
+                        w1 = sum;
+                    } else if (sum > w2) {
+                        w2 = sum;
+                    }
                 }
             }
         }
         const int32_t nd_new = (best.w + best.w > total) ? kMajBit : 0;
         if (nd_new != nd) a.ndist[s] = nd_new;
-        store_gap<A>(a, s, best.w, total);
+        store_lead<A>(a, s, w1, w2);
         const bool ch = commit_label_known(a, p, best.lab, xv, l0v, dchg, writes);
         if (a.mark) push_changed_small(a, ch, s);
     }
@@ -1340,6 +1442,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
             }
             int32_t winner;
             A wbest;
+            A wsecond = A(0);
             if (!hashed) {
                 Cand<A> best = none_cand<A>();
                 if (lane < K) best = make_cand<TIE, A>(tacc, tkey, tfirst, a.seed, a.sweep, vtx);
@@ -1355,6 +1458,14 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                 }
                 winner = __shfl_sync(0xffffffffu, best.lab, 0);
                 wbest = best.w;  // valid in lane 0
+                // runner-up weight (exact lead for the margin test)
+                A w2 = (lane < K && tkey != winner) ? tacc : A(0);
+#pragma unroll
+                for (int m = 16; m >= 1; m >>= 1) {
+                    const A o = shfl_xor_any(w2, m);
+                    w2 = o > w2 ? o : w2;
+                }
+                wsecond = w2;
             } else {
                 const Best<A> b = table_argmax<WM, TIE, kWarpBits, 1>(tab->t, tab->touched, ntouched, lane, a.seed,
                                                                      a.sweep, vtx, nullptr);
@@ -1386,7 +1497,10 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                 ++verts;
                 const bool maj = WM != kFloat && wbest + wbest > total;
                 a.ndist[s] = (hashed ? ntouched : K) | (maj ? kMajBit : 0);
-                store_gap<A>(a, s, wbest, total);
+                if (wsecond >= A(0) && !hashed)
+                    store_lead<A>(a, s, wbest, wsecond);
+                else
+                    store_gap<A>(a, s, wbest, total);
                 changed = commit_label_known(a, p, winner, xv, l0v, dchg, writes);
             }
             changed = __shfl_sync(0xffffffffu, changed, 0);
