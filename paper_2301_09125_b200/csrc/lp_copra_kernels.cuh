@@ -30,6 +30,20 @@
 
 namespace lp {
 
+#ifdef LP_DEBUG_BOUNDS
+#define LP_CHECK(cond, what)                                                                         \
+    do {                                                                                            \
+        if (!(cond)) {                                                                              \
+            printf("LP_CHECK failed: %s (block %d thread %d)\n", what, blockIdx.x, threadIdx.x);    \
+            __trap();                                                                               \
+        }                                                                                           \
+    } while (0)
+#else
+#define LP_CHECK(cond, what) \
+    do {                     \
+    } while (0)
+#endif
+
 constexpr int kCopraMaxLabels = 32;  // label-set bound on the GPU (one lane per kept label)
 constexpr int kCopraWarps = 8;       // warps per block, warp kernel
 constexpr int kCopraBits = 9;        // per-warp smem table: 512 slots
@@ -75,6 +89,8 @@ struct CopraArgs {
     int32_t* gblab;     // [gcap_contrib] per block: bucketed contributions
     double* gbval;
     int32_t* gbc;
+    int32_t* gslab;     // [gcap_contrib] per block: staged contributions (label, value)
+    double* gsval;
     int32_t* gwc;       // [W x kCopraMaxParts] per block: partition counts / offsets
     int32_t* gqs;       // [kCopraMaxParts + 1] per block: bucket starts
     size_t gcap_entries;
@@ -474,6 +490,8 @@ __global__ void __launch_bounds__(kCopraTeamWarps * 32, 2) k_copra_team(CopraArg
     int32_t* Blab = a.gblab + blockIdx.x * Cc;
     double* Bval = a.gbval + blockIdx.x * Cc;
     int32_t* Bc = a.gbc + blockIdx.x * Cc;
+    int32_t* Slab = a.gslab + blockIdx.x * Cc;
+    double* Sval = a.gsval + blockIdx.x * Cc;
     int32_t* Wc = a.gwc + blockIdx.x * (size_t)(W * kCopraMaxParts);  // [W][P] counts -> offsets
     int32_t* Qs = a.gqs + blockIdx.x * (size_t)(kCopraMaxParts + 1);  // bucket starts
     for (int i = lane; i < slots; i += 32) {
@@ -493,18 +511,31 @@ __global__ void __launch_bounds__(kCopraTeamWarps * 32, 2) k_copra_team(CopraArg
         const int est = nd_count(__ldg(a.ndist + s));
         int P = W;
         while (P < kCopraMaxParts && P * kCopraTeamLimit < est + (est >> 2)) P *= 2;
+        // (0) stage the warp's contributions once: earlier-batch label sets may
+        // change under a running round, and every later pass must see the same
+        // data (the region of arcs [k_lo, k_hi) holds at most (k_hi - k_lo) * K)
+        const int sbase = k_lo * a.K;
+        int mine = 0;
+        for_each_contribution(a, s, k_lo, k_hi, [&](int32_t lab, double val, int c, bool valid) {
+            if (valid) {
+                LP_CHECK((size_t)(sbase + c) < Cc, "stage index");
+                Slab[sbase + c] = lab;
+                Sval[sbase + c] = val;
+            }
+            mine += __popc(__ballot_sync(0xffffffffu, valid));
+        });
+        __syncwarp();
         while (true) {  // retry with more partitions on a table overflow
             // (1) per-warp partition counts
             for (int q = lane; q < P; q += 32) Wc[warp * P + q] = 0;
             __syncwarp();
-            int mine = 0;
-            for_each_contribution(a, s, k_lo, k_hi, [&](int32_t lab, double, int, bool valid) {
-                const uint32_t q = valid ? part_of(lab, (uint32_t)P) : 0xffffffffu;
+            for (int i0 = 0; i0 < mine; i0 += 32) {
+                const bool valid = i0 + lane < mine;
+                const uint32_t q = valid ? part_of(Slab[sbase + i0 + lane], (uint32_t)P) : 0xffffffffu;
                 const uint32_t grp = __match_any_sync(0xffffffffu, q);
                 if (valid && (__ffs(grp) - 1) == lane) Wc[warp * P + q] += __popc(grp);
-                mine += __popc(__ballot_sync(0xffffffffu, valid));
                 __syncwarp();
-            });
+            }
             if (lane == 0) ctl[16 + warp] = mine;
             if (tid == 0) {
                 ctl[1] = 0;
@@ -550,7 +581,15 @@ __global__ void __launch_bounds__(kCopraTeamWarps * 32, 2) k_copra_team(CopraArg
             __syncthreads();
             // (2) stable scatter into buckets
             const int cb = ctl[16 + warp];
-            for_each_contribution(a, s, k_lo, k_hi, [&](int32_t lab, double val, int c, bool valid) {
+            for (int i0 = 0; i0 < mine; i0 += 32) {
+                const int c = i0 + lane;
+                const bool valid = c < mine;
+                int32_t lab = kEmpty;
+                double val = 0.0;
+                if (valid) {
+                    lab = Slab[sbase + c];
+                    val = Sval[sbase + c];
+                }
                 const uint32_t q = valid ? part_of(lab, (uint32_t)P) : 0xffffffffu;
                 const uint32_t grp = __match_any_sync(0xffffffffu, q);
                 int pos = 0;
@@ -558,12 +597,13 @@ __global__ void __launch_bounds__(kCopraTeamWarps * 32, 2) k_copra_team(CopraArg
                 __syncwarp();
                 if (valid && (__ffs(grp) - 1) == lane) Wc[warp * P + q] += __popc(grp);
                 if (valid) {
+                    LP_CHECK(pos >= 0 && (size_t)pos < Cc, "bucket position");
                     Blab[pos] = lab;
                     Bval[pos] = val;
                     Bc[pos] = cb + c;
                 }
                 __syncwarp();
-            });
+            }
             __syncthreads();
             // (3) tally the buckets
             for (int q = warp; q < P; q += W) {
@@ -590,6 +630,7 @@ __global__ void __launch_bounds__(kCopraTeamWarps * 32, 2) k_copra_team(CopraArg
                 base = __shfl_sync(0xffffffffu, base, 0);
                 for (int i = lane; i < cnt; i += 32) {
                     const int sl = tl[i];
+                    LP_CHECK((size_t)(base + i) < D, "entry index");
                     Elab[base + i] = keys[sl];
                     Eval[base + i] = vals[sl];
                     Efirst[base + i] = firsts[sl];
@@ -608,7 +649,11 @@ __global__ void __launch_bounds__(kCopraTeamWarps * 32, 2) k_copra_team(CopraArg
         }
         // (4) first-touch order: F[first] = entry, then an ordered compaction of F
         const int nent = ctl[1], C = ctl[3];
-        for (int e = tid; e < nent; e += blockDim.x) F[Efirst[e]] = e;
+        LP_CHECK((size_t)C <= Cc, "contributions");
+        for (int e = tid; e < nent; e += blockDim.x) {
+            LP_CHECK(Efirst[e] >= 0 && Efirst[e] < C, "first index");
+            F[Efirst[e]] = e;
+        }
         __syncthreads();
         int run = 0;  // entries placed so far (block-uniform)
         for (int c0 = 0; c0 < C; c0 += blockDim.x) {
@@ -622,6 +667,7 @@ __global__ void __launch_bounds__(kCopraTeamWarps * 32, 2) k_copra_team(CopraArg
             for (int w = 0; w < warp; ++w) before += sms[w].outl[0];
             if (has) {
                 const int r = before + __popc(bal & lanemask_lt());
+                LP_CHECK((size_t)r < D && e < nent, "rank");
                 Rlab[r] = Elab[e];
                 Rval[r] = Eval[e];
                 F[c] = -1;

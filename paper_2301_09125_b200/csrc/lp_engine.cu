@@ -187,6 +187,8 @@ struct lp_graph {
     int32_t* gbc = nullptr;
     int32_t* gwc = nullptr;
     int32_t* gqs = nullptr;
+    int32_t* gslab = nullptr;
+    double* gsval = nullptr;
     size_t gent = 0, gcon = 0;
     int gblocks = 0;
     Routes routes;
@@ -763,6 +765,8 @@ static void destroy_graph(lp_graph* g) {
     dfree(g->gbc);
     dfree(g->gwc);
     dfree(g->gqs);
+    dfree(g->gslab);
+    dfree(g->gsval);
     dfree(g->off);
     dfree(g->nbr);
     dfree(g->w);
@@ -1728,12 +1732,14 @@ static int copra_buffers(lp_graph* g, int K) {
         dfree(g->gbc);
         dfree(g->gwc);
         dfree(g->gqs);
-        g->gelab = g->gefirst = g->grlab = g->gfmap = g->gblab = g->gbc = g->gwc = g->gqs = nullptr;
-        g->geval = g->grval = g->gbval = nullptr;
+        dfree(g->gslab);
+        dfree(g->gsval);
+        g->gelab = g->gefirst = g->grlab = g->gfmap = g->gblab = g->gbc = g->gwc = g->gqs = g->gslab = nullptr;
+        g->geval = g->grval = g->gbval = g->gsval = nullptr;
         g->gent = g->gcon = 0;
         const size_t parts = (size_t)kCopraTeamWarps * kCopraMaxParts + kCopraMaxParts + 1;
         const size_t per = ent * (3 * sizeof(int32_t) + 2 * sizeof(double)) +
-                           con * (3 * sizeof(int32_t) + sizeof(double)) + parts * sizeof(int32_t);
+                           con * (4 * sizeof(int32_t) + 2 * sizeof(double)) + parts * sizeof(int32_t);
         const int blocks = (int)std::max<size_t>(1, std::min<size_t>(2 * g->num_sms, ((size_t)6 << 30) / per));
         LP_CK(pool_alloc(&g->gelab, ent * blocks * sizeof(int32_t)));
         LP_CK(pool_alloc(&g->geval, ent * blocks * sizeof(double)));
@@ -1744,6 +1750,8 @@ static int copra_buffers(lp_graph* g, int K) {
         LP_CK(pool_alloc(&g->gblab, con * blocks * sizeof(int32_t)));
         LP_CK(pool_alloc(&g->gbval, con * blocks * sizeof(double)));
         LP_CK(pool_alloc(&g->gbc, con * blocks * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->gslab, con * blocks * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->gsval, con * blocks * sizeof(double)));
         LP_CK(pool_alloc(&g->gwc, (size_t)kCopraTeamWarps * kCopraMaxParts * blocks * sizeof(int32_t)));
         LP_CK(pool_alloc(&g->gqs, (size_t)(kCopraMaxParts + 1) * blocks * sizeof(int32_t)));
         k_fill_i32<<<g->num_sms * 8, 256, 0, g->stream>>>(g->gfmap, -1, (int64_t)(con * blocks));
@@ -1838,6 +1846,8 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
     a.gbval = g->gbval;
     a.gbc = g->gbc;
     a.gwc = g->gwc;
+    a.gslab = g->gslab;
+    a.gsval = g->gsval;
     a.gqs = g->gqs;
     a.gcap_entries = g->gent;
     a.gcap_contrib = g->gcon;
