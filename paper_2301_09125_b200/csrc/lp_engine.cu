@@ -427,6 +427,76 @@ __global__ void k_plan_rows(const int32_t* __restrict__ svid, const uint32_t* __
     }
 }
 
+// RAK plans: copy the rows into the storage CSR as flat pieces (warps take 32
+// pieces, eight arcs in flight per lane) and set the batch flags on the way.
+__global__ void __launch_bounds__(256)
+    k_plan_rows_pieces(const int32_t* __restrict__ svid, const uint32_t* __restrict__ off,
+                       const int32_t* __restrict__ nbr, const uint32_t* __restrict__ w,
+                       const uint32_t* __restrict__ soff, uint32_t* __restrict__ snbr, uint32_t* __restrict__ sw,
+                       const int32_t* __restrict__ dslot, const int32_t* __restrict__ dk0,
+                       const int32_t* __restrict__ dcount, int32_t* cursor, const int32_t* __restrict__ pos,
+                       int64_t bs, int flags_on) {
+    constexpr int J = 8;
+    const int lane = threadIdx.x & 31;
+    const int cnt = *dcount;
+    while (true) {
+        int b0 = 0;
+        if (lane == 0) b0 = atomicAdd(cursor, 32);
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (b0 >= cnt) break;
+        uint32_t src = 0, dst = 0, plen = 0;
+        int64_t bv = 0;
+        if (b0 + lane < cnt) {
+            const int32_t s = dslot[b0 + lane];
+            const int32_t v = svid[s];
+            const uint32_t k0 = (uint32_t)dk0[b0 + lane];
+            src = off[v] + k0;
+            dst = soff[s] + k0;
+            plen = min((uint32_t)kPieceArcs, soff[s + 1] - dst);
+            if (flags_on) bv = (int64_t)pos[v] / bs;
+        }
+        uint32_t incl = plen;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t excl = incl - plen;
+        for (uint32_t base = 0; base < total; base += 32 * J) {
+            uint32_t se[J], de[J];
+            int32_t u[J];
+            long long bvj[J];
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const uint32_t i = base + j * 32 + lane;
+                int r = 0;
+#pragma unroll
+                for (int step = 16; step >= 1; step >>= 1) {
+                    const uint32_t ex = __shfl_sync(0xffffffffu, excl, r + step);
+                    if (r + step < 32 && ex <= i) r += step;
+                }
+                const uint32_t pe = __shfl_sync(0xffffffffu, excl, r);
+                se[j] = __shfl_sync(0xffffffffu, src, r) + (i - pe);
+                de[j] = __shfl_sync(0xffffffffu, dst, r) + (i - pe);
+                bvj[j] = __shfl_sync(0xffffffffu, bv, r);
+                u[j] = i < total ? nbr[se[j]] : -1;
+            }
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                if (u[j] < 0) continue;
+                uint32_t f = 0;
+                if (flags_on) {
+                    const int64_t bu = (int64_t)pos[u[j]] / bs;
+                    f = (bu < bvj[j] ? kEarlier : 0u) | (bu > bvj[j] ? kLater : 0u);
+                }
+                snbr[de[j]] = ((uint32_t)u[j] << 2) | f;
+                if (w) sw[de[j]] = w[se[j]];
+            }
+        }
+    }
+}
+
 // INDEX plans: pieces (slot, first arc) of every active row, for phase-1
 // gathers that need the row of each arc
 __global__ void k_plan_piece_counts(const uint32_t* __restrict__ soff, uint32_t* __restrict__ cnt, int64_t S) {
@@ -878,7 +948,8 @@ static int device_shuffle(lp_graph* g, int64_t n, uint32_t seed, const int64_t**
 // degree-binned storage CSR (neighbour ids), the phase-1 label buffer.
 // RAK plans follow `order_host` (NULL: shuffled_indices(n, seed)); INDEX
 // plans use the identity order and ignore both.
-static int build_plan(lp_graph* g, int kind, const int64_t* order_host, uint32_t seed, float* plan_ms) {
+static int build_plan(lp_graph* g, int kind, const int64_t* order_host, uint32_t seed, float* plan_ms,
+                      int64_t bs_hint = -1) {
     const int64_t n = g->n;
     g->pk = kind;
     const bool index = kind == kPlanIndex;
@@ -962,11 +1033,11 @@ static int build_plan(lp_graph* g, int kind, const int64_t* order_host, uint32_t
     LP_CK(dalloc(&P.snbr, P.m_active, &bytes));
     LP_CK(dalloc(&P.lbuf, P.m_active, &bytes));
     if (g->w) LP_CK(dalloc(&P.sw, P.m_active, &bytes));
-    k_plan_rows<<<g->num_sms * 16, 256, 0, st>>>(P.svid, g->off, g->nbr, g->w, P.soff, P.snbr, P.sw, P.S,
-                                                 index ? 1 : 0);
+    if (index)
+        k_plan_rows<<<g->num_sms * 16, 256, 0, st>>>(P.svid, g->off, g->nbr, g->w, P.soff, P.snbr, P.sw, P.S, 1);
     {
         // dense piece list (reuses t.sdeg as the per-slot piece counts / offsets):
-        // SLPA's dense gathers, the pull marks at sweep boundaries
+        // SLPA's dense gathers, the pull marks at sweep boundaries, the RAK row copy
         k_plan_piece_counts<<<G, 256, 0, st>>>(P.soff, t.sdeg, P.S);
         LP_CK(cub::DeviceScan::ExclusiveSum(g->cub_tmp, need2, t.sdeg, t.sdeg, (int)(P.S + 1), st));
         uint32_t np = 0;
@@ -979,6 +1050,16 @@ static int build_plan(lp_graph* g, int kind, const int64_t* order_host, uint32_t
         const int32_t npi = (int32_t)np;
         LP_CK(cudaMemcpyAsync(P.dcount, &npi, sizeof(int32_t), cudaMemcpyHostToDevice, st));
         k_plan_pieces<<<G, 256, 0, st>>>(P.soff, t.sdeg, P.dslot, P.dk0, P.S);
+    }
+    int64_t flags_key = -1;
+    if (!index) {
+        // RAK rows: flat piece copy with the batch flags of this run's batch size
+        const bool none = bs_hint <= 0 || bs_hint >= n;
+        flags_key = none ? n : bs_hint;
+        LP_CK(cudaMemsetAsync(g->routes.len + kGatherCursor, 0, sizeof(int32_t), st));
+        k_plan_rows_pieces<<<g->num_sms * 16, 256, 0, st>>>(P.svid, g->off, g->nbr, g->w, P.soff, P.snbr, P.sw,
+                                                          P.dslot, P.dk0, P.dcount, g->routes.len + kGatherCursor,
+                                                          P.pos, none ? 1 : bs_hint, none ? 0 : 1);
     }
     if (g->wmode == kFixed && P.S > 0) {
         LP_CK(dalloc(&P.swsum, P.S, &bytes));
@@ -993,7 +1074,7 @@ static int build_plan(lp_graph* g, int kind, const int64_t* order_host, uint32_t
     P.custom_order = custom;
     P.seed = seed;
     P.order_hash = oh;
-    P.flags_bs = -1;
+    P.flags_bs = flags_key;
     P.bytes = bytes;
     g->bytes += bytes;
     return LP_OK;
@@ -1401,9 +1482,9 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         return LP_OK;
     }
     float plan_ms = 0.f;
-    if (int rc = build_plan(g, kPlanRak, order, o->seed, &plan_ms)) return rc;
     const int64_t B = (o->batches == 0 || o->batches > n) ? n : o->batches;
     const int64_t bs = (n + B - 1) / B;
+    if (int rc = build_plan(g, kPlanRak, order, o->seed, &plan_ms, bs)) return rc;
     const bool cross = bs < n;  // some vertex depends on an earlier batch
     if (int rc = ensure_flags(g, bs, &plan_ms)) return rc;
     S->plan_ms = plan_ms;
@@ -1542,9 +1623,28 @@ extern "C" int lp_labels_download(lp_graph* g, int64_t* labels_out) {
     if (!g->labels_valid) return lp_fail(LP_ERR_INVALID, "no labels: run a detection first");
     if (g->n == 0) return LP_OK;
     LP_CK(cudaSetDevice(g->device));
-    k_labels_to64<<<g->num_sms * 8, 256, 0, g->stream>>>(g->cur, g->out64, g->n);
-    LP_CK(cudaMemcpyAsync(labels_out, g->out64, g->n * sizeof(int64_t), cudaMemcpyDeviceToHost, g->stream));
+    // int32 labels into a pinned staging buffer (full-speed DMA, half the
+    // bytes), widened to the caller's int64 array by host threads -- instead
+    // of a pageable int64 copy
+    // (the staging buffer is process-wide and grow-only: pinned allocations
+    // cost milliseconds, handles come and go)
+    static std::mutex mu;
+    static int32_t* stage = nullptr;
+    static size_t stage_cap = 0;
+    std::lock_guard<std::mutex> lock(mu);
+    const int64_t n = g->n;
+    if ((size_t)n > stage_cap) {
+        if (stage) cudaFreeHost(stage);
+        stage = nullptr;
+        stage_cap = 0;
+        LP_CK(cudaMallocHost((void**)&stage, (size_t)n * sizeof(int32_t)));
+        stage_cap = (size_t)n;
+    }
+    LP_CK(cudaMemcpyAsync(stage, g->cur, n * sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
     LP_CK(cudaStreamSynchronize(g->stream));
+    const int32_t* src = stage;
+#pragma omp parallel for schedule(static) if (n > (1 << 16))
+    for (int64_t v = 0; v < n; ++v) labels_out[v] = src[v];
     return LP_OK;
 }
 
