@@ -1364,7 +1364,13 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         a.horizon = INT32_MAX;
         next = kNextQueue;
     }
+    cudaEvent_t dbg0 = nullptr, dbg1 = nullptr;
+    if (g->debug_rounds) {
+        cudaEventCreate(&dbg0);
+        cudaEventCreate(&dbg1);
+    }
     while (true) {
+        if (dbg0) cudaEventRecord(dbg0, st);
         if (next == kNextQueue) {
             // route the queue (margin test); this round's writes queue into the other one
             LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
@@ -1418,6 +1424,14 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         if (!cross) break;  // no cross-batch reads: one round solves the sweep
         int64_t w = 0;
         if (int rc = round_writes(&w)) return rc;
+        if (dbg0) {
+            cudaEventRecord(dbg1, st);
+            cudaEventSynchronize(dbg1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, dbg0, dbg1);
+            fprintf(stderr, "[lp]   round %d (%s): %.3f ms, %lld label writes\n", *rounds,
+                    next == kNextQueue ? "frontier" : (next == kNextFirst ? "first" : "dense"), ms, (long long)w);
+        }
         if (w == 0) break;  // nothing changed: every read is final
         if (w >= dense_at) {
             // most labels moved: a full round costs less than marking and routing them
@@ -1426,6 +1440,10 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
             mark_pass();
             next = kNextQueue;
         }
+    }
+    if (dbg0) {
+        cudaEventDestroy(dbg0);
+        cudaEventDestroy(dbg1);
     }
     return LP_OK;
 }

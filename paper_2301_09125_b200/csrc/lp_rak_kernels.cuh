@@ -46,6 +46,7 @@ namespace lp {
 
 struct HubCand {
     unsigned long long w;  // weight bits (u32 / u64 / float bits)
+    unsigned long long w2; // runner-up weight bits (margin test)
     uint32_t sec;
     uint32_t ter;
     int32_t lab;
@@ -1000,6 +1001,7 @@ template <int BITS> struct STable<kUnit, BITS> {
 // (weight, sec) key -- `mult` > 1 means the first-position scan decides.
 template <typename A> struct Best {
     A w;
+    A w2;          // largest weight of any other label (== w on a tie at the maximum)
     uint32_t sec;
     uint32_t ter;  // ~first position once resolved, else 0
     int32_t lab;
@@ -1016,6 +1018,7 @@ template <typename A> __device__ __forceinline__ A from_bits_any(unsigned long l
 template <typename A> __device__ __forceinline__ Best<A> none_best() {
     Best<A> b;
     b.w = A(0);
+    b.w2 = A(0);
     b.sec = 0;
     b.ter = 0;
     b.lab = -1;
@@ -1031,13 +1034,22 @@ __device__ __forceinline__ uint32_t sec_of(int32_t lab, uint32_t seed, uint32_t 
 }
 
 // merge y into x (x keeps the larger key; equal keys add multiplicities)
+// (w2 follows: the runner-up of the merge is the loser's weight or the
+// winner's own runner-up, whichever is larger)
 template <typename A> __device__ __forceinline__ void merge_best(Best<A>& x, const Best<A>& y) {
     if (y.mult == 0) return;
-    if (x.mult == 0 || y.w > x.w || (y.w == x.w && (y.sec > x.sec || (y.sec == x.sec && y.ter > x.ter)))) {
+    if (x.mult == 0) {
         x = y;
+    } else if (y.w > x.w || (y.w == x.w && (y.sec > x.sec || (y.sec == x.sec && y.ter > x.ter)))) {
+        const A xw = x.w;
+        x = y;
+        x.w2 = x.w2 > xw ? x.w2 : xw;
     } else if (y.w == x.w && y.sec == x.sec && y.ter == x.ter) {
         x.mult += y.mult;
         x.lab = min(x.lab, y.lab);
+        x.w2 = x.w;
+    } else {
+        x.w2 = x.w2 > y.w ? x.w2 : y.w;
     }
 }
 
@@ -1046,6 +1058,7 @@ template <typename A> __device__ __forceinline__ Best<A> warp_merge(Best<A> b) {
     for (int m = 16; m >= 1; m >>= 1) {
         Best<A> o;
         o.w = shfl_xor_any(b.w, m);
+        o.w2 = shfl_xor_any(b.w2, m);
         o.sec = __shfl_xor_sync(0xffffffffu, b.sec, m);
         o.ter = __shfl_xor_sync(0xffffffffu, b.ter, m);
         o.lab = __shfl_xor_sync(0xffffffffu, b.lab, m);
@@ -1079,9 +1092,11 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 // (mult > 1 -> the caller resolves by scan order).
 struct ArgmaxScratch {
     unsigned long long w;
+    unsigned long long w2;  // largest weight below the maximum
     uint32_t sec;
     int32_t cnt;
     int32_t lab;
+    int32_t cntw;           // entries at the maximum weight
 };
 
 template <int WM, int TIE, int BITS, int GROUP_NW>
@@ -1101,9 +1116,11 @@ __device__ __forceinline__ Best<typename Acc<WM>::T> table_argmax(const STable<W
     if (GROUP_NW > 1) {
         if (tid == 0) {
             red->w = 0;
+            red->w2 = 0;
             red->sec = 0;
             red->cnt = 0;
             red->lab = -1;
+            red->cntw = 0;
         }
         __syncthreads();
         if (lane == 0) atomicMax(&red->w, mw);
@@ -1127,14 +1144,22 @@ __device__ __forceinline__ Best<typename Acc<WM>::T> table_argmax(const STable<W
             ms = red->sec;
         }
     }
-    // 3. multiplicity and one label
-    int c = 0;
+    // 3. multiplicity and one label; entries at the maximum weight and the
+    //    largest weight below it (the winner's lead, for the margin test)
+    int c = 0, cw = 0;
+    unsigned long long m2 = 0;
     int32_t lab = -1;
     for (int i = tid; i < nt; i += NT) {
         const int h = touched[i];
-        if (wbits<A>(t.weight(h)) == mw && (TIE == kScanFirst || sec_of<TIE>(t.key(h), seed, sweep, vtx) == ms)) {
-            ++c;
-            lab = t.key(h);
+        const unsigned long long b = wbits<A>(t.weight(h));
+        if (b == mw) {
+            ++cw;
+            if (TIE == kScanFirst || sec_of<TIE>(t.key(h), seed, sweep, vtx) == ms) {
+                ++c;
+                lab = t.key(h);
+            }
+        } else {
+            m2 = b > m2 ? b : m2;
         }
     }
     Best<A> r;
@@ -1142,21 +1167,31 @@ __device__ __forceinline__ Best<typename Acc<WM>::T> table_argmax(const STable<W
     r.sec = ms;
     r.ter = 0;
     const int wc = (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+    const int wcw = (int)__reduce_add_sync(0xffffffffu, (unsigned)cw);
+    m2 = warp_max_u64(m2);
     const unsigned hasb = __ballot_sync(0xffffffffu, lab >= 0);
     const int32_t wl = hasb ? __shfl_sync(0xffffffffu, lab, __ffs(hasb) - 1) : -1;
+    int tcw = wcw;
     if (GROUP_NW > 1) {
-        if (lane == 0 && wc) {
-            atomicAdd(&red->cnt, wc);
-            red->lab = wl;
+        if (lane == 0) {
+            if (wc) {
+                atomicAdd(&red->cnt, wc);
+                red->lab = wl;
+            }
+            if (wcw) atomicAdd(&red->cntw, wcw);
+            if (m2) atomicMax(&red->w2, m2);
         }
         __syncthreads();
         r.mult = red->cnt;
         r.lab = red->lab;
+        tcw = red->cntw;
+        m2 = red->w2;
         __syncthreads();
     } else {
         r.mult = wc;
         r.lab = wl;
     }
+    r.w2 = tcw > 1 ? r.w : from_bits_any<A>(m2);
     return r;
 }
 
@@ -1471,6 +1506,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                                                                      a.sweep, vtx, nullptr);
                 winner = b.lab;
                 wbest = b.w;
+                wsecond = b.w2;
                 if (b.mult > 1) {
                     // several labels tie at the maximum: the earliest in scan order wins
                     winner = -1;
@@ -1497,10 +1533,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                 ++verts;
                 const bool maj = WM != kFloat && wbest + wbest > total;
                 a.ndist[s] = (hashed ? ntouched : K) | (maj ? kMajBit : 0);
-                if (wsecond >= A(0) && !hashed)
-                    store_lead<A>(a, s, wbest, wsecond);
-                else
-                    store_gap<A>(a, s, wbest, total);
+                store_lead<A>(a, s, wbest, wsecond);
                 changed = commit_label_known(a, p, winner, xv, l0v, dchg, writes);
             }
             changed = __shfl_sync(0xffffffffu, changed, 0);
@@ -1777,6 +1810,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 if (tid == 0) {
                     HubCand hc;
                     hc.w = to_bits<A>(best.w);
+                    hc.w2 = to_bits<A>(best.w2);
                     hc.sec = best.sec;
                     hc.ter = best.ter;
                     hc.lab = best.lab;
@@ -1792,6 +1826,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                             const HubCand* src = a.r.cand + item.cb + j;
                             Best<A> o;
                             o.w = from_bits<A>(__ldcg(&src->w));
+                            o.w2 = from_bits<A>(__ldcg(&src->w2));
                             o.sec = __ldcg(&src->sec);
                             o.ter = __ldcg(&src->ter);
                             o.lab = __ldcg(&src->lab);
@@ -1871,6 +1906,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                         const int32_t key = __ldcg(gkeys + g);
                         Best<A> c;
                         c.w = gacc_read<A>(gacc + g);
+                        c.w2 = A(0);
                         c.lab = key;
                         c.sec = sec_of<TIE>(key, a.seed, a.sweep, vtx);
                         c.ter = ~__ldcg(gfirst + g);
@@ -1918,7 +1954,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 ++verts;
                 const bool maj = WM != kFloat && best.w + best.w > total;
                 a.ndist[s] = distinct | (maj ? kMajBit : 0);
-                store_gap<A>(a, s, best.w, total);
+                store_lead<A>(a, s, best.w, best.w2);
                 s_flag = commit_label(a, p, best.lab, dchg, writes) ? 1 : 0;
             }
         }
