@@ -788,17 +788,23 @@ __global__ void k_route_queue(EvalArgs a, const int32_t* __restrict__ mq_in, con
 // (label, changed count, distinct count, majority flag, margin, changed row).
 __global__ void __launch_bounds__(256) k_first_round(EvalArgs a, int32_t S) {
     long long dchg = 0, arcs = 0, writes = 0, verts = 0;
-    for (int32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
-        const int32_t p = __ldg(a.svid + s);
-        const uint32_t beg = __ldg(a.soff + s);
-        const int d = (int)(__ldg(a.soff + s + 1) - beg);
-        const int32_t lab = (int32_t)(__ldg(a.snbr + beg) >> 2);
-        arcs += d;
-        ++verts;
-        a.ndist[s] = d | (2 > d ? kMajBit : 0);
-        store_gap<uint32_t>(a, s, 1u, (uint32_t)d);
-        const bool ch = commit_label_known(a, p, lab, p, p, dchg, writes);
-        if (a.mark) push_changed_small(a, ch, s);
+    // (warp-uniform loop: the changed rows are pushed as pieces by the whole warp)
+    for (int32_t base = blockIdx.x * blockDim.x; base < S; base += gridDim.x * blockDim.x) {
+        const int32_t s = base + threadIdx.x;
+        bool ch = false;
+        int d = 0;
+        if (s < S) {
+            const int32_t p = __ldg(a.svid + s);
+            const uint32_t beg = __ldg(a.soff + s);
+            d = (int)(__ldg(a.soff + s + 1) - beg);
+            const int32_t lab = (int32_t)(__ldg(a.snbr + beg) >> 2);
+            arcs += d;
+            ++verts;
+            a.ndist[s] = d | (2 > d ? kMajBit : 0);
+            store_lead<uint32_t>(a, s, 1u, d > 1 ? 1u : 0u);
+            ch = commit_label_known(a, p, lab, p, p, dchg, writes);
+        }
+        if (a.mark) push_changed_batch(a, __ballot_sync(0xffffffffu, ch), s, d);
     }
     flush_counters(a, dchg, arcs, writes, verts);
 }

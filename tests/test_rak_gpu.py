@@ -247,3 +247,31 @@ def test_malformed_csr_rejected_on_upload(gpu):
     g = lp.Graph(3, 3, np.array([0, 1, 2, 3]), np.array([0, 1, 7]), np.ones(3), 3.0)
     with pytest.raises(ValueError, match="neighbor ids"):
         _lib.DeviceGraph(g)
+
+
+@pytest.mark.parametrize("env", [
+    {"LP_DENSE_FRAC": "1.01"},                    # always marks + frontier rounds
+    {"LP_DENSE_FRAC": "0.0"},                     # always full rounds
+    {"LP_CARRY_FRAC": "1.0"},                     # carry the frontier across every sweep
+    {"LP_MARGIN": "0"},                           # no margin skipping
+    {"LP_FIRST_ROUND": "0", "LP_SWEEP_FRONTIER": "0"},
+    {"LP_WAVES": "4"},                            # dense waves
+])
+def test_engine_policies_keep_exactness(gpu, oracle, env, monkeypatch):
+    """Every scheduling policy of the engine (chosen per handle from the
+    environment) must reach the same fixed point: bit-exact to the oracle."""
+    from paper_2301_09125_b200 import _lib
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for g in (lp.rmat(14, seed=3), lp.planted_partition(6000, 60, seed=2),
+              lp.synth.with_edge_weights(lp.rmat(12, seed=4), seed=1)):
+        dg = _lib.DeviceGraph(g)  # fresh handle: reads the policy
+        for batches, tie in ((0, "scan-first"), (0, "random"), (1, "scan-first"), (16, "min-label")):
+            want, it, changed = oracle.rak(g, batches=batches, tie=ORACLE_TIE[tie], seed=2, tolerance=1e-3,
+                                           max_iterations=15)
+            p = lp.RakParams(seed=2, tolerance=1e-3, max_iterations=15, batches=batches, tie=tie)
+            out, git, st, gch = lp.rak_labels(g, p, device_graph=dg)
+            assert git == it and np.array_equal(gch, changed), (env, batches, tie)
+            assert np.array_equal(out, want), (env, batches, tie)
+        dg.close()
