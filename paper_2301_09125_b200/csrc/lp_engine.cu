@@ -141,6 +141,8 @@ struct lp_graph {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t aux[2] = {nullptr, nullptr};  // concurrent tally kernels of a round
+    cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
     int64_t n = 0, m = 0;
     int64_t max_degree = 0;
     int64_t sliceable = 0;  // rows long enough to be cut into slices
@@ -688,6 +690,14 @@ template <int WM, int TIE> struct Launcher {
             k_route_dense<<<grid_for(P.big_end, 256, sms * 8), 256, 0, st>>>(a, 0, P.big_end);
             prof->end(st);
         }
+        // The tally kernels of a round are independent except for the spill chain
+        // warp<0> -> warp<1> -> team (overflowing rows move up a class), so they
+        // run on three streams: the chain on the handle's stream, the small rows
+        // and team2 on aux[0], the hubs on aux[1]; their tails overlap.
+        cudaStream_t sB = g->aux[0], sC = g->aux[1];
+        cudaEventRecord(g->ev_fork, st);
+        cudaStreamWaitEvent(sB, g->ev_fork, 0);
+        cudaStreamWaitEvent(sC, g->ev_fork, 0);
         // small rows, one launch per degree class (MAXD 16, 8, 4)
         for (int c = 0; c < 3; ++c) {
             const int bin = kBinS16 + c;
@@ -696,15 +706,15 @@ template <int WM, int TIE> struct Launcher {
             if (cnt <= 0) continue;
             const int32_t sb = dense ? P.bin_beg[bin] : -1, se = dense ? P.bin_beg[bin + 1] : -1;
             a.bin = kKSmall;
-            prof->begin(st, kKSmall);
+            prof->begin(sB, kKSmall);
             const int grid = grid_for(cnt, 256, sms * 8);
             if (c == 0)
-                k_small<WM, TIE, 16><<<grid, 256, 0, st>>>(a, sb, se);
+                k_small<WM, TIE, 16><<<grid, 256, 0, sB>>>(a, sb, se);
             else if (c == 1)
-                k_small<WM, TIE, 8><<<grid, 256, 0, st>>>(a, sb, se);
+                k_small<WM, TIE, 8><<<grid, 256, 0, sB>>>(a, sb, se);
             else
-                k_small<WM, TIE, 4><<<grid, 256, 0, st>>>(a, sb, se);
-            prof->end(st);
+                k_small<WM, TIE, 4><<<grid, 256, 0, sB>>>(a, sb, se);
+            prof->end(sB);
         }
         const bool big = dense && P.big_end > 0;
         if (big || h_len[kLenWarp] > 0) launch_warp<0>(g, a, h_len[kLenWarp], dense, prof);
@@ -720,20 +730,24 @@ template <int WM, int TIE> struct Launcher {
         }
         if (big || h_len[kLenTeam2] > 0) {
             a.bin = kKTeam;
-            prof->begin(st, kKTeam);
+            prof->begin(sB, kKTeam);
             const int grid = dense ? sms * occ_team2 : grid_for(h_len[kLenTeam2], 1, sms * occ_team2);
             k_team<WM, TIE, kTeam2Threads, kTeam2Bits, true>
-                <<<grid, kTeam2Threads, team_smem_bytes<WM, kTeam2Bits>(), st>>>(a, kLenTeam2);
-            prof->end(st);
+                <<<grid, kTeam2Threads, team_smem_bytes<WM, kTeam2Bits>(), sB>>>(a, kLenTeam2);
+            prof->end(sB);
         }
         if (big || h_len[kLenHub] > 0) {
             a.bin = kKHub;
-            prof->begin(st, kKHub);
+            prof->begin(sC, kKHub);
             const int grid = dense ? sms * occ_hub : grid_for(h_len[kLenHub], 1, sms * occ_hub);
             k_team<WM, TIE, kHubThreads, kHubBits, true>
-                <<<grid, kHubThreads, team_smem_bytes<WM, kHubBits>(), st>>>(a, kLenHub);
-            prof->end(st);
+                <<<grid, kHubThreads, team_smem_bytes<WM, kHubBits>(), sC>>>(a, kLenHub);
+            prof->end(sC);
         }
+        cudaEventRecord(g->ev_join[0], sB);
+        cudaEventRecord(g->ev_join[1], sC);
+        cudaStreamWaitEvent(st, g->ev_join[0], 0);
+        cudaStreamWaitEvent(st, g->ev_join[1], 0);
         // (the deferred marks of the rows that changed this round are launched
         // by the sweep driver: mark_pass)
     }
@@ -857,6 +871,11 @@ static void destroy_graph(lp_graph* g) {
         cudaStreamSynchronize(g->stream);  // the pool frees above are ordered on it
         cudaStreamDestroy(g->stream);
     }
+    for (int i = 0; i < 2; ++i) {
+        if (g->aux[i]) cudaStreamDestroy(g->aux[i]);
+        if (g->ev_join[i]) cudaEventDestroy(g->ev_join[i]);
+    }
+    if (g->ev_fork) cudaEventDestroy(g->ev_fork);
     delete g;
 }
 
@@ -1177,6 +1196,11 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
                                 "CUDA error %s at %s:%d", cudaGetErrorName(_e), __FILE__, __LINE__)); \
     } while (0)
     G_CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+        G_CK(cudaStreamCreateWithFlags(&g->aux[i], cudaStreamNonBlocking));
+        G_CK(cudaEventCreateWithFlags(&g->ev_join[i], cudaEventDisableTiming));
+    }
+    G_CK(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
     StreamScope ss(g->stream);
     pool_keep(g->device);
     G_CK(cudaEventCreate(&g->ev0));
