@@ -209,6 +209,8 @@ struct lp_graph {
     bool first_round_shortcut = true;  // LP_FIRST_ROUND=0 disables k_first_round
     bool sweep_frontier = true;        // active frontier across sweeps (LP_SWEEP_FRONTIER=0 disables)
     double carry_frac = 0.5;           // ... after sweeps that changed <= this share of the rows (LP_CARRY_FRAC)
+    bool pull_rounds = false;  // LP_PULL_ROUNDS=1: pulled marks instead of full rounds after big rounds (measured: no gain)
+    double pull_max_frac = 0.8;  // ... but a full round after rounds that changed more (LP_PULL_MAX)
     double dense_frac = 0.35;   // a round that changed >= this share of the active rows is followed by a
                                 // full round instead of marks + frontier (LP_DENSE_FRAC; >= 1 disables)
     bool labels_valid = false;
@@ -1183,6 +1185,8 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_MARGIN")) g->margin_skip = atoi(ev) != 0;
     if (const char* ev = getenv("LP_DEBUG_ROUNDS")) g->debug_rounds = atoi(ev) != 0;
     if (const char* ev = getenv("LP_DENSE_FRAC")) g->dense_frac = atof(ev);
+    if (const char* ev = getenv("LP_PULL_ROUNDS")) g->pull_rounds = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_PULL_MAX")) g->pull_max_frac = atof(ev);
     if (const char* ev = getenv("LP_FIRST_ROUND")) g->first_round_shortcut = atoi(ev) != 0;
     if (const char* ev = getenv("LP_SWEEP_FRONTIER")) g->sweep_frontier = atoi(ev) != 0;
     if (const char* ev = getenv("LP_CARRY_FRAC")) g->carry_frac = atof(ev);
@@ -1458,8 +1462,23 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         }
         if (w == 0) break;  // nothing changed: every read is final
         if (w >= dense_at) {
-            // most labels moved: a full round costs less than marking and routing them
-            next = kNextDense;
+            if (g->pull_rounds && P.npieces > 0 && (double)w < g->pull_max_frac * (double)P.S) {
+                // most labels moved: every row pulls the changed flags of its
+                // earlier-batch neighbours (one flat pass instead of an atomic per
+                // later-batch arc of every changed row); the margin test then
+                // filters the queue, and a still-large frontier runs as a full round
+                LP_CK(cudaMemsetAsync(g->chg, 0, g->n, st));
+                k_flags_from_changed<<<g->num_sms * 8, 256, 0, st>>>(a, g->chg);
+                LP_CK(cudaMemsetAsync(g->routes.len + kGatherCursor, 0, sizeof(int32_t), st));
+                prof->begin(st, -1);
+                k_pull_marks<<<g->num_sms * 16, 256, 0, st>>>(a, g->chg, P.dslot, P.dk0, P.dcount,
+                                                             g->routes.len + kGatherCursor, 1);
+                prof->end(st);
+                next = kNextQueue;
+            } else {
+                // a full round costs less than marking and routing nearly every row
+                next = kNextDense;
+            }
         } else {
             mark_pass();
             next = kNextQueue;
@@ -1623,7 +1642,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
                 // pass, one atomic per row piece with a changed neighbour)
                 k_changed_flags<<<g->num_sms * 8, 256, 0, st>>>(L0, X, g->chg, n);
                 k_pull_marks<<<g->num_sms * 16, 256, 0, st>>>(a, g->chg, P.dslot, P.dk0, P.dcount,
-                                                             g->routes.len + kGatherCursor);
+                                                             g->routes.len + kGatherCursor, 0);
             }
             prof.end(st);
         }

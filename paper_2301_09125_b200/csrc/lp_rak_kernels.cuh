@@ -483,6 +483,13 @@ __global__ void k_sweep_changes(EvalArgs a, const int32_t* __restrict__ lnew, co
     }
 }
 
+// changed flags of the rows on the changed list (first pieces)
+__global__ void k_flags_from_changed(EvalArgs a, uint8_t* __restrict__ chg) {
+    const int cnt = a.r.len[kLenChg];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+        if (a.r.ck0[i] == 0) chg[__ldg(a.svid + a.r.cslot[i])] = 1;
+}
+
 __global__ void k_changed_flags(const int32_t* __restrict__ lnew, const int32_t* __restrict__ lold,
                                 uint8_t* __restrict__ chg, int64_t n) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
@@ -496,7 +503,8 @@ __global__ void k_changed_flags(const int32_t* __restrict__ lnew, const int32_t*
 __global__ void __launch_bounds__(256) k_pull_marks(EvalArgs a, const uint8_t* __restrict__ chg,
                                                     const int32_t* __restrict__ dslot,
                                                     const int32_t* __restrict__ dk0,
-                                                    const int32_t* __restrict__ dcount, int32_t* cursor) {
+                                                    const int32_t* __restrict__ dcount, int32_t* cursor,
+                                                    int earlier_only) {
     constexpr int J = 8;
     __shared__ unsigned long long sums[8][32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -545,7 +553,8 @@ __global__ void __launch_bounds__(256) k_pull_marks(EvalArgs a, const uint8_t* _
             }
 #pragma unroll
             for (int j = 0; j < J; ++j)
-                if (e[j] != 0xffffffffu && __ldg(chg + (nb[j] >> 2))) atomicAdd(&sums[wib][rr[j]], mark_weight(a, e[j]));
+                if (e[j] != 0xffffffffu && (!earlier_only || (nb[j] & kEarlier)) && __ldg(chg + (nb[j] >> 2)))
+                    atomicAdd(&sums[wib][rr[j]], mark_weight(a, e[j]));
         }
         __syncwarp();
         const unsigned long long sm = sums[wib][lane];
