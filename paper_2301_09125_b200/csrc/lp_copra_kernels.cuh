@@ -243,6 +243,56 @@ __device__ __forceinline__ void table_restore(int32_t* keys, double* vals, const
     __syncwarp();
 }
 
+// The end of an evaluation (one warp): lanes < kk hold the kept labels and
+// their normalised belongings; sort by label (copra.py:97-107), best label
+// (_best_of_row, :111-121), compare with the working state, write and mark
+// the later-batch neighbours on change.
+__device__ void copra_commit(const CopraArgs& a, int32_t s, int cnt, int kk, int32_t mylab, double myb) {
+    const int lane = threadIdx.x & 31;
+    const int32_t v = __ldg(a.svid + s);
+    const uint32_t beg = __ldg(a.soff + s);
+    const int d = (int)(__ldg(a.soff + s + 1) - beg);
+    const int K = a.K;
+    // sort the kept labels by id: rank = number of smaller labels
+    int rank = 0;
+    for (int j = 0; j < kk; ++j) {
+        const int32_t o = __shfl_sync(0xffffffffu, mylab, j);
+        rank += (lane < kk) && o < mylab;
+    }
+    // maximum belonging, smallest id among ties
+    double bb = lane < kk ? myb : -1.0;
+    int32_t bl = lane < kk ? mylab : 0x7fffffff;
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, bb, m);
+        const int32_t ol = __shfl_xor_sync(0xffffffffu, bl, m);
+        if (ob > bb || (ob == bb && ol < bl)) {
+            bb = ob;
+            bl = ol;
+        }
+    }
+    const size_t row = (size_t)v * K;
+    bool diff = *((volatile int32_t*)a.sizeX + v) != kk;
+    if (lane < kk) {
+        diff |= *((volatile int32_t*)a.labsX + row + rank) != mylab;
+        diff |= __double_as_longlong(*((volatile double*)a.belsX + row + rank)) != __double_as_longlong(myb);
+    }
+    diff = __any_sync(0xffffffffu, diff);
+    if (diff) {
+        if (lane < kk) {
+            a.labsX[row + rank] = mylab;
+            a.belsX[row + rank] = myb;
+        }
+        if (lane == 0) {
+            a.sizeX[v] = kk;
+            a.bestX[v] = bl;
+        }
+        __threadfence();
+        if (a.mark) mark_row(a, beg, d, lane, 32);
+    }
+    if (lane == 0) a.ndist[s] = cnt;
+}
+
 // Phase 2 (one warp): _select_labels + _best_of_row over the distinct
 // labels in first-touch order (get(i) -> label, tally), then compare with
 // the working state; write and mark later-batch neighbours on change.
@@ -253,37 +303,72 @@ __device__ void copra_finish(const CopraArgs& a, int32_t s, int cnt, Get get, Co
     const uint32_t beg = __ldg(a.soff + s);
     const int d = (int)(__ldg(a.soff + s + 1) - beg);
     const int K = a.K;
-    // total (copra.py:59-61): serial in touched order; the warp loads 32
-    // tallies at a time and every lane runs the same serial sum
-    double total = 0.0;
-    for (int i0 = 0; i0 < cnt; i0 += 32) {
-        double w = 0.0;
-        if (i0 + lane < cnt) {
-            int32_t l;
-            get(i0 + lane, l, w);
-        }
-        const int m = min(32, cnt - i0);
-        for (int j = 0; j < m; ++j) total = __dadd_rn(total, shfl_f64(w, j));
+    // total (copra.py:59-61) is the serial float64 sum in touched order, and it
+    // is used only by the test tally * K >= total (:64-71).  A parallel sum of
+    // the same positive values is within E = (cnt + 32) * 2^-52 * sum of it, so
+    // the test is decided by the parallel sum unless tally * K falls inside
+    // that band -- or exactly, when every tally is an integer (the parallel
+    // sum is then exact too).  Only an undecided vertex pays the serial sum.
+    double tpar = 0.0;
+    bool allint = true;
+    for (int i = lane; i < cnt; i += 32) {
+        int32_t l;
+        double w;
+        get(i, l, w);
+        tpar += w;
+        allint &= w == floor(w);
     }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) tpar += __shfl_xor_sync(0xffffffffu, tpar, m);
+    allint = __all_sync(0xffffffffu, allint) && tpar < 9007199254740992.0;
+    const double band = allint ? 0.0 : tpar * (double)(cnt + 32) * 2.220446049250313e-16;
+    double total = tpar;
+    bool exact_total = allint;
     int kk = 0;  // (:64-71): first <= K labels with tally * K >= total, touched order
-    for (int i0 = 0; i0 < cnt && kk < K; i0 += 32) {
-        const int i = i0 + lane;
-        bool qual = false;
-        int32_t lab = 0;
-        double w = 0.0;
-        if (i < cnt) {
-            get(i, lab, w);
-            qual = __dmul_rn(w, (double)K) >= total;
-        }
-        const uint32_t bal = __ballot_sync(0xffffffffu, qual);
-        if (qual) {
-            const int rank = kk + __popc(bal & lanemask_lt());
-            if (rank < K) {
-                sm.outl[rank] = lab;
-                sm.outb[rank] = w;
+    for (int pass = 0; pass < 2; ++pass) {
+        kk = 0;
+        bool undecided = false;
+        for (int i0 = 0; i0 < cnt && kk < K; i0 += 32) {
+            const int i = i0 + lane;
+            bool qual = false;
+            int32_t lab = 0;
+            double w = 0.0;
+            if (i < cnt) {
+                get(i, lab, w);
+                const double p = __dmul_rn(w, (double)K);
+                if (exact_total) {
+                    qual = p >= total;
+                } else if (p >= total + band) {
+                    qual = true;
+                } else if (!(p < total - band)) {
+                    undecided = true;
+                }
             }
+            if (__any_sync(0xffffffffu, undecided)) break;
+            const uint32_t bal = __ballot_sync(0xffffffffu, qual);
+            if (qual) {
+                const int rank = kk + __popc(bal & lanemask_lt());
+                if (rank < K) {
+                    sm.outl[rank] = lab;
+                    sm.outb[rank] = w;
+                }
+            }
+            kk = min(K, kk + __popc(bal));
         }
-        kk = min(K, kk + __popc(bal));
+        if (!__any_sync(0xffffffffu, undecided)) break;
+        // undecided: the reference's serial total, touched order (the warp loads
+        // 32 tallies at a time and every lane runs the same serial sum)
+        total = 0.0;
+        for (int i0 = 0; i0 < cnt; i0 += 32) {
+            double w = 0.0;
+            if (i0 + lane < cnt) {
+                int32_t l;
+                get(i0 + lane, l, w);
+            }
+            const int m = min(32, cnt - i0);
+            for (int j = 0; j < m; ++j) total = __dadd_rn(total, shfl_f64(w, j));
+        }
+        exact_total = true;
     }
     __syncwarp();
     int32_t mylab = 0;
@@ -341,45 +426,7 @@ __device__ void copra_finish(const CopraArgs& a, int32_t s, int cnt, Get get, Co
             myb = 1.0;
         }
     }
-    // sort the kept labels by id (:97-107): rank = number of smaller labels
-    int rank = 0;
-    for (int j = 0; j < kk; ++j) {
-        const int32_t o = __shfl_sync(0xffffffffu, mylab, j);
-        rank += (lane < kk) && o < mylab;
-    }
-    // _best_of_row (:111-121): maximum belonging, smallest id among ties
-    double bb = lane < kk ? myb : -1.0;
-    int32_t bl = lane < kk ? mylab : 0x7fffffff;
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, bb, m);
-        const int32_t ol = __shfl_xor_sync(0xffffffffu, bl, m);
-        if (ob > bb || (ob == bb && ol < bl)) {
-            bb = ob;
-            bl = ol;
-        }
-    }
-    // commit: compare with the working state; write and mark on change
-    const size_t row = (size_t)v * K;
-    bool diff = *((volatile int32_t*)a.sizeX + v) != kk;
-    if (lane < kk) {
-        diff |= *((volatile int32_t*)a.labsX + row + rank) != mylab;
-        diff |= __double_as_longlong(*((volatile double*)a.belsX + row + rank)) != __double_as_longlong(myb);
-    }
-    diff = __any_sync(0xffffffffu, diff);
-    if (diff) {
-        if (lane < kk) {
-            a.labsX[row + rank] = mylab;
-            a.belsX[row + rank] = myb;
-        }
-        if (lane == 0) {
-            a.sizeX[v] = kk;
-            a.bestX[v] = bl;
-        }
-        __threadfence();
-        if (a.mark) mark_row(a, beg, d, lane, 32);
-    }
-    if (lane == 0) a.ndist[s] = cnt;
+    copra_commit(a, s, cnt, kk, mylab, myb);
 }
 
 // Warp per vertex, table of 2^BITS slots in smem.  Input: `in` (slots)
@@ -466,8 +513,15 @@ __host__ __device__ constexpr size_t copra_team_smem_bytes() {
            (size_t)kCopraTeamWarps * sizeof(CopraWarpSmem) + 256;
 }
 
+constexpr int kQualMax = 64;  // qualifiers the unordered finish handles
+
 __global__ void __launch_bounds__(kCopraTeamWarps * 32, 2) k_copra_team(CopraArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double s_red[kCopraTeamWarps];
+    __shared__ int s_ai[kCopraTeamWarps];
+    __shared__ int s_nq, s_und;
+    __shared__ int32_t s_qfirst[kQualMax], s_qlab[kQualMax];
+    __shared__ double s_qw[kQualMax];
     constexpr int slots = 1 << kCopraTeamBits;
     constexpr int W = kCopraTeamWarps;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -647,8 +701,122 @@ __global__ void __launch_bounds__(kCopraTeamWarps * 32, 2) k_copra_team(CopraArg
             }
             P *= 2;
         }
-        // (4) first-touch order: F[first] = entry, then an ordered compaction of F
+        // (4) finish without the first-touch order when possible: the parallel
+        // total decides every qualification test (see copra_finish), the
+        // qualifiers (few) are ordered by their first contribution, and the
+        // fallback tie-break uses the first contribution too.  An undecided
+        // test or too many qualifiers take the ordered path below.
         const int nent = ctl[1], C = ctl[3];
+        {
+            double tp = 0.0;
+            bool ai = true;
+            for (int e = tid; e < nent; e += blockDim.x) {
+                const double w = Eval[e];
+                tp += w;
+                ai &= w == floor(w);
+            }
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) tp += __shfl_xor_sync(0xffffffffu, tp, m);
+            ai = __all_sync(0xffffffffu, ai);
+            if (lane == 0) {
+                s_red[warp] = tp;
+                s_ai[warp] = ai ? 1 : 0;
+            }
+            if (tid == 0) {
+                s_nq = 0;
+                s_und = 0;
+            }
+            __syncthreads();
+            double T = 0.0;
+            bool AI = true;
+            for (int w2 = 0; w2 < W; ++w2) {
+                T += s_red[w2];
+                AI = AI && s_ai[w2];
+            }
+            AI = AI && T < 9007199254740992.0;
+            const double band = AI ? 0.0 : T * (double)(nent + 32) * 2.220446049250313e-16;
+            for (int e = tid; e < nent; e += blockDim.x) {
+                const double p = __dmul_rn(Eval[e], (double)a.K);
+                if (AI ? p >= T : p >= T + band) {
+                    const int qi = atomicAdd(&s_nq, 1);
+                    if (qi < kQualMax) {
+                        s_qfirst[qi] = Efirst[e];
+                        s_qlab[qi] = Elab[e];
+                        s_qw[qi] = Eval[e];
+                    }
+                } else if (!AI && !(p < T - band)) {
+                    s_und = 1;
+                }
+            }
+            __syncthreads();
+            if (!s_und && s_nq <= kQualMax) {
+                if (warp == 0) {
+                    const int nq = s_nq, K = a.K;
+                    int kk = 0;
+                    int32_t mylab = 0;
+                    double myb = 0.0;
+                    if (nq > 0) {
+                        // the first <= K qualifiers in touched order
+                        for (int qi = lane; qi < nq; qi += 32) {
+                            int rank = 0;
+                            for (int j = 0; j < nq; ++j) rank += s_qfirst[j] < s_qfirst[qi];
+                            if (rank < K) {
+                                sm.outl[rank] = s_qlab[qi];
+                                sm.outb[rank] = s_qw[qi];
+                            }
+                        }
+                        __syncwarp();
+                        kk = min(nq, K);
+                        double kept = 0.0;
+                        for (int i = 0; i < kk; ++i) kept = __dadd_rn(kept, sm.outb[i]);  // (every lane)
+                        const double inv = __ddiv_rn(1.0, kept);
+                        if (lane < kk) {
+                            mylab = sm.outl[lane];
+                            myb = __dmul_rn(sm.outb[lane], inv);
+                        }
+                    } else {
+                        // fallback (copra.py:72-93): maximum tally; the largest counter
+                        // hash among tied maxima, the earliest first touch on equal hashes
+                        double bw = -1.0;
+                        for (int e = lane; e < nent; e += 32) bw = fmax(bw, Eval[e]);
+#pragma unroll
+                        for (int m = 16; m >= 1; m >>= 1) bw = fmax(bw, __shfl_xor_sync(0xffffffffu, bw, m));
+                        const uint32_t vv = (uint32_t)__ldg(a.svid + s);
+                        uint32_t bh = 0, bf = 0xffffffffu;
+                        int32_t bl = kEmpty;
+                        for (int e = lane; e < nent; e += 32) {
+                            if (Eval[e] != bw) continue;
+                            const uint32_t h = tie_hash(a.seed, a.sweep, vv, (uint32_t)Elab[e]);
+                            const uint32_t f = (uint32_t)Efirst[e];
+                            if (bl == kEmpty || h > bh || (h == bh && f < bf)) {
+                                bh = h;
+                                bf = f;
+                                bl = Elab[e];
+                            }
+                        }
+#pragma unroll
+                        for (int m = 16; m >= 1; m >>= 1) {
+                            const uint32_t oh = __shfl_xor_sync(0xffffffffu, bh, m);
+                            const uint32_t of = __shfl_xor_sync(0xffffffffu, bf, m);
+                            const int32_t ol = __shfl_xor_sync(0xffffffffu, bl, m);
+                            if (ol != kEmpty && (bl == kEmpty || oh > bh || (oh == bh && of < bf))) {
+                                bh = oh;
+                                bf = of;
+                                bl = ol;
+                            }
+                        }
+                        kk = 1;
+                        if (lane == 0) {
+                            mylab = bl;
+                            myb = 1.0;
+                        }
+                    }
+                    copra_commit(a, s, nent, kk, mylab, myb);
+                }
+                continue;
+            }
+        }
+        // ordered path: F[first] = entry, then an ordered compaction of F
         LP_CHECK((size_t)C <= Cc, "contributions");
         for (int e = tid; e < nent; e += blockDim.x) {
             LP_CHECK(Efirst[e] >= 0 && Efirst[e] < C, "first index");

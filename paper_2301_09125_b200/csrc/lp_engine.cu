@@ -1672,6 +1672,15 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     g->labels_valid = true;
     if (int rc = finish_stats(g, prof, S, it, rounds, gathered, ms)) return rc;
     S->arcs_dense = g->m * it;
+#ifdef LP_PATH_STATS
+    {
+        unsigned long long h[8];
+        cudaMemcpy(h, g->counters + 16, sizeof(h), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[lp] k_warp paths: majority %llu, majority-miss %llu, register %llu, hashed %llu, "
+                "hashed-tied %llu, overflow %llu\n", h[0], h[5], h[1], h[2], h[3], h[4]);
+        cudaMemset(g->counters + 16, 0, sizeof(h));
+    }
+#endif
     return LP_OK;
 }
 

@@ -160,6 +160,14 @@ enum { kCtrChanged = 0, kCtrWrites = 1, kCtrGathered = 2, kCtrArcs = 4, kCtrVert
 constexpr int32_t kMajBit = 1 << 30;
 __host__ __device__ __forceinline__ int32_t nd_count(int32_t v) { return v & (kMajBit - 1); }
 
+#ifdef LP_PATH_STATS
+#define LP_STAT(a, k) atomicAdd((a).counters + 16 + (k), 1ull)
+#else
+#define LP_STAT(a, k) \
+    do {              \
+    } while (0)
+#endif
+
 constexpr int kSmallMax = 16;     // thread-per-vertex bound (degree)
 #ifndef LP_WARP_REG_EST
 #define LP_WARP_REG_EST 32  // rows estimated to hold more labels skip the warp register table
@@ -1374,9 +1382,11 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                         arcs += d;
                         ++verts;
                         store_gap<A>(a, s, cw, total);
+                        LP_STAT(a, 0);
                     }
                     continue;
                 }
+                if (lane == 0) LP_STAT(a, 5);
                 // no majority any more: full tally from the first block
 #pragma unroll
                 for (int c = 0; c < U; ++c) {
@@ -1470,6 +1480,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                 }
             }
             if (overflow) {
+                if (lane == 0) LP_STAT(a, 4);
                 // too many distinct labels for this table: wipe it and hand the
                 // vertex to the team kernel (launched after this one); the
                 // prefetched block may be this row's, refetch the next vertex's
@@ -1508,6 +1519,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                 }
                 winner = __shfl_sync(0xffffffffu, best.lab, 0);
                 wbest = best.w;  // valid in lane 0
+                if (lane == 0) LP_STAT(a, 1);
                 // runner-up weight (exact lead for the margin test)
                 A w2 = (lane < K && tkey != winner) ? tacc : A(0);
 #pragma unroll
@@ -1522,6 +1534,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                 winner = b.lab;
                 wbest = b.w;
                 wsecond = b.w2;
+                if (lane == 0) LP_STAT(a, b.mult > 1 ? 3 : 2);
                 if (b.mult > 1) {
                     // several labels tie at the maximum: the earliest in scan order wins
                     winner = -1;
