@@ -211,6 +211,15 @@ int lp_gen_rmat(int32_t scale, int64_t edges, double a, double b, double c, uint
                 int64_t* dst);
 int lp_csr_build_undirected(int64_t n, int64_t pairs, const int64_t* u, const int64_t* v, int64_t* offsets,
                             int64_t* neighbors, int64_t* m_out);
+/* The same builders on the GPU (identical arrays):
+ * lp_gen_rmat_csr generates the R-MAT pairs of lp_gen_rmat on the device
+ * and builds the canonical CSR; lp_csr_build_undirected_gpu builds it from a
+ * host pair list.  neighbors_cap = capacity of neighbors (2*pairs + n
+ * suffices); device < 0 = the calling thread's current device. */
+int lp_gen_rmat_csr(int32_t scale, int64_t edges, double a, double b, double c, uint64_t seed, int32_t device,
+                    int64_t* offsets, int64_t* neighbors, int64_t neighbors_cap, int64_t* m_out);
+int lp_csr_build_undirected_gpu(int64_t n, int64_t pairs, const int64_t* u, const int64_t* v, int32_t device,
+                                int64_t* offsets, int64_t* neighbors, int64_t neighbors_cap, int64_t* m_out);
 /* Page-lock a host range for fast uploads / downloads (cudaHostRegister). */
 int lp_host_register(void* ptr, int64_t bytes);
 int lp_host_unregister(void* ptr);

@@ -135,6 +135,8 @@ EXPORTS = (
     "lp_shuffled_indices",
     "lp_gen_rmat",
     "lp_csr_build_undirected",
+    "lp_gen_rmat_csr",
+    "lp_csr_build_undirected_gpu",
     "lp_host_register",
     "lp_host_unregister",
     "lp_last_error",
@@ -181,6 +183,10 @@ def lib():
     L.lp_shuffled_indices.argtypes = [C.c_int64, C.c_uint32, _i64p]
     L.lp_gen_rmat.argtypes = [C.c_int32, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_uint64, _i64p, _i64p]
     L.lp_csr_build_undirected.argtypes = [C.c_int64, C.c_int64, _i64p, _i64p, _i64p, _i64p, C.POINTER(C.c_int64)]
+    L.lp_gen_rmat_csr.argtypes = [C.c_int32, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_int32,
+                                  _i64p, _i64p, C.c_int64, C.POINTER(C.c_int64)]
+    L.lp_csr_build_undirected_gpu.argtypes = [C.c_int64, C.c_int64, _i64p, _i64p, C.c_int32, _i64p, _i64p, C.c_int64,
+                                              C.POINTER(C.c_int64)]
     L.lp_host_register.argtypes = [vp, C.c_int64]
     L.lp_host_unregister.argtypes = [vp]
     L.lp_last_error.restype = C.c_char_p

@@ -21,6 +21,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import ctypes as C
+
 import numpy as np
 
 from .graph import Graph, from_arcs, preprocess, undirected_csr
@@ -194,6 +196,32 @@ def rmat_edges(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.
     return src, dst
 
 
+def _rmat_gpu(scale: int, edge_factor: int, seed: int):
+    """The same graph built on the GPU (``lp_gen_rmat_csr``) when a device is
+    present (LP_BUILD_GPU=0 forces the host builder); None otherwise."""
+    import os
+
+    from . import _lib
+    from .graph import _ro
+
+    if os.environ.get("LP_BUILD_GPU", "1") == "0" or scale < 12:
+        return None
+    try:
+        if _lib.device_count() < 1:
+            return None
+    except Exception:
+        return None
+    n = 1 << scale
+    m_pairs = edge_factor << scale
+    offsets = np.empty(n + 1, dtype=np.int64)
+    nbr = np.empty(2 * m_pairs + n, dtype=np.int64)
+    m = C.c_int64(0)
+    _lib.check(_lib.lib().lp_gen_rmat_csr(scale, m_pairs, 0.57, 0.19, 0.19, seed, -1, offsets, nbr, nbr.size,
+                                          C.byref(m)))
+    nbr = nbr[: m.value].copy()
+    return Graph(n, int(m.value), _ro(offsets), _ro(nbr), _ro(np.ones(m.value, dtype=np.float64)), float(m.value + n))
+
+
 def rmat(scale: int = 22, edge_factor: int = 16, seed: int = 1, weighted: bool = False) -> Graph:
     """Configs 1 / 3: symmetrised R-MAT, duplicates and self-loops dropped.
 
@@ -201,8 +229,10 @@ def rmat(scale: int = 22, edge_factor: int = 16, seed: int = 1, weighted: bool =
     uniformly from [1, 2) (both arc directions equal, so the graph stays
     symmetric); self-loops keep weight 1.
     """
-    src, dst = rmat_edges(scale, edge_factor, seed=seed)
-    g = undirected_csr(1 << scale, src, dst)
+    g = _rmat_gpu(scale, edge_factor, seed)
+    if g is None:
+        src, dst = rmat_edges(scale, edge_factor, seed=seed)
+        g = undirected_csr(1 << scale, src, dst)
     if weighted:
         g = with_edge_weights(g, seed=seed + 1000)
     return g

@@ -275,3 +275,37 @@ def test_engine_policies_keep_exactness(gpu, oracle, env, monkeypatch):
             assert git == it and np.array_equal(gch, changed), (env, batches, tie)
             assert np.array_equal(out, want), (env, batches, tie)
         dg.close()
+
+
+def test_gpu_graph_builders_match_host(gpu, monkeypatch):
+    """lp_gen_rmat_csr / lp_csr_build_undirected_gpu build the same arrays as
+    the host builder (which tests/test_host_abi.py pins to the reference's
+    preprocess(from_arcs(...)))."""
+    import ctypes as C
+
+    from paper_2301_09125_b200 import _lib, synth
+
+    monkeypatch.setenv("LP_BUILD_GPU", "0")
+    host = synth.rmat(14, seed=7)
+    monkeypatch.setenv("LP_BUILD_GPU", "1")
+    dev = synth.rmat(14, seed=7)
+    assert np.array_equal(host.offsets, dev.offsets) and np.array_equal(host.neighbors, dev.neighbors)
+    rng = np.random.default_rng(5)
+    n = 3000
+    u = rng.integers(0, n, 40000)
+    v = rng.integers(0, n, 40000)
+    v[:500] = u[:500]  # self pairs
+    u[500:900] = u[900:1300]  # duplicates
+    v[500:900] = v[900:1300]
+    want = lp.undirected_csr(n, u, v)
+    off = np.empty(n + 1, dtype=np.int64)
+    nbr = np.empty(2 * u.size + n, dtype=np.int64)
+    m = C.c_int64(0)
+    _lib.check(_lib.lib().lp_csr_build_undirected_gpu(n, u.size, u.astype(np.int64), v.astype(np.int64), -1, off, nbr,
+                                                      nbr.size, C.byref(m)))
+    assert m.value == want.edge_count
+    assert np.array_equal(off, want.offsets) and np.array_equal(nbr[: m.value], want.neighbors)
+    with pytest.raises(ValueError):
+        _lib.check(_lib.lib().lp_csr_build_undirected_gpu(10, 1, np.array([0]), np.array([11]), -1,
+                                                          np.empty(11, np.int64), np.empty(12, np.int64), 12,
+                                                          C.byref(m)))
