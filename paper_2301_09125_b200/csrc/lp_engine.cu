@@ -225,6 +225,21 @@ __global__ void k_i64_to_u32(const int64_t* __restrict__ in, uint32_t* __restric
         out[i] = (uint32_t)in[i];
 }
 
+// flat form: row-start flags, then every arc that is not a row start must be
+// strictly above its predecessor
+__global__ void k_row_starts(const uint32_t* __restrict__ off, int64_t n, int64_t m, uint8_t* __restrict__ start) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        if ((int64_t)off[v] < m) start[off[v]] = 1;
+}
+__global__ void k_rows_sorted_flat(const int32_t* __restrict__ nbr, const uint8_t* __restrict__ start, int64_t m,
+                                   unsigned long long* bad) {
+    unsigned long long b = 0;
+    for (int64_t e = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
+        b += !start[e] && nbr[e] <= nbr[e - 1];
+    for (int o = 16; o >= 1; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(bad, b);
+}
+
 // bad[0] counts arcs not strictly above their predecessor in the row
 __global__ void k_rows_sorted(const uint32_t* __restrict__ off, const int32_t* __restrict__ nbr, int64_t n,
                               unsigned long long* bad) {
@@ -874,7 +889,7 @@ static void destroy_graph(lp_graph* g) {
         cudaStreamDestroy(g->stream);
     }
     for (int i = 0; i < 2; ++i) {
-        if (g->aux[i]) cudaStreamDestroy(g->aux[i]);
+        if (g->aux[i]) cudaStreamSynchronize(g->aux[i]);  // (shared streams: not destroyed)
         if (g->ev_join[i]) cudaEventDestroy(g->ev_join[i]);
     }
     if (g->ev_fork) cudaEventDestroy(g->ev_fork);
@@ -1200,9 +1215,22 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
                                 "CUDA error %s at %s:%d", cudaGetErrorName(_e), __FILE__, __LINE__)); \
     } while (0)
     G_CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i) {
-        G_CK(cudaStreamCreateWithFlags(&g->aux[i], cudaStreamNonBlocking));
-        G_CK(cudaEventCreateWithFlags(&g->ev_join[i], cudaEventDisableTiming));
+    {
+        // the auxiliary tally streams are per device and live for the process
+        // (creating / destroying streams per handle costs milliseconds)
+        static std::mutex mu;
+        static cudaStream_t pool[64][2];
+        static bool made[64] = {};
+        std::lock_guard<std::mutex> lock(mu);
+        const int dv = g->device & 63;
+        if (!made[dv]) {
+            for (int i = 0; i < 2; ++i) G_CK(cudaStreamCreateWithFlags(&pool[dv][i], cudaStreamNonBlocking));
+            made[dv] = true;
+        }
+        for (int i = 0; i < 2; ++i) {
+            g->aux[i] = pool[dv][i];
+            G_CK(cudaEventCreateWithFlags(&g->ev_join[i], cudaEventDisableTiming));
+        }
     }
     G_CK(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
     StreamScope ss(g->stream);
@@ -1245,7 +1273,15 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
             k_weight_scan<<<g->num_sms * 8, 256, 0, st>>>((const double*)tmp, m, g->counters + 4);
         }
         k_degree_stats<<<g->num_sms * 8, 256, 0, st>>>(g->off, n, g->counters + 8);
-        k_rows_sorted<<<g->num_sms * 16, 256, 0, st>>>(g->off, g->nbr, n, g->counters + 12);
+        if (m > 0) {
+            uint8_t* rs = nullptr;
+            int64_t rb = 0;
+            G_CK(dalloc(&rs, m, &rb));
+            G_CK(cudaMemsetAsync(rs, 0, m, st));
+            k_row_starts<<<g->num_sms * 8, 256, 0, st>>>(g->off, n, m, rs);
+            k_rows_sorted_flat<<<g->num_sms * 8, 256, 0, st>>>(g->nbr, rs, m, g->counters + 12);
+            dfree(rs);
+        }
         G_CK(cudaMemcpyAsync(g->h_counters, g->counters, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         G_CK(cudaStreamSynchronize(st));
         if (g->h_counters[11]) {
