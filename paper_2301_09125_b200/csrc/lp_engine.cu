@@ -1433,6 +1433,7 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         cudaEventCreate(&dbg0);
         cudaEventCreate(&dbg1);
     }
+    bool small_round = false;
     while (true) {
         if (dbg0) cudaEventRecord(dbg0, st);
         if (next == kNextQueue) {
@@ -1466,6 +1467,12 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
                 if (alg == kGatherRak) *gathered += P.m_active;
             } else {
                 run_round(g, a, false, g->h_len, prof, alg);
+                // a routed frontier smaller than the full-round threshold cannot write
+                // that many labels: no need to read the write count (one sync less)
+                int64_t routed = 0;
+                for (int c = 0; c <= kLenWarpBig; ++c) routed += g->h_len[c];
+                routed += g->h_len[kLenTeam2];
+                small_round = routed < dense_at && !dbg0;
             }
         } else {
             // every active row (dense), or the trivial first round from labels = ids
@@ -1486,6 +1493,12 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         }
         ++*rounds;
         if (!cross) break;  // no cross-batch reads: one round solves the sweep
+        if (small_round) {
+            small_round = false;
+            mark_pass();  // (an empty change list marks nothing; the next route ends the loop)
+            next = kNextQueue;
+            continue;
+        }
         int64_t w = 0;
         if (int rc = round_writes(&w)) return rc;
         if (dbg0) {
