@@ -141,8 +141,8 @@ struct lp_graph {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    cudaStream_t aux[2] = {nullptr, nullptr};  // concurrent tally kernels of a round
-    cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+    cudaStream_t aux[3] = {nullptr, nullptr, nullptr};  // concurrent tally kernels of a round
+    cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
     int64_t n = 0, m = 0;
     int64_t max_degree = 0;
     int64_t sliceable = 0;  // rows long enough to be cut into slices
@@ -213,6 +213,9 @@ struct lp_graph {
     double pull_max_frac = 0.8;  // ... but a full round after rounds that changed more (LP_PULL_MAX)
     double dense_frac = 0.35;   // a round that changed >= this share of the active rows is followed by a
                                 // full round instead of marks + frontier (LP_DENSE_FRAC; >= 1 disables)
+    int cap_route = 0;      // LP_CAP_ROUTE=1: route rows by table capacity >= degree (measured: no gain)
+    bool id_single = true;  // LP_ID_SINGLE=0: no singleton labels in the first sweep (see kSingle)
+    int warp_maxd[2] = {WarpClass<0>::kMaxDeg, WarpClass<1>::kMaxDeg};  // LP_WARP0_MAXD / LP_WARP1_MAXD
     bool labels_valid = false;
     std::vector<cudaEvent_t> event_pool;
 };
@@ -633,10 +636,16 @@ template <int WM, int TIE> struct Launcher {
     using A = typename Acc<WM>::T;
     static int occ_warp[2], occ_team, occ_team2, occ_hub, done_device;
     template <int WC> static cudaError_t setup_warp() {
-        cudaError_t e = cudaFuncSetAttribute(k_warp<WM, TIE, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)warp_smem_bytes<WM, WC>());
+        cudaError_t e;
+        if constexpr (WM == kUnit) {
+            e = cudaFuncSetAttribute(k_warp<WM, TIE, WC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)warp_smem_bytes<WM, WC>());
+            if (e) return e;
+        }
+        e = cudaFuncSetAttribute(k_warp<WM, TIE, WC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)warp_smem_bytes<WM, WC>());
         if (e) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_warp[WC], k_warp<WM, TIE, WC>,
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_warp[WC], k_warp<WM, TIE, WC, false>,
                                                           WarpClass<WC>::kWarps * 32, warp_smem_bytes<WM, WC>());
         occ_warp[WC] = std::max(occ_warp[WC], 1);
         return e;
@@ -670,14 +679,22 @@ template <int WM, int TIE> struct Launcher {
         done_device = device;
         return cudaSuccess;
     }
-    template <int WC> static void launch_warp(lp_graph* g, EvalArgs a, int64_t cnt, bool dense, Prof* prof) {
+    template <int WC>
+    static void launch_warp(lp_graph* g, EvalArgs a, int64_t cnt, bool dense, Prof* prof, cudaStream_t s) {
         const int sms = g->num_sms;
         a.bin = kKWarp;
-        prof->begin(g->stream, kKWarp);
+        prof->begin(s, kKWarp);
         const int per_block = 32 * WarpClass<WC>::kWarps;
         const int grid = dense ? sms * occ_warp[WC] : grid_for(cnt, per_block, sms * occ_warp[WC]);
-        k_warp<WM, TIE, WC><<<grid, WarpClass<WC>::kWarps * 32, warp_smem_bytes<WM, WC>(), g->stream>>>(a);
-        prof->end(g->stream);
+        if constexpr (WM == kUnit) {
+            if (a.id_single) {
+                k_warp<WM, TIE, WC, true><<<grid, WarpClass<WC>::kWarps * 32, warp_smem_bytes<WM, WC>(), s>>>(a);
+                prof->end(s);
+                return;
+            }
+        }
+        k_warp<WM, TIE, WC, false><<<grid, WarpClass<WC>::kWarps * 32, warp_smem_bytes<WM, WC>(), s>>>(a);
+        prof->end(s);
     }
     // One round.  dense: k_small sweeps the small slot range and the other
     // slots are routed; frontier: everything comes from the marked route.
@@ -711,6 +728,9 @@ template <int WM, int TIE> struct Launcher {
         // warp<0> -> warp<1> -> team (overflowing rows move up a class), so they
         // run on three streams: the chain on the handle's stream, the small rows
         // and team2 on aux[0], the hubs on aux[1]; their tails overlap.
+        // (Running the routed lists of the chain concurrently and the spills
+        // afterwards, on a fourth stream, measured slower: the kernels share the
+        // SMs' shared memory, the round is throughput-bound.)
         cudaStream_t sB = g->aux[0], sC = g->aux[1];
         cudaEventRecord(g->ev_fork, st);
         cudaStreamWaitEvent(sB, g->ev_fork, 0);
@@ -734,10 +754,10 @@ template <int WM, int TIE> struct Launcher {
             prof->end(sB);
         }
         const bool big = dense && P.big_end > 0;
-        if (big || h_len[kLenWarp] > 0) launch_warp<0>(g, a, h_len[kLenWarp], dense, prof);
+        if (big || h_len[kLenWarp] > 0) launch_warp<0>(g, a, h_len[kLenWarp], dense, prof, st);
         // each class may spill into the next one: launch on any upstream work
         if (big || h_len[kLenWarp] + h_len[kLenWarpBig] > 0)
-            launch_warp<1>(g, a, h_len[kLenWarp] + h_len[kLenWarpBig], dense, prof);
+            launch_warp<1>(g, a, h_len[kLenWarp] + h_len[kLenWarpBig], dense, prof, st);
         if (big || (h_len[kLenWarp] + h_len[kLenWarpBig] + h_len[kLenTeam]) > 0) {
             a.bin = kKTeam;
             prof->begin(st, kKTeam);
@@ -888,7 +908,7 @@ static void destroy_graph(lp_graph* g) {
         cudaStreamSynchronize(g->stream);  // the pool frees above are ordered on it
         cudaStreamDestroy(g->stream);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 3; ++i) {
         if (g->aux[i]) cudaStreamSynchronize(g->aux[i]);  // (shared streams: not destroyed)
         if (g->ev_join[i]) cudaEventDestroy(g->ev_join[i]);
     }
@@ -1205,6 +1225,10 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_FIRST_ROUND")) g->first_round_shortcut = atoi(ev) != 0;
     if (const char* ev = getenv("LP_SWEEP_FRONTIER")) g->sweep_frontier = atoi(ev) != 0;
     if (const char* ev = getenv("LP_CARRY_FRAC")) g->carry_frac = atof(ev);
+    if (const char* ev = getenv("LP_CAP_ROUTE")) g->cap_route = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_ID_SINGLE")) g->id_single = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_WARP0_MAXD")) g->warp_maxd[0] = std::max(17, std::min(WarpClass<0>::kMaxDeg, atoi(ev)));
+    if (const char* ev = getenv("LP_WARP1_MAXD")) g->warp_maxd[1] = std::max(17, std::min(WarpClass<1>::kMaxDeg, atoi(ev)));
     g->n = n;
     g->m = m;
 #define G_CK(call)                                                                                      \
@@ -1219,15 +1243,15 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
         // the auxiliary tally streams are per device and live for the process
         // (creating / destroying streams per handle costs milliseconds)
         static std::mutex mu;
-        static cudaStream_t pool[64][2];
+        static cudaStream_t pool[64][3];
         static bool made[64] = {};
         std::lock_guard<std::mutex> lock(mu);
         const int dv = g->device & 63;
         if (!made[dv]) {
-            for (int i = 0; i < 2; ++i) G_CK(cudaStreamCreateWithFlags(&pool[dv][i], cudaStreamNonBlocking));
+            for (int i = 0; i < 3; ++i) G_CK(cudaStreamCreateWithFlags(&pool[dv][i], cudaStreamNonBlocking));
             made[dv] = true;
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 3; ++i) {
             g->aux[i] = pool[dv][i];
             G_CK(cudaEventCreateWithFlags(&g->ev_join[i], cudaEventDisableTiming));
         }
@@ -1653,6 +1677,10 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.r = g->routes;
     a.bin = 0;
     a.seed = o->seed;
+    a.cap_route = g->cap_route;
+    a.id_single = 0;
+    a.warp_maxd[0] = g->warp_maxd[0];
+    a.warp_maxd[1] = g->warp_maxd[1];
 
     LP_CK(cudaMemsetAsync(g->counters, 0, kCtrCount * sizeof(unsigned long long), st));
     Prof prof;
@@ -1701,6 +1729,11 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         // weights and scan-first / min-label ties on duplicate-free sorted rows
         const bool first_ids = it == 1 && !labels_init && g->wmode == kUnit && g->rows_sorted &&
                                (o->tie == kScanFirst || o->tie == kMinLabel) && g->first_round_shortcut;
+        // first sweep from labels = ids: unevaluated neighbours carry singleton labels
+        // (not with random ties: measured slower -- the first round then has no
+        // shortcut and every row takes the all-weight-1 path)
+        a.id_single = (it == 1 && !labels_init && g->wmode == kUnit && g->rows_sorted && n < (1 << 30) &&
+                       o->tie != kRandom && g->id_single) ? 1 : 0;
         if (int rc = solve_sweep(g, a, cross, run_round, kGatherRak, &prof, &rounds, &gathered, first_ids, carry))
             return rc;
         LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, kCtrCount * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -1848,6 +1881,10 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     a.seed = o->seed;
     a.slots = g->slots;
     a.T = T;
+    a.cap_route = g->cap_route;
+    a.id_single = 0;
+    a.warp_maxd[0] = g->warp_maxd[0];
+    a.warp_maxd[1] = g->warp_maxd[1];
     LP_CK(cudaMemsetAsync(g->counters, 0, kCtrCount * sizeof(unsigned long long), st));
     unsigned long long* rep_ctr = g->counters + kCtrCount;  // spare counter slot
     Prof prof;

@@ -51,6 +51,7 @@ struct HubCand {
     uint32_t ter;
     int32_t lab;
     int32_t nd;
+    int32_t single;  // kSingle labels absent from this partition's table
 };
 
 // A k_team work item.
@@ -137,7 +138,24 @@ struct EvalArgs {
     uint32_t sweep;                     // RAK: sweep number; SLPA: speaking round t
     const int32_t* __restrict__ slots;  // SLPA memories [n x T] (slot t lives in x until the round ends)
     int32_t T;
+    int32_t cap_route;  // route a row to the smallest table that holds d entries even when its
+                        // estimate is larger (such a row can never overflow that table)
+    int32_t id_single;  // first sweep from labels = ids, unit weights, duplicate-free rows: see kSingle
+    int32_t warp_maxd[2];  // longest row routed to warp class 0 / 1 (longer rows go to the teams)
 };
+
+// First sweep from labels = vertex ids (rak.py:168): a neighbour that has not
+// been evaluated yet this sweep still carries its own id, so (rows being
+// duplicate-free) its label occurs once in the row unless an evaluated
+// neighbour's label equals it.  Phase 1 then stores the id with kSingle set
+// (no label load), and the hash tallies run two passes: evaluated labels are
+// inserted, flagged ones are only looked up (bumped when present, else counted
+// as singletons of weight 1).  With unit weights a singleton cannot win unless
+// every label has weight 1 -- then the winner is picked over all arcs.  The
+// tables hold a few percent of the row instead of half of it.
+constexpr int32_t kSingle = 1 << 30;
+__device__ __forceinline__ int32_t lb_strip(const EvalArgs& a, int32_t v) { return a.id_single ? (v & ~kSingle) : v; }  // (v >= 0)
+
 
 // phase-1 variants: what an arc's neighbour contributes to the tally
 enum GatherAlg : int { kGatherRak = 0, kGatherSlpa = 1 };
@@ -207,7 +225,8 @@ template <int WM> __device__ __forceinline__ typename Acc<WM>::T arc_weight(cons
 // Label of a neighbour under the batched schedule (phase 1).
 __device__ __forceinline__ int32_t gather_label(const EvalArgs& a, uint32_t nb) {
     const int32_t u = (int32_t)(nb >> 2);
-    return (nb & kEarlier) ? a.x[u] : __ldg(a.L0 + u);
+    if (nb & kEarlier) return a.x[u];
+    return a.id_single ? (u | kSingle) : __ldg(a.L0 + u);  // (first sweep: L0[u] == u)
 }
 
 __device__ __forceinline__ void flush_counters(const EvalArgs& a, long long dchg, long long arcs, long long writes,
@@ -660,8 +679,14 @@ __device__ __forceinline__ int route_class(const EvalArgs& a, int32_t s, int& es
     }
     const int nd = nd_count(__ldg(a.ndist + s));
     est = min(d, nd + (nd >> 2) + 16);
-    if (est <= WarpClass<0>::kEst && d <= WarpClass<0>::kMaxDeg) return 3;
-    if (est <= WarpClass<1>::kEst && d <= WarpClass<1>::kMaxDeg) return 6;
+    if (a.cap_route) {
+        // a table whose touched capacity is >= d cannot overflow
+        if (d <= (1 << WarpClass<0>::kBits) / 4 * 3) return 3;
+        if (d <= (1 << WarpClass<1>::kBits) / 4 * 3) return 6;
+        if (d <= (1 << kTeamBits) / 4 * 3) return 4;
+    }
+    if (est <= WarpClass<0>::kEst && d <= a.warp_maxd[0]) return 3;
+    if (est <= WarpClass<1>::kEst && d <= a.warp_maxd[1]) return 6;
     if (est <= kTeamEst && d <= kTeamMaxDeg) return 4;
     if (est <= kTeam2Est && d <= kTeamMaxDeg) return 7;
     return 5;
@@ -852,7 +877,7 @@ __global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, i
 #pragma unroll
         for (int k = 0; k < MAXD; ++k) {
             if (k < d) {
-                lab[k] = a.lbuf[beg + k];
+                lab[k] = lb_strip(a, a.lbuf[beg + k]);
                 w[k] = arc_weight<WM>(a, beg + k);
             } else {
                 lab[k] = kEmpty;
@@ -963,6 +988,7 @@ template <int WM, int BITS> struct STable {
         if (h >= 0) atomicAdd(&acc[h], w);
         return h;
     }
+    __device__ __forceinline__ void add_at(int h, A w) { atomicAdd(&acc[h], w); }
     __device__ __forceinline__ int find(int32_t lab) const {
         int h = (int)slot_hash(lab, BITS);
         for (int probe = 0; probe < HB; ++probe) {
@@ -982,6 +1008,7 @@ template <int BITS> struct STable<kUnit, BITS> {
     __device__ __forceinline__ void init(int h) { ent[h] = kEmpty64; }
     __device__ __forceinline__ int32_t key(int h) const { return (int32_t)(ent[h] >> 32); }
     __device__ __forceinline__ A weight(int h) const { return (uint32_t)ent[h]; }
+    __device__ __forceinline__ void add_at(int h, uint32_t c) { atomicAdd(&ent[h], (unsigned long long)c); }
     __device__ __forceinline__ int add(int32_t lab, uint32_t c, bool& isnew) {
         int h = (int)slot_hash(lab, BITS);
         isnew = false;
@@ -1226,6 +1253,45 @@ template <typename A> __device__ __forceinline__ A masked_sum(uint32_t m, A w) {
     return v;
 }
 
+// Winner of a row whose labels all have weight 1 (first sweep, kSingle): the
+// tie rule over every arc -- largest tie key, then the earliest arc (what the
+// table path's scan-order resolution gives).  One warp (red = null) or a
+// block of NT threads (red = 2 shared words).
+template <int TIE>
+__device__ __forceinline__ int32_t all_singles_winner(const EvalArgs& a, uint32_t beg, int d, uint32_t vtx, int tid,
+                                                      int NT, unsigned long long* red) {
+    unsigned long long bk = 0;
+    int32_t bl = -1;
+    for (int k = tid; k < d; k += NT) {
+        const int32_t lab = lb_strip(a, a.lbuf[beg + k]);
+        const unsigned long long key =
+            ((unsigned long long)sec_of<TIE>(lab, a.seed, a.sweep, vtx) << 32) | (unsigned long long)(~(uint32_t)k);
+        if (bl < 0 || key > bk) {
+            bk = key;
+            bl = lab;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const unsigned long long ok = shfl_u64(bk, o);
+        const int32_t ol = __shfl_xor_sync(0xffffffffu, bl, o);
+        if (ol >= 0 && (bl < 0 || ok > bk)) {
+            bk = ok;
+            bl = ol;
+        }
+    }
+    if (red == nullptr) return bl;
+    if (tid == 0) red[0] = 0ull;
+    __syncthreads();
+    if ((tid & 31) == 0 && bl >= 0) atomicMax(&red[0], bk);
+    __syncthreads();
+    if ((tid & 31) == 0 && bl >= 0 && bk == red[0]) red[1] = (unsigned long long)(uint32_t)bl;
+    __syncthreads();
+    const int32_t r = (int32_t)(uint32_t)red[1];
+    __syncthreads();
+    return r;
+}
+
 // ---------------------------------------------------------------------------
 // warp per vertex
 // ---------------------------------------------------------------------------
@@ -1272,7 +1338,9 @@ __device__ __forceinline__ int insert_chunk(STable<WM, BITS>& t, int32_t lab, ty
 // the first sweep most rows hold a handful of labels and this path needs no
 // shared memory and no atomics.  Rows estimated to hold more labels, or that
 // outgrow the register table, use the warp's shared-memory hash.
-template <int WM, int TIE, int WC>
+// TWO: the kSingle two-pass tally (first sweep from ids; a separate
+// instantiation keeps the other sweeps' code and registers unchanged)
+template <int WM, int TIE, int WC, bool TWO>
 __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k_warp(EvalArgs a) {
     using A = typename Acc<WM>::T;
     using WT = WarpTable<WM, WC>;
@@ -1291,12 +1359,13 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
     const int32_t cnt = a.r.len[WarpClass<WC>::kList];
     long long dchg = 0, arcs = 0, writes = 0, verts = 0;
     const int32_t* list = a.r.warp[WC];
+    const int cursor = kWarpCursor + WC;
     // batch size: 32 when the list is long, down to 1 so that short
     // (frontier) lists still spread over every warp
     const int bsz = max(1, min(32, cnt / (int)(gridDim.x * kWarpsPerBlock)));
     while (true) {
         int32_t b0 = 0;
-        if (lane == 0) b0 = atomicAdd(a.r.len + kWarpCursor + WC, bsz);
+        if (lane == 0) b0 = atomicAdd(a.r.len + cursor, bsz);
         b0 = __shfl_sync(0xffffffffu, b0, 0);
         if (b0 >= cnt) break;
         const int nv = min(bsz, cnt - b0);
@@ -1333,11 +1402,13 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
             const int32_t nd = __shfl_sync(0xffffffffu, mnd, v);
             const uint32_t vtx = (uint32_t)p;
             // prefetch the next block: of this row, else the next vertex's first one
-#define LP_WARP_PREFETCH(base_done)                                                             \
+#define LP_WARP_PREFETCH(base_done, wrap)                                                       \
     do {                                                                                        \
         uint32_t nb_beg = beg;                                                                  \
         int nb_base = (base_done) + 32 * U, nb_d = d;                                           \
-        if (nb_base >= d) {                                                                     \
+        if (nb_base >= d && (wrap)) {                                                           \
+            nb_base = 0;                                                                        \
+        } else if (nb_base >= d) {                                                              \
             const int vn = v + 1 < nv ? v + 1 : v;                                              \
             nb_beg = __shfl_sync(0xffffffffu, mbeg, vn);                                        \
             nb_d = v + 1 < nv ? (int)(__shfl_sync(0xffffffffu, mend, vn) - nb_beg) : 0;         \
@@ -1368,11 +1439,11 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                         const int k = base + c * 32 + lane;
                         labv[c] = (k < d) ? nbr_next[c] : kEmpty;
                     }
-                    LP_WARP_PREFETCH(base);
+                    LP_WARP_PREFETCH(base, false);
 #pragma unroll
                     for (int c = 0; c < U; ++c) {
                         const int k = base + c * 32 + lane;
-                        if (labv[c] == cand && k < d) cw += arc_weight<WM>(a, beg + k);
+                        if (k < d && (TWO ? lb_strip(a, labv[c]) : labv[c]) == cand) cw += arc_weight<WM>(a, beg + k);
                     }
                 }
 #pragma unroll
@@ -1395,7 +1466,9 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                 }
             }
             const int est = min(d, nd_count(nd) + (nd_count(nd) >> 2) + 16);
-            const bool agg = true;  // fold equal labels (__match_any_sync) before inserting
+            // fold equal labels (__match_any_sync) before inserting (per-lane inserts of
+            // diverse rows measured 2x slower: hot labels serialise on one address)
+            const bool agg = true;
             // register table (rows estimated to hold few labels)
             int32_t tkey = kEmpty;
             A tacc = A(0);
@@ -1404,6 +1477,9 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
             bool hashed = est > LP_WARP_REG_EST;  // use the shared hash
             int ntouched = 0;
             bool overflow = false;
+            int singles = 0;  // (two passes) flagged labels absent from the table, this lane
+            constexpr int npass = TWO ? 2 : 1;
+            for (int pass = 0; pass < npass && !overflow; ++pass)
             for (int base = 0; base < d && !overflow; base += 32 * U) {
                 int32_t labv[U];
                 A wv[U];
@@ -1413,12 +1489,42 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                     labv[c] = (k < d) ? nbr_next[c] : kEmpty;
                     wv[c] = (k < d) ? arc_weight<WM>(a, beg + k) : A(0);
                 }
-                LP_WARP_PREFETCH(base);
+                LP_WARP_PREFETCH(base, pass + 1 < npass);
 #pragma unroll
                 for (int c = 0; c < U; ++c) {
                     if (base + c * 32 >= d) break;  // warp-uniform
                     const int k0 = base + c * 32;
                     int32_t lab = labv[c];
+                    const bool flag = TWO && lab >= 0 && (lab & kSingle);
+                    if (TWO && lab >= 0) lab = lb_strip(a, lab);
+                    if (TWO && pass == 1) {
+                        // flagged labels: look up only
+                        if (!__any_sync(0xffffffffu, flag)) continue;
+                        bool hit = false;
+                        if (!hashed) {
+                            for (int t = 0; t < K; ++t) {
+                                const int32_t key = __shfl_sync(0xffffffffu, tkey, t);
+                                const uint32_t m = __ballot_sync(0xffffffffu, flag && lab == key);
+                                if (m) {
+                                    if (lane == t) {
+                                        tacc += (A)__popc(m);
+                                        // (scan-first: a flagged arc may precede the entry's first one)
+                                        tfirst = min(tfirst, (uint32_t)(k0 + __ffs(m) - 1));
+                                    }
+                                    hit |= flag && lab == key;
+                                }
+                            }
+                        } else if (flag) {
+                            const int h = tab->t.find(lab);
+                            if (h >= 0) {
+                                tab->t.add_at(h, A(1));
+                                hit = true;
+                            }
+                        }
+                        singles += (flag && !hit) ? 1 : 0;
+                        continue;
+                    }
+                    if (flag) lab = kEmpty;  // pass 0 of two: evaluated labels only
                     if (!hashed) {
                         uint32_t pending = __ballot_sync(0xffffffffu, lab != kEmpty);
                         for (int t = 0; t < K && pending; ++t) {
@@ -1498,7 +1604,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                     a.ndist[s] = max(nd_count(nd), 2 * WarpClass<WC>::kEst);
                 }
                 __syncwarp();
-                LP_WARP_PREFETCH(d);
+                LP_WARP_PREFETCH(d, false);
                 continue;
             }
             int32_t winner;
@@ -1544,6 +1650,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                         int32_t lab = kEmpty;
                         if (k < d) {
                             lab = a.lbuf[beg + k];
+                            if (TWO) lab = lb_strip(a, lab);
                             const int h = tab->t.find(lab);
                             ok = h >= 0 && tab->t.weight(h) == b.w && sec_of<TIE>(lab, a.seed, a.sweep, vtx) == b.sec;
                         }
@@ -1554,6 +1661,20 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                 __syncwarp();
                 for (int t = lane; t < ntouched; t += 32) tab->t.init(tab->touched[t]);
                 __syncwarp();
+            }
+            if (TWO) {
+                const int nsingle = (int)__reduce_add_sync(0xffffffffu, (unsigned)singles);
+                wbest = __shfl_sync(0xffffffffu, wbest, 0);
+                if (nsingle > 0) {
+                    if (wbest < A(2)) {
+                        // every label has weight 1: the tie rule over all arcs
+                        winner = all_singles_winner<TIE>(a, beg, d, vtx, lane, 32, nullptr);
+                        wbest = A(1);
+                        wsecond = d > 1 ? A(1) : A(0);
+                    } else if (wsecond < A(1)) {
+                        wsecond = A(1);
+                    }
+                }
             }
             bool changed = false;
             if (lane == 0) {
@@ -1627,6 +1748,9 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
     __shared__ int32_t s_gnew;
     __shared__ int32_t s_full;
     __shared__ int32_t s_sp;
+    __shared__ int32_t s_single;  // kSingle labels absent from the tables (this item)
+    __shared__ int32_t s_fb;      // every label has weight 1: pick over all arcs
+    __shared__ unsigned long long s_fbred[2];
     __shared__ unsigned long long s_first;  // (position << 32) | label of the earliest tied arc
     __shared__ uint32_t s_stack[STACK][2];  // (parts, want)
     __shared__ Best<A> s_red[NW];
@@ -1636,6 +1760,9 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
+    // kSingle two-pass tally on the 8/16-warp teams; the hub kernel inserts
+    // every label (its rows are sliced / partitioned by the true label count)
+    const bool two = a.id_single && NT < 1024;
     for (int h = tid; h < HB; h += NT) tab->t.init(h);
     const Item* items = which == kLenHub ? a.r.hub : (which == kLenTeam2 ? a.r.team2 : a.r.team);
     const int cursor = which == kLenHub ? kHubCursor : (which == kLenTeam2 ? kTeam2Cursor : kTeamCursor);
@@ -1683,7 +1810,9 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                     if (k < d) {
                         lab = a.lbuf[beg + k];
                         w = arc_weight<WM>(a, beg + k);
-                        if (parts > 1 && part_of(lab, parts) != want) lab = kEmpty;
+                        if (two && (lab & kSingle)) lab = kEmpty;  // (two passes: looked up below)
+                        else if (parts > 1 && part_of(lb_strip(a, lab), parts) != want) lab = kEmpty;
+                        else lab = lb_strip(a, lab);
                     }
                     labv[c] = lab;
                     wv[c] = w;
@@ -1723,6 +1852,29 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 __syncthreads();
                 continue;
             }
+            if (two) {
+                // pass 2: flagged labels of this partition are looked up only
+                int sg = 0;
+                for (int base = warp * 32; base < d; base += NT) {
+                    const int k = base + lane;
+                    if (k < d) {
+                        int32_t lab = a.lbuf[beg + k];
+                        if (lab & kSingle) {
+                            lab = lb_strip(a, lab);
+                            if (parts <= 1 || part_of(lab, parts) == want) {
+                                const int h = tab->t.find(lab);
+                                if (h >= 0)
+                                    tab->t.add_at(h, A(1));
+                                else
+                                    ++sg;
+                            }
+                        }
+                    }
+                }
+                sg = (int)__reduce_add_sync(0xffffffffu, (unsigned)sg);
+                if (lane == 0 && sg) atomicAdd(&s_single, sg);
+                __syncthreads();
+            }
             Best<A> b = table_argmax<WM, TIE, TBITS, NW>(tab->t, tab->touched, nt, tid, a.seed, a.sweep, vtx, &s_arg);
             const bool last_pass = single && s_sp == 0;
             if (b.mult > 1 || !last_pass) {
@@ -1736,7 +1888,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                     bool ok = false;
                     int32_t lab = kEmpty;
                     if (k < d) {
-                        lab = a.lbuf[beg + k];
+                        lab = lb_strip(a, a.lbuf[beg + k]);
                         if (parts <= 1 || part_of(lab, parts) == want) {
                             const int h = tab->t.find(lab);
                             ok = h >= 0 && tab->t.weight(h) == b.w &&
@@ -1794,7 +1946,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
 #pragma unroll
                 for (int c = 0; c < U; ++c) {
                     const int k = base + c * 32 + lane;
-                    labv[c] = (k < d) ? a.lbuf[beg + k] : kEmpty;
+                    labv[c] = (k < d) ? lb_strip(a, a.lbuf[beg + k]) : kEmpty;
                 }
 #pragma unroll
                 for (int c = 0; c < U; ++c) {
@@ -1830,9 +1982,17 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 s_sp = 1;
                 s_stack[0][0] = (uint32_t)item.P;
                 s_stack[0][1] = (uint32_t)item.q;
+                s_single = 0;
+                s_fb = 0;
             }
             __syncthreads();
             best = row_best(beg, d, vtx, item.P == 1, agg, distinct);
+            if (item.P == 1 && two && tid == 0 && s_single > 0) {
+                if (best.w < A(2))
+                    s_fb = 1;
+                else if (best.w2 < A(1))
+                    best.w2 = A(1);
+            }
             if (item.P > 1) {
                 // the last partition block merges the P candidates
                 if (tid == 0) {
@@ -1843,12 +2003,14 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                     hc.ter = best.ter;
                     hc.lab = best.lab;
                     hc.nd = distinct;
+                    hc.single = s_single;
                     a.r.cand[item.cb + item.q] = hc;
                     __threadfence();
                     s_last = atomicAdd(a.r.cand_done + item.cb, 1) == item.P - 1;
                     if (s_last) {
                         __threadfence();
                         distinct = 0;
+                        int msingle = 0;
                         best = none_best<A>();
                         for (int j = 0; j < item.P; ++j) {
                             const HubCand* src = a.r.cand + item.cb + j;
@@ -1860,13 +2022,29 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                             o.lab = __ldcg(&src->lab);
                             o.mult = 1;
                             distinct += __ldcg(&src->nd);
+                            msingle += __ldcg(&src->single);
                             merge_best(best, o);
+                        }
+                        if (two && msingle > 0) {
+                            if (best.w < A(2))
+                                s_fb = 1;
+                            else if (best.w2 < A(1))
+                                best.w2 = A(1);
                         }
                         a.r.cand_done[item.cb] = 0;
                     }
                 }
                 __syncthreads();
                 last = s_last;
+            }
+            __syncthreads();
+            if (s_fb) {  // (block-uniform; set only where this block commits)
+                const int32_t wl = all_singles_winner<TIE>(a, beg, d, vtx, tid, NT, s_fbred);
+                if (tid == 0) {
+                    best.lab = wl;
+                    best.w = A(1);
+                    best.w2 = d > 1 ? A(1) : A(0);
+                }
             }
         } else {
             // ---- arc slice: fold this slice into the per-vertex global table ----
@@ -1885,7 +2063,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 int32_t lab = kEmpty;
                 A w = A(0);
                 if (k < k_hi) {
-                    lab = a.lbuf[beg + k];
+                    lab = lb_strip(a, a.lbuf[beg + k]);
                     w = arc_weight<WM>(a, beg + k);
                 }
                 const uint32_t grp = __match_any_sync(0xffffffffu, lab);

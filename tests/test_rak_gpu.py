@@ -256,6 +256,9 @@ def test_malformed_csr_rejected_on_upload(gpu):
     {"LP_MARGIN": "0"},                           # no margin skipping
     {"LP_FIRST_ROUND": "0", "LP_SWEEP_FRONTIER": "0"},
     {"LP_WAVES": "4"},                            # dense waves
+    {"LP_ID_SINGLE": "0"},                        # no first-sweep singleton labels
+    {"LP_FIRST_ROUND": "0"},                      # singleton labels in a full first round (all weight 1)
+    {"LP_CAP_ROUTE": "1", "LP_WARP0_MAXD": "512"},  # capacity / degree routing
 ])
 def test_engine_policies_keep_exactness(gpu, oracle, env, monkeypatch):
     """Every scheduling policy of the engine (chosen per handle from the
