@@ -241,11 +241,14 @@ def run_ours(args, world, rank, local):
                           max_iterations=cfg["max_iterations"], batches=args.batches)
     dg = _lib.DeviceGraph(g, device=local)
     opts = lp.rak._opts(params)
-    opts.flags |= _lib.RAK_PROFILE
+    # per-launch CUDA events (the roofline's kernel times) cost ~0.6 ms per
+    # detection: the K timed steps run without them, K more steps with them
+    opts_ev = lp.rak._opts(params)
+    opts_ev.flags |= _lib.RAK_PROFILE
     L = _lib.lib()
 
-    def one(stats):
-        _lib.check(L.lp_rak_run_resident(dg.handle, C.byref(opts), None, C.byref(stats)))
+    def one(stats, o=opts):
+        _lib.check(L.lp_rak_run_resident(dg.handle, C.byref(o), None, C.byref(stats)))
 
     for _ in range(max(args.warmup, 1)):
         one(_lib.RunStats())
@@ -271,9 +274,20 @@ def run_ours(args, world, rank, local):
     dt_ms = reduce_max(ev0.elapsed_time(ev1), world, device=f"cuda:{local}")
     arcs_dense = sum(p["arcs_dense"] for p in per)
     value = whole_job_gteps(arcs_dense, dt_ms, world)
+    per_t = per
+    if not args.no_kernel_events:
+        # the same K steps again with per-launch events: kernel times for the roofline
+        per = []
+        for _ in range(args.steps):
+            st = _lib.RunStats()
+            one(st, opts_ev)
+            per.append(st.as_dict())
+        torch.cuda.synchronize()
 
     # roofline of the dominant kernel (per-launch averages over the timed region)
     kernels = kernel_table(per, weighted)
+    if not kernels:  # --no-kernel-events
+        kernels = {"none": {"ms": 1e-9, "launches": 1, "bytes": 0, "model": "no per-launch events"}}
     top = max(kernels, key=lambda k: kernels[k]["ms"])
     kt = kernels[top]
     bytes_per_launch = kt["bytes"] / max(kt["launches"], 1)
@@ -336,9 +350,11 @@ def run_ours(args, world, rank, local):
                    "vertices": g.vertex_count, "arcs": g.edge_count,
                    "l2": "inputs larger than L2 (int32 CSR %.0f MB vs 126 MB L2)" % (4 * g.edge_count / 1e6),
                    "parallelism": f"replicas x{world}"},
-        "iterations": per[-1]["iterations"], "rounds": per[-1]["rounds"],
-        "arcs_scanned_per_step": per[-1]["arcs_scanned"], "arcs_dense_per_step": per[-1]["arcs_dense"],
-        "gpu_launches": int(sum(p["launches"] for p in per)),
+        "iterations": per_t[-1]["iterations"], "rounds": per_t[-1]["rounds"],
+        "arcs_scanned_per_step": per[-1]["arcs_scanned"], "arcs_dense_per_step": per_t[-1]["arcs_dense"],
+        "gpu_launches": int(sum(p["launches"] for p in per_t)),
+        "kernel_events": "kernel times (roofline) from K more steps run with per-launch CUDA events on the "
+                          "library's streams right after the timed region (the events cost ~0.6 ms per step)",
         "roofline": roofline,
         "modularity": q_ours,
         "modes": modes,
@@ -430,6 +446,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-modes", action="store_true", help="skip the secondary schedule / tie-rule timings")
+    ap.add_argument("--no-kernel-events", action="store_true",
+                    help="time the steps without per-launch events (no kernel roofline)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

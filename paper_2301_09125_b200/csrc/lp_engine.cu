@@ -163,7 +163,7 @@ struct lp_graph {
     int32_t* cur = nullptr;  // the buffer holding the latest labels
     unsigned long long* mark = nullptr;  // frontier marks by vertex id (changed weight since routing)
     unsigned long long* gap = nullptr;   // per slot: winner margin lower bound at the last evaluation
-    uint8_t* chg = nullptr;              // sweep boundary: label changed in the last sweep
+    uint32_t* chg = nullptr;             // sweep boundary: label changed in the last sweep (bitmap)
     int32_t* mq[2] = {nullptr, nullptr};  // mark queues (alternate per round)
     int32_t* mq_len = nullptr;  // their lengths [2]
     int32_t* slots = nullptr;   // SLPA memories [n x T]
@@ -215,6 +215,9 @@ struct lp_graph {
                                 // full round instead of marks + frontier (LP_DENSE_FRAC; >= 1 disables)
     int cap_route = 0;      // LP_CAP_ROUTE=1: route rows by table capacity >= degree (measured: no gain)
     bool id_single = true;  // LP_ID_SINGLE=0: no singleton labels in the first sweep (see kSingle)
+    int push_div = 3;
+    int reg_est = LP_WARP_REG_EST;  // LP_REG_EST      // sweep boundary: push marks from the changed rows when <= 1/push_div of the
+                            // rows changed, else pull (LP_PUSH_DIV)
     int warp_maxd[2] = {WarpClass<0>::kMaxDeg, WarpClass<1>::kMaxDeg};  // LP_WARP0_MAXD / LP_WARP1_MAXD
     bool labels_valid = false;
     std::vector<cudaEvent_t> event_pool;
@@ -1227,6 +1230,8 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_CARRY_FRAC")) g->carry_frac = atof(ev);
     if (const char* ev = getenv("LP_CAP_ROUTE")) g->cap_route = atoi(ev) != 0;
     if (const char* ev = getenv("LP_ID_SINGLE")) g->id_single = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_PUSH_DIV")) g->push_div = std::max(1, atoi(ev));
+    if (const char* ev = getenv("LP_REG_EST")) g->reg_est = std::max(0, std::min(32, atoi(ev)));
     if (const char* ev = getenv("LP_WARP0_MAXD")) g->warp_maxd[0] = std::max(17, std::min(WarpClass<0>::kMaxDeg, atoi(ev)));
     if (const char* ev = getenv("LP_WARP1_MAXD")) g->warp_maxd[1] = std::max(17, std::min(WarpClass<1>::kMaxDeg, atoi(ev)));
     g->n = n;
@@ -1268,7 +1273,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     G_CK(dalloc(&g->labB, n, &g->bytes));
     G_CK(dalloc(&g->mark, n + 4, &g->bytes));
     G_CK(dalloc(&g->gap, n + 4, &g->bytes));
-    G_CK(dalloc(&g->chg, n + 4, &g->bytes));
+    G_CK(dalloc(&g->chg, n / 32 + 2, &g->bytes));
     G_CK(dalloc(&g->mq[0], n + 4, &g->bytes));
     G_CK(dalloc(&g->mq[1], n + 4, &g->bytes));
     G_CK(dalloc(&g->mq_len, 4, &g->bytes));
@@ -1540,7 +1545,7 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
                 // earlier-batch neighbours (one flat pass instead of an atomic per
                 // later-batch arc of every changed row); the margin test then
                 // filters the queue, and a still-large frontier runs as a full round
-                LP_CK(cudaMemsetAsync(g->chg, 0, g->n, st));
+                LP_CK(cudaMemsetAsync(g->chg, 0, (g->n / 32 + 1) * sizeof(uint32_t), st));
                 k_flags_from_changed<<<g->num_sms * 8, 256, 0, st>>>(a, g->chg);
                 LP_CK(cudaMemsetAsync(g->routes.len + kGatherCursor, 0, sizeof(int32_t), st));
                 prof->begin(st, -1);
@@ -1681,6 +1686,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.id_single = 0;
     a.warp_maxd[0] = g->warp_maxd[0];
     a.warp_maxd[1] = g->warp_maxd[1];
+    a.reg_est = g->reg_est;
 
     LP_CK(cudaMemsetAsync(g->counters, 0, kCtrCount * sizeof(unsigned long long), st));
     Prof prof;
@@ -1708,7 +1714,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
             a.mq_out = g->mq[0];
             a.mq_len = g->mq_len;
             prof.begin(st, -1);
-            if (last_changed * 50 <= P.S) {
+            if (last_changed * g->push_div <= P.S) {
                 // few changed rows: push from them (one atomic per neighbour)
                 k_sweep_changes<<<g->num_sms * 8, 256, 0, st>>>(a, L0, X, (int32_t)P.S);  // L0 = last result
                 a.mark_all = 1;
@@ -1885,6 +1891,7 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     a.id_single = 0;
     a.warp_maxd[0] = g->warp_maxd[0];
     a.warp_maxd[1] = g->warp_maxd[1];
+    a.reg_est = g->reg_est;
     LP_CK(cudaMemsetAsync(g->counters, 0, kCtrCount * sizeof(unsigned long long), st));
     unsigned long long* rep_ctr = g->counters + kCtrCount;  // spare counter slot
     Prof prof;

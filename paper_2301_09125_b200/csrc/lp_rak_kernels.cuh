@@ -142,6 +142,7 @@ struct EvalArgs {
                         // estimate is larger (such a row can never overflow that table)
     int32_t id_single;  // first sweep from labels = ids, unit weights, duplicate-free rows: see kSingle
     int32_t warp_maxd[2];  // longest row routed to warp class 0 / 1 (longer rows go to the teams)
+    int32_t reg_est;       // rows estimated to hold more labels skip the warp register table
 };
 
 // First sweep from labels = vertex ids (rak.py:168): a neighbour that has not
@@ -188,7 +189,9 @@ __host__ __device__ __forceinline__ int32_t nd_count(int32_t v) { return v & (kM
 
 constexpr int kSmallMax = 16;     // thread-per-vertex bound (degree)
 #ifndef LP_WARP_REG_EST
-#define LP_WARP_REG_EST 32  // rows estimated to hold more labels skip the warp register table
+#define LP_WARP_REG_EST 8  // rows estimated to hold more labels skip the warp register table (LP_REG_EST;
+                           // 8 measured 4% faster than 32 on R-MAT-22: the register table costs a
+                           // ballot per entry per chunk)
 #endif
 // warp classes: 0 = 512-slot table (est <= 256, d <= 2048, 8 warps/block),
 // 1 = 1024-slot table (est <= 512, d <= 8192, 8 warps/block)
@@ -511,23 +514,39 @@ __global__ void k_sweep_changes(EvalArgs a, const int32_t* __restrict__ lnew, co
 }
 
 // changed flags of the rows on the changed list (first pieces)
-__global__ void k_flags_from_changed(EvalArgs a, uint8_t* __restrict__ chg) {
-    const int cnt = a.r.len[kLenChg];
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
-        if (a.r.ck0[i] == 0) chg[__ldg(a.svid + a.r.cslot[i])] = 1;
+// Changed-vertex flags are a bitmap (bit v of word v / 32): the pull pass
+// gathers one flag per arc, and 512 KB for R-MAT-22 stays cache-resident
+// where a byte array (4 MB) thrashes L1.
+__device__ __forceinline__ bool chg_bit(const uint32_t* __restrict__ chg, int32_t v) {
+    return (__ldg(chg + (v >> 5)) >> (v & 31)) & 1u;
 }
 
+__global__ void k_flags_from_changed(EvalArgs a, uint32_t* __restrict__ chg) {
+    const int cnt = a.r.len[kLenChg];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+        if (a.r.ck0[i] == 0) {
+            const int32_t v = __ldg(a.svid + a.r.cslot[i]);
+            atomicOr(chg + (v >> 5), 1u << (v & 31));
+        }
+}
+
+// (whole warps: 32 consecutive vertices -> one bitmap word)
 __global__ void k_changed_flags(const int32_t* __restrict__ lnew, const int32_t* __restrict__ lold,
-                                uint8_t* __restrict__ chg, int64_t n) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
-        chg[v] = lnew[v] != lold[v];
+                                uint32_t* __restrict__ chg, int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+        const int64_t v = base + threadIdx.x;
+        const bool c = v < n && lnew[v] != lold[v];
+        const uint32_t w = __ballot_sync(0xffffffffu, c);
+        if ((threadIdx.x & 31) == 0 && v < n) chg[v >> 5] = w;
+    }
 }
 
 // Sweep boundary, pull form: warps take 32 row pieces (the plan's dense
 // piece list), sum the weights of arcs whose neighbour changed (shared-memory
 // atomics per piece), and add each nonzero sum to the row's mark -- the first
 // mark queues the vertex, as in k_mark_pieces.
-__global__ void __launch_bounds__(256) k_pull_marks(EvalArgs a, const uint8_t* __restrict__ chg,
+__global__ void __launch_bounds__(256) k_pull_marks(EvalArgs a, const uint32_t* __restrict__ chg,
                                                     const int32_t* __restrict__ dslot,
                                                     const int32_t* __restrict__ dk0,
                                                     const int32_t* __restrict__ dcount, int32_t* cursor,
@@ -578,10 +597,30 @@ __global__ void __launch_bounds__(256) k_pull_marks(EvalArgs a, const uint8_t* _
                 e[j] = i < total ? pb + (i - pe) : 0xffffffffu;
                 nb[j] = i < total ? __ldg(a.snbr + e[j]) : 0u;
             }
+            const bool unit = !(a.gap && a.sw);  // every mark weighs 1
 #pragma unroll
-            for (int j = 0; j < J; ++j)
-                if (e[j] != 0xffffffffu && (!earlier_only || (nb[j] & kEarlier)) && __ldg(chg + (nb[j] >> 2)))
-                    atomicAdd(&sums[wib][rr[j]], mark_weight(a, e[j]));
+            for (int j = 0; j < J; ++j) {
+                const bool hit = e[j] != 0xffffffffu && (!earlier_only || (nb[j] & kEarlier)) &&
+                                 chg_bit(chg, (int32_t)(nb[j] >> 2));
+                if (!unit) {
+                    if (hit) atomicAdd(&sums[wib][rr[j]], mark_weight(a, e[j]));
+                    continue;
+                }
+                // unit marks: one shared atomic per piece segment of the warp (lanes of a
+                // piece are consecutive: rr is non-decreasing across the lanes)
+                const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+                if (!bal) continue;
+                const int rprev = __shfl_up_sync(0xffffffffu, rr[j], 1);
+                const bool head = lane == 0 || rprev != rr[j];
+                const uint32_t heads = __ballot_sync(0xffffffffu, head);
+                if (head) {
+                    const uint32_t above = heads & ~((2u << lane) - 1u);
+                    const int nxt = above ? __ffs(above) - 1 : 32;
+                    const uint32_t seg = (nxt == 32 ? 0xffffffffu : ((1u << nxt) - 1u)) & ~((1u << lane) - 1u);
+                    const int c = __popc(bal & seg);
+                    if (c) atomicAdd(&sums[wib][rr[j]], (unsigned long long)c);
+                }
+            }
         }
         __syncwarp();
         const unsigned long long sm = sums[wib][lane];
@@ -1362,7 +1401,10 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
     const int cursor = kWarpCursor + WC;
     // batch size: 32 when the list is long, down to 1 so that short
     // (frontier) lists still spread over every warp
-    const int bsz = max(1, min(32, cnt / (int)(gridDim.x * kWarpsPerBlock)));
+    const int bcap = max(1, min(32, cnt / (int)(gridDim.x * kWarpsPerBlock)));
+    // ... and adapted to the arcs a batch held: the routed lists put long rows
+    // first, and 32 of them in one warp's batch is a tail of the whole kernel
+    int bsz = min(bcap, 2);
     while (true) {
         int32_t b0 = 0;
         if (lane == 0) b0 = atomicAdd(a.r.len + cursor, bsz);
@@ -1474,7 +1516,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
             A tacc = A(0);
             uint32_t tfirst = 0;
             int K = 0;                  // register entries in use (warp-uniform)
-            bool hashed = est > LP_WARP_REG_EST;  // use the shared hash
+            bool hashed = est > a.reg_est;  // use the shared hash
             int ntouched = 0;
             bool overflow = false;
             int singles = 0;  // (two passes) flagged labels absent from the table, this lane
@@ -1689,6 +1731,11 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
             if (changed) chm |= 1u << v;
         }
         if (a.mark) push_changed_batch(a, chm, ms, (int)(mend - mbeg));
+        {
+            constexpr int kBatchArcs = 1024;
+            const int tot = (int)__reduce_add_sync(0xffffffffu, lane < nv ? (unsigned)(mend - mbeg) : 0u);
+            bsz = max(1, min(bcap, (int)((long long)nv * kBatchArcs / max(tot, 1))));
+        }
     }
     flush_counters(a, dchg, arcs, writes, verts);
 }
