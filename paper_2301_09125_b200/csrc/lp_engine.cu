@@ -1513,7 +1513,12 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
             if (next == kNextFirst) {
                 a.bin = kKSmall;
                 prof->begin(st, kKSmall);
-                k_first_round<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S);
+                if (g->wmode == kFixed) {
+                    k_first_round_wbig<<<g->num_sms * 4, 256, 0, st>>>(a, (int32_t)P.S);
+                    k_first_round_w<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S);
+                }
+                else
+                    k_first_round<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S);
                 prof->end(st);
             } else {
                 run_round(g, a, true, g->h_len, prof, alg);  // (refreshes every margin)
@@ -1733,7 +1738,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         LP_CK(cudaMemsetAsync(g->counters + kCtrChanged, 0, 2 * sizeof(unsigned long long), st));
         // first sweep from labels = ids: the dense round is trivial for unit
         // weights and scan-first / min-label ties on duplicate-free sorted rows
-        const bool first_ids = it == 1 && !labels_init && g->wmode == kUnit && g->rows_sorted &&
+        const bool first_ids = it == 1 && !labels_init && (g->wmode == kUnit || g->wmode == kFixed) && g->rows_sorted &&
                                (o->tie == kScanFirst || o->tie == kMinLabel) && g->first_round_shortcut;
         // first sweep from labels = ids: unevaluated neighbours carry singleton labels
         // (not with random ties: measured slower -- the first round then has no

@@ -890,6 +890,123 @@ __global__ void __launch_bounds__(256) k_first_round(EvalArgs a, int32_t S) {
     flush_counters(a, dchg, arcs, writes, verts);
 }
 
+// Weighted (exact fixed-point) first round from labels = ids: every label of
+// a row is distinct, so its weight is its arc's weight -- the winner is the
+// heaviest arc (the earliest of equal ones: scan-first, and min-label on
+// sorted rows), the runner-up the second heaviest.  No gather, no tally:
+// k_first_round_w takes rows of <= kFirstBig arcs (one warp per row, 32 rows
+// per warp batch), k_first_round_wbig the longer ones (a block per row; the
+// plan stores long rows first, by descending degree).
+constexpr int kFirstBig = 4096;
+
+struct Top2 {
+    uint32_t w1, w2;
+    int k1;  // INT32_MAX = none
+};
+__device__ __forceinline__ void top2_add(Top2& t, uint32_t w, int k) {
+    if (t.k1 == INT32_MAX || w > t.w1) {
+        t.w2 = t.k1 == INT32_MAX ? 0u : t.w1;
+        t.w1 = w;
+        t.k1 = k;
+    } else if (w > t.w2) {
+        t.w2 = w;
+    }
+}
+__device__ __forceinline__ void top2_merge(Top2& t, const Top2& o) {
+    if (o.k1 == INT32_MAX) return;
+    if (t.k1 == INT32_MAX || o.w1 > t.w1 || (o.w1 == t.w1 && o.k1 < t.k1)) {
+        const uint32_t nw2 = t.k1 == INT32_MAX ? o.w2 : max(o.w2, t.w1);
+        t.w1 = o.w1;
+        t.w2 = nw2;
+        t.k1 = o.k1;
+    } else {
+        t.w2 = max(t.w2, o.w1);
+    }
+}
+__device__ __forceinline__ Top2 top2_warp(Top2 t) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        Top2 x;
+        x.w1 = __shfl_xor_sync(0xffffffffu, t.w1, o);
+        x.w2 = __shfl_xor_sync(0xffffffffu, t.w2, o);
+        x.k1 = __shfl_xor_sync(0xffffffffu, t.k1, o);
+        top2_merge(t, x);
+    }
+    return t;
+}
+// one thread: record the first-round result of row s
+__device__ __forceinline__ bool first_w_commit(const EvalArgs& a, int32_t s, int32_t p, uint32_t beg, int d,
+                                               const Top2& t, long long& dchg, long long& arcs, long long& writes,
+                                               long long& verts) {
+    const int32_t lab = (int32_t)(__ldg(a.snbr + beg + t.k1) >> 2);
+    const unsigned long long total = __ldg(a.swsum + s);
+    arcs += d;
+    ++verts;
+    const bool maj = 2ull * t.w1 > total;
+    a.ndist[s] = d | (maj ? kMajBit : 0);
+    store_lead<unsigned long long>(a, s, (unsigned long long)t.w1, (unsigned long long)t.w2);
+    return commit_label_known(a, p, lab, p, p, dchg, writes);
+}
+
+__global__ void __launch_bounds__(256) k_first_round_wbig(EvalArgs a, int32_t S) {
+    __shared__ Top2 red[8];
+    long long dchg = 0, arcs = 0, writes = 0, verts = 0;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    for (int32_t s = blockIdx.x; s < S; s += gridDim.x) {
+        const uint32_t beg = __ldg(a.soff + s);
+        const int d = (int)(__ldg(a.soff + s + 1) - beg);
+        if (d <= kFirstBig) break;  // (long rows come first)
+        Top2 t = {0u, 0u, INT32_MAX};
+        for (int k = threadIdx.x; k < d; k += blockDim.x) top2_add(t, __ldg(a.sw + beg + k), k);
+        t = top2_warp(t);
+        if (lane == 0) red[wib] = t;
+        __syncthreads();
+        if (wib == 0) {
+            t = lane < 8 ? red[lane] : Top2{0u, 0u, INT32_MAX};
+            t = top2_warp(t);
+            if (lane == 0) {
+                const int32_t p = __ldg(a.svid + s);
+                if (first_w_commit(a, s, p, beg, d, t, dchg, arcs, writes, verts) && a.mark) push_changed(a, s, d);
+            }
+        }
+        __syncthreads();
+    }
+    if (wib == 0) flush_counters(a, dchg, arcs, writes, verts);
+}
+
+__global__ void __launch_bounds__(256) k_first_round_w(EvalArgs a, int32_t S) {
+    long long dchg = 0, arcs = 0, writes = 0, verts = 0;
+    const int lane = threadIdx.x & 31;
+    const int32_t nwarps = (int32_t)(gridDim.x * blockDim.x / 32);
+    for (int32_t base = (int32_t)((blockIdx.x * blockDim.x + threadIdx.x) / 32) * 32; base < S; base += nwarps * 32) {
+        const int32_t ms = base + lane;
+        uint32_t mbeg = 0, mend = 0;
+        int32_t mp = 0;
+        if (ms < S) {
+            mp = __ldg(a.svid + ms);
+            mbeg = __ldg(a.soff + ms);
+            mend = __ldg(a.soff + ms + 1);
+        }
+        uint32_t chm = 0;
+        const int nv = min(32, S - base);
+        for (int v = 0; v < nv; ++v) {
+            const int32_t s = base + v;
+            const uint32_t beg = __shfl_sync(0xffffffffu, mbeg, v);
+            const int d = (int)(__shfl_sync(0xffffffffu, mend, v) - beg);
+            const int32_t p = __shfl_sync(0xffffffffu, mp, v);
+            if (d > kFirstBig) continue;  // k_first_round_wbig
+            Top2 t = {0u, 0u, INT32_MAX};
+            for (int k = lane; k < d; k += 32) top2_add(t, __ldg(a.sw + beg + k), k);
+            t = top2_warp(t);
+            bool ch = false;
+            if (lane == 0 && d > 0) ch = first_w_commit(a, s, p, beg, d, t, dchg, arcs, writes, verts);
+            if (__shfl_sync(0xffffffffu, ch, 0)) chm |= 1u << v;
+        }
+        if (a.mark) push_changed_batch(a, chm, ms, (int)(mend - mbeg));
+    }
+    flush_counters(a, dchg, arcs, writes, verts);
+}
+
 // ---------------------------------------------------------------------------
 // thread per vertex
 // ---------------------------------------------------------------------------

@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 for cfg in "$@"; do
   echo "== $cfg" >> gpurun_out/ab.log
-  env $cfg timeout 300 python scripts/prof_run.py --runs 4 --no-calibrate 2>&1 | grep -o "run 3: iterations.*kernel_ms [0-9.]*" >> gpurun_out/ab.log
+  env $cfg timeout 300 python scripts/prof_run.py --runs 4 --no-calibrate --config ${CONFIG:-rmat22} 2>&1 | grep -o "run 3: iterations.*kernel_ms [0-9.]*" >> gpurun_out/ab.log
   env $cfg timeout 300 python scripts/prof_run.py --runs 4 --no-calibrate --batches 1 2>&1 | grep -o "run 3: iterations.*kernel_ms [0-9.]*" >> gpurun_out/ab.log
   [ -n "$NONSTRICT" ] && env $cfg timeout 300 python scripts/prof_run.py --runs 3 --no-calibrate --non-strict 2>&1 | grep -o "run 2: iterations.*kernel_ms [0-9.]*" >> gpurun_out/ab.log
 done
