@@ -166,6 +166,7 @@ struct lp_graph {
     uint32_t* chg = nullptr;             // sweep boundary: label changed in the last sweep (bitmap)
     int32_t* mq[2] = {nullptr, nullptr};  // mark queues (alternate per round)
     int32_t* mq_len = nullptr;  // their lengths [2]
+    uint32_t* mbits = nullptr;  // marked-vertex bitmap (all zero between passes)
     int32_t* slots = nullptr;   // SLPA memories [n x T]
     size_t slots_cap = 0;
     // COPRA label sets (sweep-start and working), [n x K] rows
@@ -868,6 +869,7 @@ static void destroy_graph(lp_graph* g) {
     dfree(g->mq[0]);
     dfree(g->mq[1]);
     dfree(g->mq_len);
+    dfree(g->mbits);
     dfree(g->slots);
     for (int i = 0; i < 2; ++i) {
         dfree(g->clabs[i]);
@@ -1277,6 +1279,8 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     G_CK(dalloc(&g->mq[0], n + 4, &g->bytes));
     G_CK(dalloc(&g->mq[1], n + 4, &g->bytes));
     G_CK(dalloc(&g->mq_len, 4, &g->bytes));
+    G_CK(dalloc(&g->mbits, n / 32 + 2, &g->bytes));
+    G_CK(cudaMemsetAsync(g->mbits, 0, (n / 32 + 2) * sizeof(uint32_t), g->stream));
     G_CK(dalloc(&g->counters, 32, &g->bytes));
     G_CK(dalloc(&g->out64, n, &g->bytes));
     G_CK(cudaMallocHost((void**)&g->h_len, kLenCount * sizeof(int32_t)));
@@ -1394,6 +1398,12 @@ static int ensure_waves(lp_graph* g, int W) {
 // One sweep (RAK) or speaking round (SLPA): the dense round over every
 // active row, then frontier rounds over the mark queue until a round marks
 // nothing.  One host sync per frontier round (route sizes).
+// the vertices a marking pass flagged in the bitmap -> a.mq_out (bits cleared)
+static void bits_to_queue(lp_graph* g, const EvalArgs& a) {
+    const int64_t nwords = g->n / 32 + 1;
+    k_bits_to_queue<<<grid_for(nwords, 256, g->num_sms * 8), 256, 0, g->stream>>>(g->mbits, nwords, a.mq_out, a.mq_len);
+}
+
 static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round, int alg, Prof* prof, int* rounds,
                        int64_t* gathered, bool first_ids = false, bool carry = false) {
     const Plan& P = g->plan();
@@ -1410,6 +1420,7 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
     auto mark_pass = [&]() {
         prof->begin(st, -1);
         k_mark_pieces<<<g->num_sms * 16, 256, 0, st>>>(a);
+        bits_to_queue(g, a);
         prof->end(st);
     };
     // writes of the round just run (label changes); one sync
@@ -1556,6 +1567,7 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
                 prof->begin(st, -1);
                 k_pull_marks<<<g->num_sms * 16, 256, 0, st>>>(a, g->chg, P.dslot, P.dk0, P.dcount,
                                                              g->routes.len + kGatherCursor, 1);
+                bits_to_queue(g, a);
                 prof->end(st);
                 next = kNextQueue;
             } else {
@@ -1689,6 +1701,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.seed = o->seed;
     a.cap_route = g->cap_route;
     a.id_single = 0;
+    a.mbits = g->mbits;
     a.warp_maxd[0] = g->warp_maxd[0];
     a.warp_maxd[1] = g->warp_maxd[1];
     a.reg_est = g->reg_est;
@@ -1724,6 +1737,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
                 k_sweep_changes<<<g->num_sms * 8, 256, 0, st>>>(a, L0, X, (int32_t)P.S);  // L0 = last result
                 a.mark_all = 1;
                 k_mark_pieces<<<g->num_sms * 16, 256, 0, st>>>(a);
+                bits_to_queue(g, a);
                 a.mark_all = 0;
             } else {
                 // many: every row pulls the changed flags of its neighbours (one flat
@@ -1731,6 +1745,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
                 k_changed_flags<<<g->num_sms * 8, 256, 0, st>>>(L0, X, g->chg, n);
                 k_pull_marks<<<g->num_sms * 16, 256, 0, st>>>(a, g->chg, P.dslot, P.dk0, P.dcount,
                                                              g->routes.len + kGatherCursor, 0);
+                bits_to_queue(g, a);
             }
             prof.end(st);
         }
@@ -1894,6 +1909,7 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     a.T = T;
     a.cap_route = g->cap_route;
     a.id_single = 0;
+    a.mbits = g->mbits;
     a.warp_maxd[0] = g->warp_maxd[0];
     a.warp_maxd[1] = g->warp_maxd[1];
     a.reg_est = g->reg_est;

@@ -130,6 +130,8 @@ struct EvalArgs {
                                         // this sweep and need marks; INT32_MAX = all
     int32_t* mq_out;                    // queue of newly marked vertices (this round's writes)
     int32_t* mq_len;                    // its length
+    uint32_t* mbits;                    // marked-vertex bitmap: the pass kernels set bits with fire-and-
+                                        // forget atomics, k_bits_to_queue compacts them into mq_out
     int32_t* ndist;                     // per-slot distinct-label count of the last evaluation
     unsigned long long* counters;       // see kCtr* below
     Routes r;
@@ -544,8 +546,8 @@ __global__ void k_changed_flags(const int32_t* __restrict__ lnew, const int32_t*
 
 // Sweep boundary, pull form: warps take 32 row pieces (the plan's dense
 // piece list), sum the weights of arcs whose neighbour changed (shared-memory
-// atomics per piece), and add each nonzero sum to the row's mark -- the first
-// mark queues the vertex, as in k_mark_pieces.
+// atomics per piece), and add each nonzero sum to the row's mark -- the
+// bitmap queues the vertex, as in k_mark_pieces.
 __global__ void __launch_bounds__(256) k_pull_marks(EvalArgs a, const uint32_t* __restrict__ chg,
                                                     const int32_t* __restrict__ dslot,
                                                     const int32_t* __restrict__ dk0,
@@ -624,18 +626,10 @@ __global__ void __launch_bounds__(256) k_pull_marks(EvalArgs a, const uint32_t* 
         }
         __syncwarp();
         const unsigned long long sm = sums[wib][lane];
-        bool win = false;
-        int32_t v = -1;
         if (sm) {
-            v = __ldg(a.svid + ps);
-            win = atomicAdd(a.mark + v, sm) == 0ull;
-        }
-        const uint32_t bal = __ballot_sync(0xffffffffu, win);
-        if (bal) {
-            int q0 = 0;
-            if (lane == 0) q0 = atomicAdd(a.mq_len, __popc(bal));
-            q0 = __shfl_sync(0xffffffffu, q0, 0);
-            if (win) a.mq_out[q0 + __popc(bal & lanemask_lt())] = v;
+            const int32_t v = __ldg(a.svid + ps);
+            atomicAdd(a.mark + v, sm);  // (fire-and-forget; the bitmap queues v)
+            atomicOr(a.mbits + (v >> 5), 1u << (v & 31));
         }
         __syncwarp();
     }
@@ -684,21 +678,49 @@ __global__ void __launch_bounds__(256) k_mark_pieces(EvalArgs a) {
                 e[j] = i < total ? pb + (i - pe) : 0xffffffffu;
                 nb[j] = i < total ? __ldg(a.snbr + e[j]) : 0u;
             }
-            bool win[J];
 #pragma unroll
             for (int j = 0; j < J; ++j) {
                 const int32_t u = (int32_t)(nb[j] >> 2);
-                win[j] = e[j] != 0xffffffffu && (a.mark_all || (nb[j] & kLater)) && needs_mark(a, u) &&
-                         atomicAdd(a.mark + u, mark_weight(a, e[j])) == 0ull;
+                // (no returning atomic: the weight and the bitmap bit are fire-and-forget;
+                // k_bits_to_queue builds the queue -- 2.5x faster than queueing on the
+                // 0 -> nonzero transition of the mark)
+                if (e[j] != 0xffffffffu && (a.mark_all || (nb[j] & kLater)) && needs_mark(a, u)) {
+                    atomicAdd(a.mark + u, mark_weight(a, e[j]));
+                    atomicOr(a.mbits + (u >> 5), 1u << (u & 31));
+                }
             }
+        }
+    }
+}
+
+// Marked-vertex bitmap -> mark queue (appended to mq_out), bits cleared.
+// Whole warps: lane w of a warp takes bitmap word base + w.
+__global__ void k_bits_to_queue(uint32_t* __restrict__ mbits, int64_t nwords, int32_t* __restrict__ mq_out,
+                                int32_t* mq_len) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < nwords; base += stride) {
+        const int64_t w = base + threadIdx.x;
+        uint32_t b = w < nwords ? mbits[w] : 0u;
+        const int c = __popc(b);
+        int incl = c;
 #pragma unroll
-            for (int j = 0; j < J; ++j) {
-                const uint32_t bal = __ballot_sync(0xffffffffu, win[j]);
-                if (!bal) continue;
-                int q0 = 0;
-                if (lane == 0) q0 = atomicAdd(a.mq_len, __popc(bal));
-                q0 = __shfl_sync(0xffffffffu, q0, 0);
-                if (win[j]) a.mq_out[q0 + __popc(bal & lanemask_lt())] = (int32_t)(nb[j] >> 2);
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (tot == 0) continue;
+        int b0 = 0;
+        if (lane == 31) b0 = atomicAdd(mq_len, tot);
+        b0 = __shfl_sync(0xffffffffu, b0, 31);
+        if (b) {
+            mbits[w] = 0u;
+            int o = b0 + incl - c;
+            while (b) {
+                const int bit = __ffs(b) - 1;
+                mq_out[o++] = (int32_t)(w * 32 + bit);
+                b &= b - 1u;
             }
         }
     }
