@@ -217,7 +217,8 @@ struct lp_graph {
     int cap_route = 0;      // LP_CAP_ROUTE=1: route rows by table capacity >= degree (measured: no gain)
     bool id_single = true;  // LP_ID_SINGLE=0: no singleton labels in the first sweep (see kSingle)
     int push_div = 3;
-    int reg_est = LP_WARP_REG_EST;  // LP_REG_EST      // sweep boundary: push marks from the changed rows when <= 1/push_div of the
+    int reg_est = LP_WARP_REG_EST;  // LP_REG_EST
+    int mid_max = kMidMax;          // LP_MID_MAX: thread-per-row k_mid up to this degree (0 = off)      // sweep boundary: push marks from the changed rows when <= 1/push_div of the
                             // rows changed, else pull (LP_PUSH_DIV)
     int warp_maxd[2] = {WarpClass<0>::kMaxDeg, WarpClass<1>::kMaxDeg};  // LP_WARP0_MAXD / LP_WARP1_MAXD
     bool labels_valid = false;
@@ -638,7 +639,7 @@ struct Prof {
 
 template <int WM, int TIE> struct Launcher {
     using A = typename Acc<WM>::T;
-    static int occ_warp[2], occ_team, occ_team2, occ_hub, done_device;
+    static int occ_warp[2], occ_team, occ_team2, occ_hub, occ_mid, done_device;
     template <int WC> static cudaError_t setup_warp() {
         cudaError_t e;
         if constexpr (WM == kUnit) {
@@ -662,6 +663,11 @@ template <int WM, int TIE> struct Launcher {
         e = cudaFuncSetAttribute(k_team<WM, TIE, kTeamThreads, kTeamBits, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)team_smem_bytes<WM, kTeamBits>());
         if (e) return e;
+        e = cudaFuncSetAttribute(k_mid<WM, TIE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mid_smem_bytes<WM>());
+        if (e) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_mid, k_mid<WM, TIE>, kMidThreads, mid_smem_bytes<WM>());
+        if (e) return e;
+        occ_mid = std::max(occ_mid, 1);
         e = cudaFuncSetAttribute(k_team<WM, TIE, kTeam2Threads, kTeam2Bits, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)team_smem_bytes<WM, kTeam2Bits>());
         if (e) return e;
@@ -758,6 +764,13 @@ template <int WM, int TIE> struct Launcher {
             prof->end(sB);
         }
         const bool big = dense && P.big_end > 0;
+        if (a.mid_max > 0 && (big || h_len[kLenMid] > 0)) {
+            a.bin = kKSmall;
+            prof->begin(sB, kKSmall);
+            const int grid = dense ? sms * occ_mid : grid_for(h_len[kLenMid], kMidThreads, sms * occ_mid);
+            k_mid<WM, TIE><<<grid, kMidThreads, mid_smem_bytes<WM>(), sB>>>(a);
+            prof->end(sB);
+        }
         if (big || h_len[kLenWarp] > 0) launch_warp<0>(g, a, h_len[kLenWarp], dense, prof, st);
         // each class may spill into the next one: launch on any upstream work
         if (big || h_len[kLenWarp] + h_len[kLenWarpBig] > 0)
@@ -797,6 +810,7 @@ template <int WM, int TIE> int Launcher<WM, TIE>::occ_warp[2] = {1, 1};
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_team = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_team2 = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_hub = 1;
+template <int WM, int TIE> int Launcher<WM, TIE>::occ_mid = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::done_device = -1;
 
 typedef void (*round_fn)(lp_graph*, EvalArgs, bool, const int32_t*, Prof*, int);
@@ -845,6 +859,7 @@ static void free_routes(Routes& r) {
     dfree(r.warp[1]);
     dfree(r.team);
     dfree(r.team2);
+    dfree(r.mid);
     dfree(r.hub);
     dfree(r.len);
     dfree(r.cand);
@@ -997,7 +1012,12 @@ static int device_shuffle(lp_graph* g, int64_t n, uint32_t seed, const int64_t**
             LP_CK(cudaMalloc((void**)&e.d, std::max<size_t>((size_t)n, 1) * sizeof(int64_t)));
             e.cap = (size_t)n;
         }
-        LP_CK(cudaMemcpy(e.d, h.data(), (size_t)n * sizeof(int64_t), cudaMemcpyHostToDevice));
+        // (ordered on the handle's stream and completed before return: a pageable
+        // cudaMemcpy may return before its DMA lands, and the handle's
+        // non-blocking stream would then copy a stale order -- seen as a rare
+        // "order is not a permutation" when consecutive runs change the order)
+        LP_CK(cudaMemcpyAsync(e.d, h.data(), (size_t)n * sizeof(int64_t), cudaMemcpyHostToDevice, g->stream));
+        LP_CK(cudaStreamSynchronize(g->stream));
         e.n = n;
         e.seed = seed;
     }
@@ -1177,6 +1197,7 @@ static cudaError_t alloc_routes(lp_graph* g) {
     if ((e = dalloc(&r.warp[1], n, &g->bytes))) return e;
     if ((e = dalloc(&r.team, 2 * n, &g->bytes))) return e;
     if ((e = dalloc(&r.team2, n, &g->bytes))) return e;
+    if ((e = dalloc(&r.mid, n, &g->bytes))) return e;
     if ((e = dalloc(&r.hub, g->cap_items, &g->bytes))) return e;
     if ((e = dalloc(&r.len, kLenCount, &g->bytes))) return e;
     if ((e = dalloc(&r.cand, g->cap_items, &g->bytes))) return e;
@@ -1234,6 +1255,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_ID_SINGLE")) g->id_single = atoi(ev) != 0;
     if (const char* ev = getenv("LP_PUSH_DIV")) g->push_div = std::max(1, atoi(ev));
     if (const char* ev = getenv("LP_REG_EST")) g->reg_est = std::max(0, std::min(32, atoi(ev)));
+    if (const char* ev = getenv("LP_MID_MAX")) g->mid_max = std::max(0, std::min(kMidMax, atoi(ev)));
     if (const char* ev = getenv("LP_WARP0_MAXD")) g->warp_maxd[0] = std::max(17, std::min(WarpClass<0>::kMaxDeg, atoi(ev)));
     if (const char* ev = getenv("LP_WARP1_MAXD")) g->warp_maxd[1] = std::max(17, std::min(WarpClass<1>::kMaxDeg, atoi(ev)));
     g->n = n;
@@ -1417,10 +1439,15 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
     // carry: mq[0] already holds the vertices whose inputs changed since their
     // last evaluation (built at the sweep boundary); keep it
     LP_CK(cudaMemsetAsync(g->mq_len + (carry ? 1 : 0), 0, (carry ? 1 : 2) * sizeof(int32_t), st));
-    auto mark_pass = [&]() {
+    // (grid sized by the changed rows when known: every warp of the grid takes
+    // one atomic on the shared piece cursor, ~10 us for a full grid)
+    // (compact: the bitmap becomes the queue; the dense waves compact once after
+    // the last wave, so that a vertex marked by two waves is queued once)
+    auto mark_pass = [&](int64_t changed_rows, bool compact = true) {
+        const int64_t pieces = changed_rows + changed_rows / 8 + 32;
         prof->begin(st, -1);
-        k_mark_pieces<<<g->num_sms * 16, 256, 0, st>>>(a);
-        bits_to_queue(g, a);
+        k_mark_pieces<<<grid_for(pieces, 32 * 8, g->num_sms * 16), 256, 0, st>>>(a);
+        if (compact) bits_to_queue(g, a);
         prof->end(st);
     };
     // writes of the round just run (label changes); one sync
@@ -1461,11 +1488,12 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
             a.horizon = (int32_t)std::min<int64_t>(g->n, (w + 1) * ws);
             if (g->h_len[kLenGather] > 0) {
                 run_round(g, a, false, g->h_len, prof, alg);
-                if (a.mark) mark_pass();
+                if (a.mark) mark_pass(INT64_MAX / 4, false);
             }
             ++*rounds;
         }
         a.horizon = INT32_MAX;
+        if (a.mark) bits_to_queue(g, a);
         next = kNextQueue;
     }
     cudaEvent_t dbg0 = nullptr, dbg1 = nullptr;
@@ -1474,6 +1502,7 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         cudaEventCreate(&dbg1);
     }
     bool small_round = false;
+    int64_t last_routed = 0;
     while (true) {
         if (dbg0) cudaEventRecord(dbg0, st);
         if (next == kNextQueue) {
@@ -1511,8 +1540,9 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
                 // that many labels: no need to read the write count (one sync less)
                 int64_t routed = 0;
                 for (int c = 0; c <= kLenWarpBig; ++c) routed += g->h_len[c];
-                routed += g->h_len[kLenTeam2];
+                routed += g->h_len[kLenTeam2] + g->h_len[kLenMid];
                 small_round = routed < dense_at && !dbg0;
+                last_routed = routed;
             }
         } else {
             // every active row (dense), or the trivial first round from labels = ids
@@ -1540,7 +1570,7 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         if (!cross) break;  // no cross-batch reads: one round solves the sweep
         if (small_round) {
             small_round = false;
-            mark_pass();  // (an empty change list marks nothing; the next route ends the loop)
+            mark_pass(last_routed);  // (an empty change list marks nothing; the next route ends the loop)
             next = kNextQueue;
             continue;
         }
@@ -1575,7 +1605,7 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
                 next = kNextDense;
             }
         } else {
-            mark_pass();
+            mark_pass(w);
             next = kNextQueue;
         }
     }
@@ -1705,6 +1735,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.warp_maxd[0] = g->warp_maxd[0];
     a.warp_maxd[1] = g->warp_maxd[1];
     a.reg_est = g->reg_est;
+    a.mid_max = g->mid_max > kSmallMax ? g->mid_max : 0;
 
     LP_CK(cudaMemsetAsync(g->counters, 0, kCtrCount * sizeof(unsigned long long), st));
     Prof prof;
@@ -1913,6 +1944,7 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     a.warp_maxd[0] = g->warp_maxd[0];
     a.warp_maxd[1] = g->warp_maxd[1];
     a.reg_est = g->reg_est;
+    a.mid_max = g->mid_max > kSmallMax ? g->mid_max : 0;
     LP_CK(cudaMemsetAsync(g->counters, 0, kCtrCount * sizeof(unsigned long long), st));
     unsigned long long* rep_ctr = g->counters + kCtrCount;  // spare counter slot
     Prof prof;

@@ -86,11 +86,13 @@ enum {
     kChgCursor = 16,
     kLenTeam2 = 17,    // 16-warp team, 8192-slot table (est <= kTeam2Est, d <= kTeamMaxDeg)
     kTeam2Cursor = 18,
+    kLenMid = 19,      // thread per row, kSmallMax < d <= kMidMax (k_mid)
     kLenCount = 20
 };
 
 struct Routes {
     int32_t* small[3];  // slot lists by small degree class (4, 8, 16)
+    int32_t* mid;       // thread-per-row rows of kSmallMax < d <= kMidMax
     int32_t* warp[2];   // slot lists of the two warp classes
     Item* team;
     Item* team2;
@@ -145,6 +147,7 @@ struct EvalArgs {
     int32_t id_single;  // first sweep from labels = ids, unit weights, duplicate-free rows: see kSingle
     int32_t warp_maxd[2];  // longest row routed to warp class 0 / 1 (longer rows go to the teams)
     int32_t reg_est;       // rows estimated to hold more labels skip the warp register table
+    int32_t mid_max;       // rows of kSmallMax < d <= mid_max go to k_mid (0 = off)
 };
 
 // First sweep from labels = vertex ids (rak.py:168): a neighbour that has not
@@ -740,6 +743,7 @@ __device__ __forceinline__ int route_class(const EvalArgs& a, int32_t s, int& es
     }
     const int nd = nd_count(__ldg(a.ndist + s));
     est = min(d, nd + (nd >> 2) + 16);
+    if (d <= a.mid_max) return 8;
     if (a.cap_route) {
         // a table whose touched capacity is >= d cannot overflow
         if (d <= (1 << WarpClass<0>::kBits) / 4 * 3) return 3;
@@ -759,17 +763,19 @@ __device__ __forceinline__ void route_append(const EvalArgs& a, int cls, int32_t
     const int lane = threadIdx.x & 31;
     const uint32_t act = __activemask();
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < 9; ++c) {
         if (c == 5) continue;  // hubs below
         const uint32_t m = __ballot_sync(act, cls == c);
         if (!m) continue;
         const int leader = __ffs(m) - 1;
         int base = 0;
-        if (lane == leader) base = atomicAdd(a.r.len + (c == 7 ? kLenTeam2 : c), __popc(m));
+        if (lane == leader) base = atomicAdd(a.r.len + (c == 7 ? kLenTeam2 : (c == 8 ? kLenMid : c)), __popc(m));
         base = __shfl_sync(act, base, leader);
         if (cls == c) {
             const int idx = base + __popc(m & lanemask_lt());
-            if (c < 3) {
+            if (c == 8) {
+                a.r.mid[idx] = s;
+            } else if (c < 3) {
                 a.r.small[c][idx] = s;
             } else if (c == 3) {
                 a.r.warp[0][idx] = s;
@@ -1111,6 +1117,94 @@ __global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, i
         if (nd_new != nd) a.ndist[s] = nd_new;
         store_lead<A>(a, s, w1, w2);
         const bool ch = commit_label_known(a, p, best.lab, xv, l0v, dchg, writes);
+        if (a.mark) push_changed_small(a, ch, s);
+    }
+    flush_counters(a, dchg, arcs, writes, verts);
+}
+
+// Thread per row for kSmallMax < d <= kMidMax (listed rows): k_small's
+// O(d^2) tally with the row's labels staged in shared memory (column layout:
+// label k of thread t at [k][t], conflict-free) instead of registers.  A
+// warp then evaluates 32 rows at once with no shuffles, hashes or barriers --
+// mid-degree rows are latency-bound on the warp-per-row path.
+constexpr int kMidMax = 64;
+constexpr int kMidThreads = 128;
+template <int WM> constexpr size_t mid_smem_bytes() {
+    return (size_t)kMidMax * kMidThreads * (sizeof(int32_t) + (WM == kUnit ? 0 : sizeof(typename Acc<WM>::T)));
+}
+
+template <int WM, int TIE>
+__global__ void __launch_bounds__(kMidThreads) k_mid(EvalArgs a) {
+    using A = typename Acc<WM>::T;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int32_t* lab = reinterpret_cast<int32_t*>(smem_raw) + threadIdx.x;  // lab[k * kMidThreads]
+    A* wv = reinterpret_cast<A*>(smem_raw + (size_t)kMidMax * kMidThreads * sizeof(int32_t)) + threadIdx.x;
+    const int32_t cnt = a.r.len[kLenMid];
+    long long dchg = 0, arcs = 0, writes = 0, verts = 0;
+    for (int32_t base = blockIdx.x * blockDim.x; base < cnt; base += gridDim.x * blockDim.x) {
+        const int32_t i = base + threadIdx.x;
+        bool ch = false;
+        int32_t s = -1;
+        if (i < cnt) {
+            s = a.r.mid[i];
+            const int32_t p = __ldg(a.svid + s);
+            const uint32_t beg = __ldg(a.soff + s);
+            const int d = (int)(__ldg(a.soff + s + 1) - beg);
+            const int32_t xv = a.x[p];
+            const int32_t l0v = __ldg(a.L0 + p);
+            const int32_t nd = __ldg(a.ndist + s);
+            A total = A(0);
+            for (int k = 0; k < d; ++k) {
+                lab[k * kMidThreads] = lb_strip(a, a.lbuf[beg + k]);
+                const A w = arc_weight<WM>(a, beg + k);
+                if (WM != kUnit) wv[k * kMidThreads] = w;
+                total += w;
+            }
+#define LP_MID_W(k) (WM == kUnit ? A(1) : wv[(k) * kMidThreads])
+            arcs += d;
+            ++verts;
+            bool done = false;
+            if ((nd & kMajBit) && WM != kFloat) {
+                A cw = A(0);
+                for (int k = 0; k < d; ++k)
+                    if (lab[k * kMidThreads] == xv) cw += LP_MID_W(k);
+                if (cw + cw > total) {  // strict majority: label unchanged
+                    store_gap<A>(a, s, cw, total);
+                    done = true;
+                }
+            }
+            if (!done) {
+                const uint32_t vtx = (uint32_t)p;
+                Cand<A> best = none_cand<A>();
+                A w1 = A(0), w2 = A(0);
+                for (int i2 = 0; i2 < d; ++i2) {
+                    const int32_t li = lab[i2 * kMidThreads];
+                    bool dup = false;
+                    for (int j = 0; j < i2; ++j)
+                        if (lab[j * kMidThreads] == li) {
+                            dup = true;
+                            break;
+                        }
+                    if (dup) continue;  // counted at its first occurrence
+                    A sum = LP_MID_W(i2);
+                    for (int j = i2 + 1; j < d; ++j)
+                        if (lab[j * kMidThreads] == li) sum += LP_MID_W(j);
+                    const Cand<A> c = make_cand<TIE, A>(sum, li, (uint32_t)i2, a.seed, a.sweep, vtx);
+                    if (better(c, best)) best = c;
+                    if (sum > w1) {
+                        w2 = w1;
+                        w1 = sum;
+                    } else if (sum > w2) {
+                        w2 = sum;
+                    }
+                }
+#undef LP_MID_W
+                const int32_t nd_new = (best.w + best.w > total) ? kMajBit : 0;
+                if (nd_new != nd) a.ndist[s] = nd_new;
+                store_lead<A>(a, s, w1, w2);
+                ch = commit_label_known(a, p, best.lab, xv, l0v, dchg, writes);
+            }
+        }
         if (a.mark) push_changed_small(a, ch, s);
     }
     flush_counters(a, dchg, arcs, writes, verts);
