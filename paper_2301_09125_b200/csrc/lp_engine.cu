@@ -218,7 +218,8 @@ struct lp_graph {
     bool id_single = true;  // LP_ID_SINGLE=0: no singleton labels in the first sweep (see kSingle)
     int push_div = 3;
     int reg_est = LP_WARP_REG_EST;  // LP_REG_EST
-    int mid_max = kMidMax;          // LP_MID_MAX: thread-per-row k_mid up to this degree (0 = off)      // sweep boundary: push marks from the changed rows when <= 1/push_div of the
+    int mid_max = kMidMax;          // LP_MID_MAX: thread-per-row k_mid up to this degree (0 = off)
+    bool mid_hash = true;           // LP_MID_HASH=0: unit-weight mid rows by O(d^2) compares (k_mid)      // sweep boundary: push marks from the changed rows when <= 1/push_div of the
                             // rows changed, else pull (LP_PUSH_DIV)
     int warp_maxd[2] = {WarpClass<0>::kMaxDeg, WarpClass<1>::kMaxDeg};  // LP_WARP0_MAXD / LP_WARP1_MAXD
     bool labels_valid = false;
@@ -639,7 +640,7 @@ struct Prof {
 
 template <int WM, int TIE> struct Launcher {
     using A = typename Acc<WM>::T;
-    static int occ_warp[2], occ_team, occ_team2, occ_hub, occ_mid, done_device;
+    static int occ_warp[2], occ_team, occ_team2, occ_hub, occ_mid, occ_midh, done_device;
     template <int WC> static cudaError_t setup_warp() {
         cudaError_t e;
         if constexpr (WM == kUnit) {
@@ -668,6 +669,13 @@ template <int WM, int TIE> struct Launcher {
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_mid, k_mid<WM, TIE>, kMidThreads, mid_smem_bytes<WM>());
         if (e) return e;
         occ_mid = std::max(occ_mid, 1);
+        if constexpr (WM == kUnit) {
+            e = cudaFuncSetAttribute(k_midh<TIE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mid_hash_smem_bytes());
+            if (e) return e;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_midh, k_midh<TIE>, kMidHThreads, mid_hash_smem_bytes());
+            if (e) return e;
+            occ_midh = std::max(occ_midh, 1);
+        }
         e = cudaFuncSetAttribute(k_team<WM, TIE, kTeam2Threads, kTeam2Bits, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)team_smem_bytes<WM, kTeam2Bits>());
         if (e) return e;
@@ -767,8 +775,18 @@ template <int WM, int TIE> struct Launcher {
         if (a.mid_max > 0 && (big || h_len[kLenMid] > 0)) {
             a.bin = kKSmall;
             prof->begin(sB, kKSmall);
-            const int grid = dense ? sms * occ_mid : grid_for(h_len[kLenMid], kMidThreads, sms * occ_mid);
-            k_mid<WM, TIE><<<grid, kMidThreads, mid_smem_bytes<WM>(), sB>>>(a);
+            bool hashed = false;
+            if constexpr (WM == kUnit) {
+                if (g->mid_hash) {
+                    const int grid = dense ? sms * occ_midh : grid_for(h_len[kLenMid], kMidHThreads, sms * occ_midh);
+                    k_midh<TIE><<<grid, kMidHThreads, mid_hash_smem_bytes(), sB>>>(a);
+                    hashed = true;
+                }
+            }
+            if (!hashed) {
+                const int grid = dense ? sms * occ_mid : grid_for(h_len[kLenMid], kMidThreads, sms * occ_mid);
+                k_mid<WM, TIE><<<grid, kMidThreads, mid_smem_bytes<WM>(), sB>>>(a);
+            }
             prof->end(sB);
         }
         if (big || h_len[kLenWarp] > 0) launch_warp<0>(g, a, h_len[kLenWarp], dense, prof, st);
@@ -811,6 +829,7 @@ template <int WM, int TIE> int Launcher<WM, TIE>::occ_team = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_team2 = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_hub = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_mid = 1;
+template <int WM, int TIE> int Launcher<WM, TIE>::occ_midh = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::done_device = -1;
 
 typedef void (*round_fn)(lp_graph*, EvalArgs, bool, const int32_t*, Prof*, int);
@@ -1256,6 +1275,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_PUSH_DIV")) g->push_div = std::max(1, atoi(ev));
     if (const char* ev = getenv("LP_REG_EST")) g->reg_est = std::max(0, std::min(32, atoi(ev)));
     if (const char* ev = getenv("LP_MID_MAX")) g->mid_max = std::max(0, std::min(kMidMax, atoi(ev)));
+    if (const char* ev = getenv("LP_MID_HASH")) g->mid_hash = atoi(ev) != 0;
     if (const char* ev = getenv("LP_WARP0_MAXD")) g->warp_maxd[0] = std::max(17, std::min(WarpClass<0>::kMaxDeg, atoi(ev)));
     if (const char* ev = getenv("LP_WARP1_MAXD")) g->warp_maxd[1] = std::max(17, std::min(WarpClass<1>::kMaxDeg, atoi(ev)));
     g->n = n;

@@ -1210,6 +1210,105 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(EvalArgs a) {
     flush_counters(a, dchg, arcs, writes, verts);
 }
 
+// Unit weights: the same rows through a private per-thread hash table in
+// shared memory (128 slots, column layout) -- d probes instead of d^2
+// compares.  An entry is (label, tag, first arc, count); `tag` names the row
+// that wrote it (entries of earlier rows read as empty; the table is wiped
+// every 255 rows), so nothing is cleared per row.  The argmax is kept
+// incrementally (counts only grow; ties as make_cand), the runner-up comes
+// from a pass over the row's touched slots.
+constexpr int kMidHThreads = 64;
+constexpr int kMidHSlots = 128;
+constexpr size_t mid_hash_smem_bytes() {
+    return (size_t)kMidHSlots * kMidHThreads * sizeof(unsigned long long) + (size_t)kMidMax * kMidHThreads;
+}
+
+template <int TIE>
+__global__ void __launch_bounds__(kMidHThreads) k_midh(EvalArgs a) {
+    using A = uint32_t;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(smem_raw) + threadIdx.x;  // [slot * T]
+    uint8_t* touched = smem_raw + (size_t)kMidHSlots * kMidHThreads * sizeof(unsigned long long) + threadIdx.x;
+    for (int h = 0; h < kMidHSlots; ++h) tab[h * kMidHThreads] = 0ull;
+    uint32_t tag = 0;
+    const int32_t cnt = a.r.len[kLenMid];
+    long long dchg = 0, arcs = 0, writes = 0, verts = 0;
+    for (int32_t base = blockIdx.x * blockDim.x; base < cnt; base += gridDim.x * blockDim.x) {
+        const int32_t i = base + threadIdx.x;
+        bool ch = false;
+        int32_t s = -1;
+        if (i < cnt) {
+            s = a.r.mid[i];
+            const int32_t p = __ldg(a.svid + s);
+            const uint32_t beg = __ldg(a.soff + s);
+            const int d = (int)(__ldg(a.soff + s + 1) - beg);
+            const int32_t xv = a.x[p];
+            const int32_t l0v = __ldg(a.L0 + p);
+            const int32_t nd = __ldg(a.ndist + s);
+            arcs += d;
+            ++verts;
+            bool done = false;
+            if (nd & kMajBit) {
+                int cw = 0;
+                for (int k = 0; k < d; ++k) cw += lb_strip(a, a.lbuf[beg + k]) == xv;
+                if (cw + cw > d) {  // strict majority: label unchanged
+                    store_gap<A>(a, s, (A)cw, (A)d);
+                    done = true;
+                }
+            }
+            if (!done) {
+                if (tag == 255u) {  // wipe: tags are about to repeat
+                    for (int h = 0; h < kMidHSlots; ++h) tab[h * kMidHThreads] = 0ull;
+                    tag = 0;
+                }
+                ++tag;
+                const uint32_t vtx = (uint32_t)p;
+                Cand<A> best = none_cand<A>();
+                int nt = 0;
+                for (int k = 0; k < d; ++k) {
+                    const int32_t lab = lb_strip(a, a.lbuf[beg + k]);
+                    uint32_t h = slot_hash(lab, 7);
+                    while (true) {
+                        const unsigned long long e = tab[h * kMidHThreads];
+                        if ((((uint32_t)(e >> 24)) & 0xffu) != tag) {  // another row's entry: empty here
+                            const unsigned long long ne = ((unsigned long long)(uint32_t)lab << 32) |
+                                                          ((unsigned long long)tag << 24) | ((unsigned long long)k << 16) | 1ull;
+                            tab[h * kMidHThreads] = ne;
+                            touched[nt * kMidHThreads] = (uint8_t)h;
+                            ++nt;
+                            const Cand<A> c = make_cand<TIE, A>(1u, lab, (uint32_t)k, a.seed, a.sweep, vtx);
+                            if (better(c, best)) best = c;
+                            break;
+                        }
+                        if ((int32_t)(e >> 32) == lab) {
+                            const unsigned long long ne = e + 1ull;
+                            tab[h * kMidHThreads] = ne;
+                            const Cand<A> c = make_cand<TIE, A>((A)(ne & 0xffffu), lab, (uint32_t)((ne >> 16) & 0xffu),
+                                                                a.seed, a.sweep, vtx);
+                            if (better(c, best)) best = c;
+                            break;
+                        }
+                        h = (h + 1) & (kMidHSlots - 1);
+                    }
+                }
+                // runner-up: the largest count of any other label
+                A w2 = 0;
+                for (int t = 0; t < nt; ++t) {
+                    const unsigned long long e = tab[touched[t * kMidHThreads] * kMidHThreads];
+                    const A c = (A)(e & 0xffffu);
+                    if ((int32_t)(e >> 32) != best.lab && c > w2) w2 = c;
+                }
+                const int32_t nd_new = (best.w + best.w > (A)d) ? kMajBit : 0;
+                if (nd_new != nd) a.ndist[s] = nd_new;
+                store_lead<A>(a, s, best.w, w2);
+                ch = commit_label_known(a, p, best.lab, xv, l0v, dchg, writes);
+            }
+        }
+        if (a.mark) push_changed_small(a, ch, s);
+    }
+    flush_counters(a, dchg, arcs, writes, verts);
+}
+
 // ---------------------------------------------------------------------------
 // shared-memory tally tables
 // ---------------------------------------------------------------------------

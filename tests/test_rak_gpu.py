@@ -261,6 +261,7 @@ def test_malformed_csr_rejected_on_upload(gpu):
     {"LP_CAP_ROUTE": "1", "LP_WARP0_MAXD": "512"},  # capacity / degree routing
     {"LP_REG_EST": "32", "LP_PUSH_DIV": "50"},    # register tables up to 32 labels, pulled sweep marks
     {"LP_MID_MAX": "0"},                          # no thread-per-row mid-degree kernel
+    {"LP_MID_HASH": "0"},                         # mid-degree rows by O(d^2) compares
 ])
 def test_engine_policies_keep_exactness(gpu, oracle, env, monkeypatch):
     """Every scheduling policy of the engine (chosen per handle from the
