@@ -18,7 +18,8 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblabelprop_cuda.so")
+# (LP_LIB_PATH: an alternative build of the same library, for A/B timing)
+LIB_PATH = os.environ.get("LP_LIB_PATH") or os.path.join(HERE, "liblabelprop_cuda.so")
 CSRC = os.path.join(HERE, "csrc")
 
 LP_OK = 0

@@ -120,6 +120,8 @@ struct Plan {
     unsigned long long* swsum = nullptr;  // [S] row weight totals (fixed-point mode)
     int32_t* ndist = nullptr;        // [S]
     int32_t* lbuf = nullptr;         // [m_active] phase-1 gathered labels
+    int32_t* hb_lab = nullptr;       // [m_active] hub rows' labels bucketed by partition (k_hub_bucket)
+    uint32_t* hb_pos = nullptr;      // [m_active] ... and their arc positions
     int64_t S = 0;
     int64_t m_active = 0;
     int64_t flags_bs = -1;           // batch size the snbr flags were computed for
@@ -167,6 +169,8 @@ struct lp_graph {
     int32_t* mq[2] = {nullptr, nullptr};  // mark queues (alternate per round)
     int32_t* mq_len = nullptr;  // their lengths [2]
     uint32_t* mbits = nullptr;  // marked-vertex bitmap (all zero between passes)
+    int2* hb_off = nullptr;     // hub partition buckets (per item cb + q)
+    bool hub_bucket = true;     // LP_HUB_BUCKET=0: partition blocks re-read the whole row
     int32_t* slots = nullptr;   // SLPA memories [n x T]
     size_t slots_cap = 0;
     // COPRA label sets (sweep-start and working), [n x K] rows
@@ -811,6 +815,7 @@ template <int WM, int TIE> struct Launcher {
         if (big || h_len[kLenHub] > 0) {
             a.bin = kKHub;
             prof->begin(sC, kKHub);
+            if (a.hb_off) k_hub_bucket<<<sms * 2, 1024, 0, sC>>>(a);
             const int grid = dense ? sms * occ_hub : grid_for(h_len[kLenHub], 1, sms * occ_hub);
             k_team<WM, TIE, kHubThreads, kHubBits, true>
                 <<<grid, kHubThreads, team_smem_bytes<WM, kHubBits>(), sC>>>(a, kLenHub);
@@ -864,6 +869,8 @@ static void free_plan(Plan& P) {
     dfree(P.swsum);
     dfree(P.ndist);
     dfree(P.lbuf);
+    dfree(P.hb_lab);
+    dfree(P.hb_pos);
     dfree(P.vorder);
     dfree(P.wave_len);
     dfree(P.dslot);
@@ -904,6 +911,7 @@ static void destroy_graph(lp_graph* g) {
     dfree(g->mq[1]);
     dfree(g->mq_len);
     dfree(g->mbits);
+    dfree(g->hb_off);
     dfree(g->slots);
     for (int i = 0; i < 2; ++i) {
         dfree(g->clabs[i]);
@@ -1132,6 +1140,8 @@ static int build_plan(lp_graph* g, int kind, const int64_t* order_host, uint32_t
     P.m_active = m_active;
     LP_CK(dalloc(&P.snbr, P.m_active, &bytes));
     LP_CK(dalloc(&P.lbuf, P.m_active, &bytes));
+    LP_CK(dalloc(&P.hb_lab, P.m_active, &bytes));
+    LP_CK(dalloc(&P.hb_pos, P.m_active, &bytes));
     if (g->w) LP_CK(dalloc(&P.sw, P.m_active, &bytes));
     if (index)
         k_plan_rows<<<g->num_sms * 16, 256, 0, st>>>(P.svid, g->off, g->nbr, g->w, P.soff, P.snbr, P.sw, P.S, 1);
@@ -1220,6 +1230,7 @@ static cudaError_t alloc_routes(lp_graph* g) {
     if ((e = dalloc(&r.hub, g->cap_items, &g->bytes))) return e;
     if ((e = dalloc(&r.len, kLenCount, &g->bytes))) return e;
     if ((e = dalloc(&r.cand, g->cap_items, &g->bytes))) return e;
+    if ((e = dalloc(&g->hb_off, g->cap_items, &g->bytes))) return e;
     if ((e = dalloc(&r.cand_done, g->cap_items, &g->bytes))) return e;
     if ((e = dalloc(&r.gcount, g->cap_items, &g->bytes))) return e;
     if ((e = dalloc(&r.gkeys, gpool, &g->bytes))) return e;
@@ -1276,6 +1287,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_REG_EST")) g->reg_est = std::max(0, std::min(32, atoi(ev)));
     if (const char* ev = getenv("LP_MID_MAX")) g->mid_max = std::max(0, std::min(kMidMax, atoi(ev)));
     if (const char* ev = getenv("LP_MID_HASH")) g->mid_hash = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_HUB_BUCKET")) g->hub_bucket = atoi(ev) != 0;
     if (const char* ev = getenv("LP_WARP0_MAXD")) g->warp_maxd[0] = std::max(17, std::min(WarpClass<0>::kMaxDeg, atoi(ev)));
     if (const char* ev = getenv("LP_WARP1_MAXD")) g->warp_maxd[1] = std::max(17, std::min(WarpClass<1>::kMaxDeg, atoi(ev)));
     g->n = n;
@@ -1752,6 +1764,12 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.cap_route = g->cap_route;
     a.id_single = 0;
     a.mbits = g->mbits;
+    // (unit weights only: with weights the bucketed arcs' weight loads are
+    // indirect, measured slower on R-MAT-22 float32 weights)
+    const bool buckets = g->hub_bucket && g->wmode == kUnit;
+    a.hb_lab = buckets ? P.hb_lab : nullptr;
+    a.hb_pos = buckets ? P.hb_pos : nullptr;
+    a.hb_off = buckets ? g->hb_off : nullptr;
     a.warp_maxd[0] = g->warp_maxd[0];
     a.warp_maxd[1] = g->warp_maxd[1];
     a.reg_est = g->reg_est;
@@ -1961,6 +1979,12 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     a.cap_route = g->cap_route;
     a.id_single = 0;
     a.mbits = g->mbits;
+    // (unit weights only: with weights the bucketed arcs' weight loads are
+    // indirect, measured slower on R-MAT-22 float32 weights)
+    const bool buckets = g->hub_bucket && g->wmode == kUnit;
+    a.hb_lab = buckets ? P.hb_lab : nullptr;
+    a.hb_pos = buckets ? P.hb_pos : nullptr;
+    a.hb_off = buckets ? g->hb_off : nullptr;
     a.warp_maxd[0] = g->warp_maxd[0];
     a.warp_maxd[1] = g->warp_maxd[1];
     a.reg_est = g->reg_est;

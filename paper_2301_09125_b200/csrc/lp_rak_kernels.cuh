@@ -148,6 +148,12 @@ struct EvalArgs {
     int32_t warp_maxd[2];  // longest row routed to warp class 0 / 1 (longer rows go to the teams)
     int32_t reg_est;       // rows estimated to hold more labels skip the warp register table
     int32_t mid_max;       // rows of kSmallMax < d <= mid_max go to k_mid (0 = off)
+    // hub rows split into P > 1 label partitions: k_hub_bucket reorders each
+    // row's labels (and arc positions) by partition, so a partition block reads
+    // its own bucket instead of the whole row (null = off)
+    int32_t* hb_lab;
+    uint32_t* hb_pos;
+    int2* hb_off;  // per partition item (cb + q): (bucket start, length); length -1 = not bucketed
 };
 
 // First sweep from labels = vertex ids (rak.py:168): a neighbour that has not
@@ -192,6 +198,9 @@ __host__ __device__ __forceinline__ int32_t nd_count(int32_t v) { return v & (kM
     } while (0)
 #endif
 
+#ifndef LP_TEAM_U
+#define LP_TEAM_U 2
+#endif
 constexpr int kSmallMax = 16;     // thread-per-vertex bound (degree)
 #ifndef LP_WARP_REG_EST
 #define LP_WARP_REG_EST 8  // rows estimated to hold more labels skip the warp register table (LP_REG_EST;
@@ -1309,6 +1318,65 @@ __global__ void __launch_bounds__(kMidHThreads) k_midh(EvalArgs a) {
     flush_counters(a, dchg, arcs, writes, verts);
 }
 
+// Hub rows routed as P > 1 label partitions (one k_team block each): reorder
+// the row's labels by partition once -- a counting scatter with
+// __match_any_sync-folded shared counters -- so that each partition block
+// reads its own bucket (1/P of the row) instead of the whole row.  Bucket
+// order is arbitrary; hb_pos keeps each label's arc position (scan-order ties).
+constexpr int kHubBucketMaxP = 64;
+__global__ void __launch_bounds__(1024) k_hub_bucket(EvalArgs a) {
+    __shared__ int32_t cntp[kHubBucketMaxP];
+    __shared__ int32_t curp[kHubBucketMaxP];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int32_t cnt = a.r.len[kLenHub];
+    for (int32_t it = blockIdx.x; it < cnt; it += gridDim.x) {
+        const Item item = a.r.hub[it];
+        if (item.R != 1 || item.P <= 1 || item.q != 0) continue;  // (block-uniform)
+        const uint32_t P = (uint32_t)item.P;
+        if (P > (uint32_t)kHubBucketMaxP) {
+            for (int q = tid; q < item.P; q += blockDim.x) a.hb_off[item.cb + q] = make_int2(0, -1);
+            continue;
+        }
+        const int32_t s = item.s;
+        const uint32_t beg = __ldg(a.soff + s);
+        const int d = (int)(__ldg(a.soff + s + 1) - beg);
+        if (tid < kHubBucketMaxP) cntp[tid] = 0;
+        __syncthreads();
+        for (int base = 0; base < d; base += blockDim.x) {
+            const int k = base + tid;
+            const uint32_t part = k < d ? part_of(lb_strip(a, a.lbuf[beg + k]), P) : 0xffffffffu;
+            const uint32_t grp = __match_any_sync(0xffffffffu, part);
+            if (part != 0xffffffffu && lane == __ffs(grp) - 1) atomicAdd(&cntp[part], __popc(grp));
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int32_t o = 0;
+            for (uint32_t q = 0; q < P; ++q) {
+                a.hb_off[item.cb + q] = make_int2((int32_t)beg + o, cntp[q]);
+                curp[q] = o;
+                o += cntp[q];
+            }
+        }
+        __syncthreads();
+        for (int base = 0; base < d; base += blockDim.x) {
+            const int k = base + tid;
+            const int32_t lab = k < d ? lb_strip(a, a.lbuf[beg + k]) : 0;
+            const uint32_t part = k < d ? part_of(lab, P) : 0xffffffffu;
+            const uint32_t grp = __match_any_sync(0xffffffffu, part);
+            const int leader = __ffs(grp) - 1;
+            int b0 = 0;
+            if (part != 0xffffffffu && lane == leader) b0 = atomicAdd(&curp[part], __popc(grp));
+            b0 = __shfl_sync(0xffffffffu, b0, leader);
+            if (part != 0xffffffffu) {
+                const int o = b0 + __popc(grp & lanemask_lt());
+                a.hb_lab[beg + o] = lab;
+                a.hb_pos[beg + o] = (uint32_t)k;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------------------
 // shared-memory tally tables
 // ---------------------------------------------------------------------------
@@ -2115,7 +2183,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
     constexpr int HB = Tab::HB;
     constexpr int CAP = Tab::CAP;
     constexpr int NW = NT / 32;
-    constexpr int U = 2;
+    constexpr int U = LP_TEAM_U;  // 32-arc chunks in flight per warp
     constexpr int STACK = 40;
     constexpr int GHB = 1 << kGlobalBits;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -2164,9 +2232,12 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
     // the work stack (preloaded by the caller).  Sub-splits on overflow.
     // `single`: one whole-row pass (no first position needed unless tied).
     auto row_best = [&](const uint32_t beg, const int d, const uint32_t vtx, bool single,
-                        bool agg, int& distinct) -> Best<A> {
+                        bool agg, int& distinct, int2 bk = make_int2(0, -1), uint32_t topP = 1) -> Best<A> {
         Best<A> overall = none_best<A>();
         distinct = 0;
+        // bucketed: the arcs are the partition's bucket hb_lab/hb_pos[bk.x, bk.x + bk.y)
+        const bool bucketed = bk.y >= 0 && !two;
+        const int dd = bucketed ? bk.y : d;
         while (true) {
             const int sp = s_sp;
             if (sp == 0) break;
@@ -2178,7 +2249,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 s_full = 0;
             }
             __syncthreads();
-            for (int base = warp * 32 * U; base < d; base += NT * U) {
+            for (int base = warp * 32 * U; base < dd; base += NT * U) {
                 int32_t labv[U];
                 A wv[U];
 #pragma unroll
@@ -2186,7 +2257,13 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                     const int k = base + c * 32 + lane;
                     int32_t lab = kEmpty;
                     A w = A(0);
-                    if (k < d) {
+                    if (bucketed) {
+                        if (k < dd) {
+                            lab = a.hb_lab[bk.x + k];
+                            w = WM == kUnit ? A(1) : arc_weight<WM>(a, beg + a.hb_pos[bk.x + k]);
+                            if (parts > topP && part_of(lab, parts) != want) lab = kEmpty;
+                        }
+                    } else if (k < d) {
                         lab = a.lbuf[beg + k];
                         w = arc_weight<WM>(a, beg + k);
                         if (two && (lab & kSingle)) lab = kEmpty;  // (two passes: looked up below)
@@ -2260,7 +2337,18 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 // earliest arc (scan order) whose label carries the pass maximum
                 if (tid == 0) s_first = ~0ull;
                 __syncthreads();
-                for (int base = warp * 32; base < d; base += NT) {
+                if (bucketed) {
+                    // (bucket order is not scan order: every hit proposes its position)
+                    for (int k = tid; k < dd; k += NT) {
+                        const int32_t lab = a.hb_lab[bk.x + k];
+                        if (parts <= topP || part_of(lab, parts) == want) {
+                            const int h = tab->t.find(lab);
+                            if (h >= 0 && tab->t.weight(h) == b.w && sec_of<TIE>(lab, a.seed, a.sweep, vtx) == b.sec)
+                                atomicMin(&s_first, ((unsigned long long)a.hb_pos[bk.x + k] << 32) | (uint32_t)lab);
+                        }
+                    }
+                }
+                for (int base = warp * 32; base < d && !bucketed; base += NT) {
                     const unsigned long long seen = __shfl_sync(0xffffffffu, *(volatile unsigned long long*)&s_first, 0);
                     if ((unsigned long long)base > (seen >> 32)) break;  // an earlier hit exists
                     const int k = base + lane;
@@ -2365,7 +2453,9 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 s_fb = 0;
             }
             __syncthreads();
-            best = row_best(beg, d, vtx, item.P == 1, agg, distinct);
+            int2 bk = make_int2(0, -1);
+            if (item.P > 1 && a.hb_off) bk = a.hb_off[item.cb + item.q];
+            best = row_best(beg, d, vtx, item.P == 1, agg, distinct, bk, (uint32_t)item.P);
             if (item.P == 1 && two && tid == 0 && s_single > 0) {
                 if (best.w < A(2))
                     s_fb = 1;
