@@ -1164,7 +1164,7 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(EvalArgs a) {
             const int32_t nd = __ldg(a.ndist + s);
             A total = A(0);
             for (int k = 0; k < d; ++k) {
-                lab[k * kMidThreads] = lb_strip(a, a.lbuf[beg + k]);
+                lab[k * kMidThreads] = lb_strip(a, __ldg(a.lbuf + beg + k));
                 const A w = arc_weight<WM>(a, beg + k);
                 if (WM != kUnit) wv[k * kMidThreads] = w;
                 total += w;
@@ -1259,7 +1259,7 @@ __global__ void __launch_bounds__(kMidHThreads) k_midh(EvalArgs a) {
             bool done = false;
             if (nd & kMajBit) {
                 int cw = 0;
-                for (int k = 0; k < d; ++k) cw += lb_strip(a, a.lbuf[beg + k]) == xv;
+                for (int k = 0; k < d; ++k) cw += lb_strip(a, __ldg(a.lbuf + beg + k)) == xv;
                 if (cw + cw > d) {  // strict majority: label unchanged
                     store_gap<A>(a, s, (A)cw, (A)d);
                     done = true;
@@ -1274,8 +1274,20 @@ __global__ void __launch_bounds__(kMidHThreads) k_midh(EvalArgs a) {
                 const uint32_t vtx = (uint32_t)p;
                 Cand<A> best = none_cand<A>();
                 int nt = 0;
+                // (labels in batches of 8 registers: the row's loads overlap instead of
+                // one dependent L2 round trip per arc)
+                constexpr int kB = 8;
+                int32_t lv[kB];
                 for (int k = 0; k < d; ++k) {
-                    const int32_t lab = lb_strip(a, a.lbuf[beg + k]);
+                    if ((k & (kB - 1)) == 0) {
+#pragma unroll
+                        for (int j = 0; j < kB; ++j) lv[j] = k + j < d ? __ldg(a.lbuf + beg + k + j) : 0;
+                    }
+                    int32_t lab = lv[0];
+#pragma unroll
+                    for (int j = 1; j < kB; ++j)
+                        if ((k & (kB - 1)) == j) lab = lv[j];
+                    lab = lb_strip(a, lab);
                     uint32_t h = slot_hash(lab, 7);
                     while (true) {
                         const unsigned long long e = tab[h * kMidHThreads];
