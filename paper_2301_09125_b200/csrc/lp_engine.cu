@@ -170,7 +170,9 @@ struct lp_graph {
     int32_t* mq_len = nullptr;  // their lengths [2]
     uint32_t* mbits = nullptr;  // marked-vertex bitmap (all zero between passes)
     int2* hb_off = nullptr;     // hub partition buckets (per item cb + q)
-    bool hub_bucket = true;     // LP_HUB_BUCKET=0: partition blocks re-read the whole row
+    bool hub_bucket = false;    // LP_HUB_BUCKET=1: bucket hub partitions (measured: no gain once hubs
+                                // use the singleton two-pass tally)
+    int first_est_min = 256, first_est_div = 4;  // LP_FIRST_EST_MIN / LP_FIRST_EST_DIV (tuned on R-MAT-22)
     int32_t* slots = nullptr;   // SLPA memories [n x T]
     size_t slots_cap = 0;
     // COPRA label sets (sweep-start and working), [n x K] rows
@@ -1288,6 +1290,8 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_MID_MAX")) g->mid_max = std::max(0, std::min(kMidMax, atoi(ev)));
     if (const char* ev = getenv("LP_MID_HASH")) g->mid_hash = atoi(ev) != 0;
     if (const char* ev = getenv("LP_HUB_BUCKET")) g->hub_bucket = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_FIRST_EST_MIN")) g->first_est_min = std::max(16, atoi(ev));
+    if (const char* ev = getenv("LP_FIRST_EST_DIV")) g->first_est_div = std::max(1, atoi(ev));
     if (const char* ev = getenv("LP_WARP0_MAXD")) g->warp_maxd[0] = std::max(17, std::min(WarpClass<0>::kMaxDeg, atoi(ev)));
     if (const char* ev = getenv("LP_WARP1_MAXD")) g->warp_maxd[1] = std::max(17, std::min(WarpClass<1>::kMaxDeg, atoi(ev)));
     g->n = n;
@@ -1764,6 +1768,8 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.cap_route = g->cap_route;
     a.id_single = 0;
     a.mbits = g->mbits;
+    a.first_est_min = g->first_est_min;
+    a.first_est_div = g->first_est_div;
     // (unit weights only: with weights the bucketed arcs' weight loads are
     // indirect, measured slower on R-MAT-22 float32 weights)
     const bool buckets = g->hub_bucket && g->wmode == kUnit;
@@ -1979,6 +1985,8 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     a.cap_route = g->cap_route;
     a.id_single = 0;
     a.mbits = g->mbits;
+    a.first_est_min = g->first_est_min;
+    a.first_est_div = g->first_est_div;
     // (unit weights only: with weights the bucketed arcs' weight loads are
     // indirect, measured slower on R-MAT-22 float32 weights)
     const bool buckets = g->hub_bucket && g->wmode == kUnit;

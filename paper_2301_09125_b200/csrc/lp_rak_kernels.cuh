@@ -148,6 +148,8 @@ struct EvalArgs {
     int32_t warp_maxd[2];  // longest row routed to warp class 0 / 1 (longer rows go to the teams)
     int32_t reg_est;       // rows estimated to hold more labels skip the warp register table
     int32_t mid_max;       // rows of kSmallMax < d <= mid_max go to k_mid (0 = off)
+    int32_t first_est_min, first_est_div;  // first round of a singleton sweep: rows longer than
+                                           // first_est_min estimate d / first_est_div labels
     // hub rows split into P > 1 label partitions: k_hub_bucket reorders each
     // row's labels (and arc positions) by partition, so a partition block reads
     // its own bucket instead of the whole row (null = off)
@@ -805,7 +807,7 @@ __device__ __forceinline__ void route_append(const EvalArgs& a, int cls, int32_t
         int gt = -1;
         // slices when the labels are few (a small L2 table); with many labels the
         // smem label partitions are faster than global-table atomics (measured)
-        if (d > kSliceArcs * 2 && est <= kSliceEst) {
+        if (d > kSliceArcs * 2 && est <= kSliceEst && !a.id_single) {
             gt = atomicAdd(a.r.len + kGtabCursor, 1 << gbits);
             if ((int64_t)gt + (1 << gbits) > a.r.gcap) gt = -1;  // pool exhausted: partitions
         }
@@ -918,7 +920,9 @@ __global__ void __launch_bounds__(256) k_first_round(EvalArgs a, int32_t S) {
             const int32_t lab = (int32_t)(__ldg(a.snbr + beg) >> 2);
             arcs += d;
             ++verts;
-            a.ndist[s] = d | (2 > d ? kMajBit : 0);
+            // (the next round of a singleton first sweep tables only the evaluated
+            // labels, a few percent of a long row: a lower estimate for long rows)
+            a.ndist[s] = (a.id_single && d > a.first_est_min ? d / a.first_est_div : d) | (2 > d ? kMajBit : 0);
             store_lead<uint32_t>(a, s, 1u, d > 1 ? 1u : 0u);
             ch = commit_label_known(a, p, lab, p, p, dchg, writes);
         }
@@ -1372,8 +1376,8 @@ __global__ void __launch_bounds__(1024) k_hub_bucket(EvalArgs a) {
         __syncthreads();
         for (int base = 0; base < d; base += blockDim.x) {
             const int k = base + tid;
-            const int32_t lab = k < d ? lb_strip(a, a.lbuf[beg + k]) : 0;
-            const uint32_t part = k < d ? part_of(lab, P) : 0xffffffffu;
+            const int32_t lab = k < d ? a.lbuf[beg + k] : 0;  // (kSingle flags kept)
+            const uint32_t part = k < d ? part_of(lb_strip(a, lab), P) : 0xffffffffu;
             const uint32_t grp = __match_any_sync(0xffffffffu, part);
             const int leader = __ffs(grp) - 1;
             int b0 = 0;
@@ -2219,9 +2223,10 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    // kSingle two-pass tally on the 8/16-warp teams; the hub kernel inserts
-    // every label (its rows are sliced / partitioned by the true label count)
-    const bool two = a.id_single && NT < 1024;
+    // kSingle two-pass tally (first sweep from ids; hub rows are then routed as
+    // label partitions, never as slices: a slice cannot look labels up after
+    // the other slices' inserts)
+    const bool two = a.id_single;
     for (int h = tid; h < HB; h += NT) tab->t.init(h);
     const Item* items = which == kLenHub ? a.r.hub : (which == kLenTeam2 ? a.r.team2 : a.r.team);
     const int cursor = which == kLenHub ? kHubCursor : (which == kLenTeam2 ? kTeam2Cursor : kTeamCursor);
@@ -2248,7 +2253,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
         Best<A> overall = none_best<A>();
         distinct = 0;
         // bucketed: the arcs are the partition's bucket hb_lab/hb_pos[bk.x, bk.x + bk.y)
-        const bool bucketed = bk.y >= 0 && !two;
+        const bool bucketed = bk.y >= 0;
         const int dd = bucketed ? bk.y : d;
         while (true) {
             const int sp = s_sp;
@@ -2273,7 +2278,11 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                         if (k < dd) {
                             lab = a.hb_lab[bk.x + k];
                             w = WM == kUnit ? A(1) : arc_weight<WM>(a, beg + a.hb_pos[bk.x + k]);
-                            if (parts > topP && part_of(lab, parts) != want) lab = kEmpty;
+                            if (two && (lab & kSingle)) lab = kEmpty;  // (looked up below)
+                            else {
+                                lab = lb_strip(a, lab);
+                                if (parts > topP && part_of(lab, parts) != want) lab = kEmpty;
+                            }
                         }
                     } else if (k < d) {
                         lab = a.lbuf[beg + k];
@@ -2323,7 +2332,20 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
             if (two) {
                 // pass 2: flagged labels of this partition are looked up only
                 int sg = 0;
-                for (int base = warp * 32; base < d; base += NT) {
+                for (int k = tid; k < dd && bucketed; k += NT) {
+                    int32_t lab = a.hb_lab[bk.x + k];
+                    if (lab & kSingle) {
+                        lab = lb_strip(a, lab);
+                        if (parts <= topP || part_of(lab, parts) == want) {
+                            const int h = tab->t.find(lab);
+                            if (h >= 0)
+                                tab->t.add_at(h, A(1));
+                            else
+                                ++sg;
+                        }
+                    }
+                }
+                for (int base = warp * 32; base < d && !bucketed; base += NT) {
                     const int k = base + lane;
                     if (k < d) {
                         int32_t lab = a.lbuf[beg + k];
@@ -2352,7 +2374,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 if (bucketed) {
                     // (bucket order is not scan order: every hit proposes its position)
                     for (int k = tid; k < dd; k += NT) {
-                        const int32_t lab = a.hb_lab[bk.x + k];
+                        const int32_t lab = lb_strip(a, a.hb_lab[bk.x + k]);
                         if (parts <= topP || part_of(lab, parts) == want) {
                             const int h = tab->t.find(lab);
                             if (h >= 0 && tab->t.weight(h) == b.w && sec_of<TIE>(lab, a.seed, a.sweep, vtx) == b.sec)

@@ -262,7 +262,7 @@ def test_malformed_csr_rejected_on_upload(gpu):
     {"LP_REG_EST": "32", "LP_PUSH_DIV": "50"},    # register tables up to 32 labels, pulled sweep marks
     {"LP_MID_MAX": "0"},                          # no thread-per-row mid-degree kernel
     {"LP_MID_HASH": "0"},                         # mid-degree rows by O(d^2) compares
-    {"LP_HUB_BUCKET": "0"},                       # hub partitions re-read the whole row
+    {"LP_HUB_BUCKET": "1", "LP_FIRST_EST_MIN": "16", "LP_FIRST_EST_DIV": "64"},  # hub buckets, low estimates
 ])
 def test_engine_policies_keep_exactness(gpu, oracle, env, monkeypatch):
     """Every scheduling policy of the engine (chosen per handle from the
