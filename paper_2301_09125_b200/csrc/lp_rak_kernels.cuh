@@ -1754,7 +1754,11 @@ template <int WM, int WC> struct WarpTable {
     static constexpr int kCap = (1 << WarpClass<WC>::kBits) / 4 * 3;  // touched entries before a spill
     STable<WM, WarpClass<WC>::kBits> t;
     uint16_t touched[kCap + 32];
+    uint32_t sig[32];  // key signature (kSingle two-pass lookups); zero between rows
 };
+
+// 10-bit signature hash of a label (independent of slot_hash)
+__device__ __forceinline__ uint32_t sig_hash(int32_t lab) { return ((uint32_t)lab * 0x85EBCA77u) >> 22; }
 
 // Insert one 32-arc chunk into a shared table.  agg: fold equal labels with
 // __match_any_sync first (rows with few distinct labels); otherwise every lane
@@ -1809,6 +1813,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
     const int wib = threadIdx.x >> 5;
     WT* tab = reinterpret_cast<WT*>(smem_raw) + wib;
     for (int h = lane; h < HB; h += 32) tab->t.init(h);
+    tab->sig[lane] = 0u;
     __syncwarp();
 
     const int32_t cnt = a.r.len[WarpClass<WC>::kList];
@@ -1937,7 +1942,18 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
             bool overflow = false;
             int singles = 0;  // (two passes) flagged labels absent from the table, this lane
             constexpr int npass = TWO ? 2 : 1;
-            for (int pass = 0; pass < npass && !overflow; ++pass)
+            uint32_t mysig = 0;  // (two passes, hashed) lane's word of the table keys' 1024-bit signature
+            for (int pass = 0; pass < npass && !overflow; ++pass) {
+            if (TWO && pass == 1 && hashed) {
+                // a flagged label whose signature bit is clear is absent: no probe
+                for (int t = lane; t < ntouched; t += 32) {
+                    const uint32_t h2 = sig_hash(tab->t.key(tab->touched[t]));
+                    atomicOr(&tab->sig[h2 >> 5], 1u << (h2 & 31u));
+                }
+                __syncwarp();
+                mysig = tab->sig[lane];
+                tab->sig[lane] = 0u;
+            }
             for (int base = 0; base < d && !overflow; base += 32 * U) {
                 int32_t labv[U];
                 A wv[U];
@@ -1972,11 +1988,15 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                                     hit |= flag && lab == key;
                                 }
                             }
-                        } else if (flag) {
-                            const int h = tab->t.find(lab);
-                            if (h >= 0) {
-                                tab->t.add_at(h, A(1));
-                                hit = true;
+                        } else {
+                            const uint32_t h2 = sig_hash(lab);
+                            const uint32_t word = __shfl_sync(0xffffffffu, mysig, (int)(h2 >> 5));
+                            if (flag && ((word >> (h2 & 31u)) & 1u)) {
+                                const int h = tab->t.find(lab);
+                                if (h >= 0) {
+                                    tab->t.add_at(h, A(1));
+                                    hit = true;
+                                }
                             }
                         }
                         singles += (flag && !hit) ? 1 : 0;
@@ -2042,6 +2062,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                         break;
                     }
                 }
+            }
             }
             if (overflow) {
                 if (lane == 0) LP_STAT(a, 4);
