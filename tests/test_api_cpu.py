@@ -172,3 +172,27 @@ def test_copra_params_validation():
             lp.CopraParams(**bad)
     p = lp.CopraParams()
     assert (p.tolerance, p.max_labels, p.max_iterations, p.workers, p.seed) == (0.01, 8, 100, 1, 1)
+
+
+def test_sweep_spec_and_csv_schema():
+    """sweep.py keeps the reference harness's contract (labelprop/sweep.py:26-102):
+    grid validation, combos per graph, the 11-column CSV row."""
+    from paper_2301_09125_b200 import sweep
+
+    assert lp.CSV_HEADER.split(",") == ["graph", "algorithm", "mode", "tolerance", "max_labels", "memory_size",
+                                         "workers", "seed", "iterations", "elapsed_ms", "modularity"]
+    with pytest.raises(ValueError):
+        lp.SweepSpec("louvain")
+    with pytest.raises(ValueError):
+        lp.SweepSpec("rak", tolerances=())
+    with pytest.raises(ValueError):
+        lp.SweepSpec("rak", repetitions=0)
+    assert lp.SweepSpec("rak", tolerances=(0.1, 0.05), workers=(1, 2), repetitions=3).combos_per_graph() == 24
+    assert lp.SweepSpec("copra", tolerances=(0.01,), max_labels=(1, 4)).combos_per_graph() == 2
+    assert lp.SweepSpec("slpa", memory_sizes=(4, 8), batches=(0, 1)).combos_per_graph() == 8
+    pts = list(sweep.combos(lp.SweepSpec("copra", tolerances=(0.01,), max_labels=(1, 4))))
+    assert [p["max_labels"] for p in pts] == [1, 4] and all(p["mode"] == "" for p in pts)
+    r = lp.RunRecord("g", "copra", "", 0.01, 4, None, 1, 7, 3, 1.5, 0.25, batches=1, edges_scanned=3_000_000)
+    assert r.csv_row() == "g,copra,,0.01,4,,1,7,3,1.500,0.250000000"
+    assert r.csv_row(extended=True).endswith(",1,3000000,2.0000")
+    assert len(r.csv_row(extended=True).split(",")) == len(sweep.CSV_HEADER_EXTENDED.split(","))

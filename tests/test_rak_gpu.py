@@ -316,3 +316,19 @@ def test_gpu_graph_builders_match_host(gpu, monkeypatch):
         _lib.check(_lib.lib().lp_csr_build_undirected_gpu(10, 1, np.array([0]), np.array([11]), -1,
                                                           np.empty(11, np.int64), np.empty(12, np.int64), 12,
                                                           C.byref(m)))
+
+
+def test_sweep_runs_the_cuda_detectors(gpu):
+    """run_sweep (sweep.py, the reference harness's interface) streams one record
+    per grid point with the detectors' own results."""
+    g = lp.planted_partition(3000, 30, seed=4)
+    spec = lp.SweepSpec("rak", tolerances=(0.05,), modes=("strict",), batches=(0, 1), repetitions=2, seed=3)
+    recs = list(lp.run_sweep(spec, [("planted", g)]))
+    assert len(recs) == spec.combos_per_graph() == 4
+    for r in recs:
+        want = lp.rak_detect(g, lp.RakParams(tolerance=0.05, strict=True, seed=r.seed, batches=r.batches))
+        assert r.iterations == want.iterations and abs(r.modularity - want.modularity) < 1e-12
+        assert r.edges_scanned == g.edge_count * r.iterations and r.gteps > 0
+    crec = list(lp.run_sweep(lp.SweepSpec("copra", tolerances=(0.01,), max_labels=(2,)), [("planted", g)]))
+    srec = list(lp.run_sweep(lp.SweepSpec("slpa", memory_sizes=(8,), modes=("strict",)), [("planted", g)]))
+    assert len(crec) == 1 and len(srec) == 1 and crec[0].iterations >= 1 and srec[0].iterations >= 1
