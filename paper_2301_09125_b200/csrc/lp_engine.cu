@@ -223,6 +223,7 @@ struct lp_graph {
     int cap_route = 0;      // LP_CAP_ROUTE=1: route rows by table capacity >= degree (measured: no gain)
     bool id_single = true;  // LP_ID_SINGLE=0: no singleton labels in the first sweep (see kSingle)
     int push_div = 3;
+    bool id_single_random = true;  // LP_ID_SINGLE_RANDOM=0: no singleton labels with random ties
     int reg_est = LP_WARP_REG_EST;  // LP_REG_EST
     int mid_max = kMidMax;          // LP_MID_MAX: thread-per-row k_mid up to this degree (0 = off)
     bool mid_hash = true;           // LP_MID_HASH=0: unit-weight mid rows by O(d^2) compares (k_mid)      // sweep boundary: push marks from the changed rows when <= 1/push_div of the
@@ -1286,6 +1287,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_CAP_ROUTE")) g->cap_route = atoi(ev) != 0;
     if (const char* ev = getenv("LP_ID_SINGLE")) g->id_single = atoi(ev) != 0;
     if (const char* ev = getenv("LP_PUSH_DIV")) g->push_div = std::max(1, atoi(ev));
+    if (const char* ev = getenv("LP_ID_SINGLE_RANDOM")) g->id_single_random = atoi(ev) != 0;
     if (const char* ev = getenv("LP_REG_EST")) g->reg_est = std::max(0, std::min(32, atoi(ev)));
     if (const char* ev = getenv("LP_MID_MAX")) g->mid_max = std::max(0, std::min(kMidMax, atoi(ev)));
     if (const char* ev = getenv("LP_MID_HASH")) g->mid_hash = atoi(ev) != 0;
@@ -1463,7 +1465,7 @@ static void bits_to_queue(lp_graph* g, const EvalArgs& a) {
 }
 
 static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round, int alg, Prof* prof, int* rounds,
-                       int64_t* gathered, bool first_ids = false, bool carry = false) {
+                       int64_t* gathered, bool first_ids = false, bool carry = false, bool first_random = false) {
     const Plan& P = g->plan();
     cudaStream_t st = g->stream;
     LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
@@ -1593,6 +1595,10 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
                 if (g->wmode == kFixed) {
                     k_first_round_wbig<<<g->num_sms * 4, 256, 0, st>>>(a, (int32_t)P.S);
                     k_first_round_w<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S);
+                }
+                else if (first_random) {
+                    k_first_round_rbig<<<g->num_sms * 4, 256, 0, st>>>(a, (int32_t)P.S);
+                    k_first_round_r<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S);
                 }
                 else
                     k_first_round<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S);
@@ -1830,12 +1836,14 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         // weights and scan-first / min-label ties on duplicate-free sorted rows
         const bool first_ids = it == 1 && !labels_init && (g->wmode == kUnit || g->wmode == kFixed) && g->rows_sorted &&
                                (o->tie == kScanFirst || o->tie == kMinLabel) && g->first_round_shortcut;
+        // random ties, unit weights: the first round is the row's largest tie hash
+        const bool first_random = it == 1 && !labels_init && g->wmode == kUnit && g->rows_sorted &&
+                                  o->tie == kRandom && g->first_round_shortcut;
         // first sweep from labels = ids: unevaluated neighbours carry singleton labels
-        // (not with random ties: measured slower -- the first round then has no
-        // shortcut and every row takes the all-weight-1 path)
         a.id_single = (it == 1 && !labels_init && g->wmode == kUnit && g->rows_sorted && n < (1 << 30) &&
-                       o->tie != kRandom && g->id_single) ? 1 : 0;
-        if (int rc = solve_sweep(g, a, cross, run_round, kGatherRak, &prof, &rounds, &gathered, first_ids, carry))
+                       (o->tie != kRandom || g->id_single_random) && g->id_single) ? 1 : 0;
+        if (int rc = solve_sweep(g, a, cross, run_round, kGatherRak, &prof, &rounds, &gathered, first_ids || first_random,
+                                 carry, first_random))
             return rc;
         LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, kCtrCount * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                               st));

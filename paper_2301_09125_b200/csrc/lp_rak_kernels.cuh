@@ -1015,6 +1015,115 @@ __global__ void __launch_bounds__(256) k_first_round_wbig(EvalArgs a, int32_t S)
     if (wib == 0) flush_counters(a, dchg, arcs, writes, verts);
 }
 
+// Random ties (non-strict), unit weights, first round from ids: every label
+// has weight 1, so the winner is the label with the largest tie_hash (the
+// earliest arc on a hash collision) -- a max over the row, no tally.  Warp per
+// row, 32 rows per warp batch (long rows stream 32 arcs per step).
+__global__ void __launch_bounds__(256) k_first_round_r(EvalArgs a, int32_t S) {
+    long long dchg = 0, arcs = 0, writes = 0, verts = 0;
+    const int lane = threadIdx.x & 31;
+    const int32_t nwarps = (int32_t)(gridDim.x * blockDim.x / 32);
+    for (int32_t base = (int32_t)((blockIdx.x * blockDim.x + threadIdx.x) / 32) * 32; base < S; base += nwarps * 32) {
+        const int32_t ms = base + lane;
+        uint32_t mbeg = 0, mend = 0;
+        int32_t mp = 0;
+        if (ms < S) {
+            mp = __ldg(a.svid + ms);
+            mbeg = __ldg(a.soff + ms);
+            mend = __ldg(a.soff + ms + 1);
+        }
+        uint32_t chm = 0;
+        const int nv = min(32, S - base);
+        for (int v = 0; v < nv; ++v) {
+            const int32_t s = base + v;
+            const uint32_t beg = __shfl_sync(0xffffffffu, mbeg, v);
+            const int d = (int)(__shfl_sync(0xffffffffu, mend, v) - beg);
+            const int32_t p = __shfl_sync(0xffffffffu, mp, v);
+            if (d > kFirstBig) continue;  // k_first_round_rbig
+            unsigned long long bk = 0;  // (tie hash << 32) | ~arc; 0 = none (~arc > 0)
+            int32_t bl = -1;
+            for (int k = lane; k < d; k += 32) {
+                const int32_t lab = (int32_t)(__ldg(a.snbr + beg + k) >> 2);
+                const unsigned long long key = ((unsigned long long)tie_hash(a.seed, a.sweep, (uint32_t)p, (uint32_t)lab) << 32) |
+                                               (unsigned long long)(~(uint32_t)k);
+                if (key > bk) {
+                    bk = key;
+                    bl = lab;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                const unsigned long long ok = shfl_u64(bk, o);
+                const int32_t ol = __shfl_xor_sync(0xffffffffu, bl, o);
+                if (ok > bk) {
+                    bk = ok;
+                    bl = ol;
+                }
+            }
+            bool ch = false;
+            if (lane == 0 && d > 0) {
+                arcs += d;
+                ++verts;
+                a.ndist[s] = (a.id_single && d > a.first_est_min ? d / a.first_est_div : d) | (2 > d ? kMajBit : 0);
+                store_lead<uint32_t>(a, s, 1u, d > 1 ? 1u : 0u);
+                ch = commit_label_known(a, p, bl, p, p, dchg, writes);
+            }
+            if (__shfl_sync(0xffffffffu, ch, 0)) chm |= 1u << v;
+        }
+        if (a.mark) push_changed_batch(a, chm, ms, (int)(mend - mbeg));
+    }
+    flush_counters(a, dchg, arcs, writes, verts);
+}
+
+// (long rows of k_first_round_r: a block per row; the plan stores them first)
+__global__ void __launch_bounds__(256) k_first_round_rbig(EvalArgs a, int32_t S) {
+    __shared__ unsigned long long red[2];
+    long long dchg = 0, arcs = 0, writes = 0, verts = 0;
+    const int lane = threadIdx.x & 31;
+    for (int32_t s = blockIdx.x; s < S; s += gridDim.x) {
+        const uint32_t beg = __ldg(a.soff + s);
+        const int d = (int)(__ldg(a.soff + s + 1) - beg);
+        if (d <= kFirstBig) break;  // (long rows come first)
+        const int32_t p = __ldg(a.svid + s);
+        unsigned long long bk = 0;
+        int32_t bl = -1;
+        for (int k = threadIdx.x; k < d; k += blockDim.x) {
+            const int32_t lab = (int32_t)(__ldg(a.snbr + beg + k) >> 2);
+            const unsigned long long key = ((unsigned long long)tie_hash(a.seed, a.sweep, (uint32_t)p, (uint32_t)lab) << 32) |
+                                           (unsigned long long)(~(uint32_t)k);
+            if (key > bk) {
+                bk = key;
+                bl = lab;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            const unsigned long long ok = shfl_u64(bk, o);
+            const int32_t ol = __shfl_xor_sync(0xffffffffu, bl, o);
+            if (ok > bk) {
+                bk = ok;
+                bl = ol;
+            }
+        }
+        if (threadIdx.x == 0) red[0] = 0ull;
+        __syncthreads();
+        if (lane == 0) atomicMax(&red[0], bk);
+        __syncthreads();
+        if (lane == 0 && bk == red[0]) red[1] = (unsigned long long)(uint32_t)bl;  // (keys are unique)
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int32_t lab = (int32_t)(uint32_t)red[1];
+            arcs += d;
+            ++verts;
+            a.ndist[s] = (a.id_single && d > a.first_est_min ? d / a.first_est_div : d);
+            store_lead<uint32_t>(a, s, 1u, 1u);
+            if (commit_label_known(a, p, lab, p, p, dchg, writes) && a.mark) push_changed(a, s, d);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < 32) flush_counters(a, dchg, arcs, writes, verts);
+}
+
 __global__ void __launch_bounds__(256) k_first_round_w(EvalArgs a, int32_t S) {
     long long dchg = 0, arcs = 0, writes = 0, verts = 0;
     const int lane = threadIdx.x & 31;
