@@ -143,8 +143,8 @@ struct lp_graph {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    cudaStream_t aux[3] = {nullptr, nullptr, nullptr};  // concurrent tally kernels of a round
-    cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t aux[2] = {nullptr, nullptr};  // concurrent tally kernels of a round
+    cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
     int64_t n = 0, m = 0;
     int64_t max_degree = 0;
     int64_t sliceable = 0;  // rows long enough to be cut into slices
@@ -751,8 +751,8 @@ template <int WM, int TIE> struct Launcher {
         }
         // The tally kernels of a round are independent except for the spill chain
         // warp<0> -> warp<1> -> team (overflowing rows move up a class), so they
-        // run on three streams: the chain on the handle's stream, the small rows
-        // and team2 on aux[0], the hubs on aux[1]; their tails overlap.
+        // run on three streams: the chain on the handle's stream, the small and
+        // mid rows and team2 on aux[0], the hubs on aux[1]; their tails overlap.
         // (Running the routed lists of the chain concurrently and the spills
         // afterwards, on a fourth stream, measured slower: the kernels share the
         // SMs' shared memory, the round is throughput-bound.)
@@ -958,7 +958,7 @@ static void destroy_graph(lp_graph* g) {
         cudaStreamSynchronize(g->stream);  // the pool frees above are ordered on it
         cudaStreamDestroy(g->stream);
     }
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 2; ++i) {
         if (g->aux[i]) cudaStreamSynchronize(g->aux[i]);  // (shared streams: not destroyed)
         if (g->ev_join[i]) cudaEventDestroy(g->ev_join[i]);
     }
@@ -1310,15 +1310,15 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
         // the auxiliary tally streams are per device and live for the process
         // (creating / destroying streams per handle costs milliseconds)
         static std::mutex mu;
-        static cudaStream_t pool[64][3];
+        static cudaStream_t pool[64][2];
         static bool made[64] = {};
         std::lock_guard<std::mutex> lock(mu);
         const int dv = g->device & 63;
         if (!made[dv]) {
-            for (int i = 0; i < 3; ++i) G_CK(cudaStreamCreateWithFlags(&pool[dv][i], cudaStreamNonBlocking));
+            for (int i = 0; i < 2; ++i) G_CK(cudaStreamCreateWithFlags(&pool[dv][i], cudaStreamNonBlocking));
             made[dv] = true;
         }
-        for (int i = 0; i < 3; ++i) {
+        for (int i = 0; i < 2; ++i) {
             g->aux[i] = pool[dv][i];
             G_CK(cudaEventCreateWithFlags(&g->ev_join[i], cudaEventDisableTiming));
         }

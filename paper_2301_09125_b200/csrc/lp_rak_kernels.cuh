@@ -2112,6 +2112,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                         continue;
                     }
                     if (flag) lab = kEmpty;  // pass 0 of two: evaluated labels only
+                    if (TWO && !__any_sync(0xffffffffu, lab != kEmpty)) continue;  // (all flagged)
                     if (!hashed) {
                         uint32_t pending = __ballot_sync(0xffffffffu, lab != kEmpty);
                         for (int t = 0; t < K && pending; ++t) {
