@@ -1885,6 +1885,14 @@ __device__ __forceinline__ int insert_chunk(STable<WM, BITS>& t, int32_t lab, ty
         const int leader = __ffs(grp) - 1;
         if constexpr (WM == kUnit) {
             if (lab != kEmpty && lane == leader) h = t.add(lab, (A)__popc(grp), isnew);
+        } else if constexpr (WM == kFixed) {
+            // the group's fixed-point weights (u32 each) summed in two 16-bit halves by
+            // redux over the match group: one shared atomic per distinct label, not
+            // one per arc (hot labels serialise on one address)
+            const uint32_t wu = (uint32_t)w;
+            const unsigned long long gs = ((unsigned long long)__reduce_add_sync(grp, wu >> 16) << 16) +
+                                          (unsigned long long)__reduce_add_sync(grp, wu & 0xffffu);
+            if (lab != kEmpty && lane == leader) h = t.add(lab, (A)gs, isnew);
         } else {
             if (lab != kEmpty && lane == leader) h = t.add(lab, A(0), isnew);
             const int hb = __shfl_sync(0xffffffffu, h, leader);
@@ -2722,7 +2730,12 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                     const int ti = t0 + __popc(nbal & lanemask_lt());
                     if (isnew && ti < gcapv) gtl[ti] = g;
                 }
-                if constexpr (WM != kUnit) {
+                if constexpr (WM == kFixed) {
+                    const uint32_t wu = (uint32_t)w;  // (group sum, as in insert_chunk)
+                    const unsigned long long gs = ((unsigned long long)__reduce_add_sync(grp, wu >> 16) << 16) +
+                                                  (unsigned long long)__reduce_add_sync(grp, wu & 0xffffu);
+                    if (lab != kEmpty && lane == leader && g >= 0) gacc_add<A>(gacc + g, (A)gs);
+                } else if constexpr (WM != kUnit) {
                     const int gb = __shfl_sync(0xffffffffu, g, leader);
                     if (lab != kEmpty && gb >= 0) gacc_add<A>(gacc + gb, w);
                 }

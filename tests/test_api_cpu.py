@@ -196,3 +196,20 @@ def test_sweep_spec_and_csv_schema():
     assert r.csv_row() == "g,copra,,0.01,4,,1,7,3,1.500,0.250000000"
     assert r.csv_row(extended=True).endswith(",1,3000000,2.0000")
     assert len(r.csv_row(extended=True).split(",")) == len(sweep.CSV_HEADER_EXTENDED.split(","))
+
+
+def test_cli_specs_and_info(tmp_path, capsys):
+    """cli.py: generator specs, .npz CSR files, `info` (no GPU needed)."""
+    from paper_2301_09125_b200 import cli
+
+    g = cli.load_spec("planted:2000:20:3")
+    assert G.graphs_equal(g, lp.planted_partition(2000, 20, seed=3))
+    p = tmp_path / "g.npz"
+    np.savez(p, offsets=g.offsets, neighbors=g.neighbors)
+    assert G.graphs_equal(cli.load_spec(str(p)), g)
+    with pytest.raises(ValueError):
+        cli.load_spec("louvain:3")
+    assert cli.main(["info", "rmat:10", str(p)]) == 0
+    out = capsys.readouterr().out.splitlines()
+    assert out[0] == "graph\tvertices\tedges\tavg_degree" and out[1].startswith("rmat:10\t1024\t")
+    assert cli.main(["info", "bogus:1"]) == 2

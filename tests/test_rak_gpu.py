@@ -332,3 +332,20 @@ def test_sweep_runs_the_cuda_detectors(gpu):
     crec = list(lp.run_sweep(lp.SweepSpec("copra", tolerances=(0.01,), max_labels=(2,)), [("planted", g)]))
     srec = list(lp.run_sweep(lp.SweepSpec("slpa", memory_sizes=(8,), modes=("strict",)), [("planted", g)]))
     assert len(crec) == 1 and len(srec) == 1 and crec[0].iterations >= 1 and srec[0].iterations >= 1
+
+
+def test_cli_detect_and_sweep(gpu, tmp_path, capsys):
+    """`python -m paper_2301_09125_b200 detect / sweep` (cli.py) on the CUDA detectors."""
+    from paper_2301_09125_b200 import cli
+
+    out = tmp_path / "labels.tsv"
+    assert cli.main(["detect", "--graph", "planted:3000:30:4", "--algorithm", "rak", "--strict", "--seed", "3",
+                     "--output", str(out)]) == 0
+    got = np.loadtxt(out, dtype=np.int64)
+    want = lp.rak_detect(lp.planted_partition(3000, 30, seed=4), lp.RakParams(strict=True, seed=3))
+    assert np.array_equal(got[:, 0], np.arange(3000)) and np.array_equal(got[:, 1], want.assignment)
+    assert "iterations=%d" % want.iterations in capsys.readouterr().err
+    assert cli.main(["sweep", "--algorithm", "slpa", "--graph", "planted:3000:30:4", "--memory-sizes", "8",
+                     "--modes", "strict", "--batches-grid", "0,1", "--extended"]) == 0
+    lines = capsys.readouterr().out.splitlines()
+    assert lines[0].endswith(",batches,edges_scanned,gteps") and len(lines) == 3
