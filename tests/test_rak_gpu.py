@@ -236,6 +236,24 @@ def test_exact_schedule_full_size_rmat20(gpu, oracle):
         assert res.iterations == it and np.array_equal(res.assignment, want), batches
 
 
+def test_exact_schedule_full_size_other_rules(gpu, oracle):
+    """The reference visit order at scale for the other tie rules and weights
+    (first rounds from ids, singleton two-pass tallies, hub partitions):
+    non-strict and min-label on R-MAT-20, float32 weights (exact fixed point)
+    on R-MAT-18 -- labels and per-sweep changed counts bit-exact to the oracle."""
+    g = lp.rmat(20, seed=3)
+    for tie in ("random", "min-label"):
+        want, it, changed = oracle.rak(g, batches=0, tie=ORACLE_TIE[tie], seed=4, tolerance=0.05, max_iterations=20)
+        res = lp.rak_detect(g, lp.RakParams(seed=4, tolerance=0.05, max_iterations=20, tie=tie), changed_history=True)
+        assert res.iterations == it and np.array_equal(res.stats["changed"], changed), tie
+        assert np.array_equal(res.assignment, want), tie
+    gw = lp.rmat(18, seed=5, weighted=True)
+    want, it, changed = oracle.rak(gw, batches=0, tie=0, seed=1, tolerance=0.05, max_iterations=20)
+    res = lp.rak_detect(gw, lp.RakParams(strict=True, seed=1, tolerance=0.05, max_iterations=20), changed_history=True)
+    assert res.iterations == it and np.array_equal(res.stats["changed"], changed)
+    assert np.array_equal(res.assignment, want)
+
+
 def test_malformed_csr_rejected_on_upload(gpu):
     from paper_2301_09125_b200 import _lib
 
