@@ -107,6 +107,11 @@ __device__ __forceinline__ unsigned long long shfl_u64(unsigned long long v, int
     hi = __shfl_xor_sync(0xffffffffu, hi, src);
     return ((unsigned long long)hi << 32) | lo;
 }
+__device__ __forceinline__ uint32_t shfl_idx_any(uint32_t v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ float shfl_idx_any(float v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ unsigned long long shfl_idx_any(unsigned long long v, int src) {
+    return __shfl_sync(0xffffffffu, v, src);
+}
 __device__ __forceinline__ uint32_t shfl_xor_any(uint32_t v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
 __device__ __forceinline__ float shfl_xor_any(float v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
 __device__ __forceinline__ unsigned long long shfl_xor_any(unsigned long long v, int m) { return shfl_u64(v, m); }

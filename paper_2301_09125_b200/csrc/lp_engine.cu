@@ -224,6 +224,7 @@ struct lp_graph {
     bool id_single = true;  // LP_ID_SINGLE=0: no singleton labels in the first sweep (see kSingle)
     int push_div = 3;
     bool id_single_random = true;  // LP_ID_SINGLE_RANDOM=0: no singleton labels with random ties
+    bool id_single_w = true;       // LP_ID_SINGLE_W=0: no singleton labels with fixed-point weights
     int reg_est = LP_WARP_REG_EST;  // LP_REG_EST
     int mid_max = kMidMax;          // LP_MID_MAX: thread-per-row k_mid up to this degree (0 = off)
     bool mid_hash = true;           // LP_MID_HASH=0: unit-weight mid rows by O(d^2) compares (k_mid)      // sweep boundary: push marks from the changed rows when <= 1/push_div of the
@@ -650,7 +651,7 @@ template <int WM, int TIE> struct Launcher {
     static int occ_warp[2], occ_team, occ_team2, occ_hub, occ_mid, occ_midh, done_device;
     template <int WC> static cudaError_t setup_warp() {
         cudaError_t e;
-        if constexpr (WM == kUnit) {
+        if constexpr (WM == kUnit || WM == kFixed) {
             e = cudaFuncSetAttribute(k_warp<WM, TIE, WC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)warp_smem_bytes<WM, WC>());
             if (e) return e;
@@ -711,7 +712,7 @@ template <int WM, int TIE> struct Launcher {
         prof->begin(s, kKWarp);
         const int per_block = 32 * WarpClass<WC>::kWarps;
         const int grid = dense ? sms * occ_warp[WC] : grid_for(cnt, per_block, sms * occ_warp[WC]);
-        if constexpr (WM == kUnit) {
+        if constexpr (WM == kUnit || WM == kFixed) {
             if (a.id_single) {
                 k_warp<WM, TIE, WC, true><<<grid, WarpClass<WC>::kWarps * 32, warp_smem_bytes<WM, WC>(), s>>>(a);
                 prof->end(s);
@@ -1288,6 +1289,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_ID_SINGLE")) g->id_single = atoi(ev) != 0;
     if (const char* ev = getenv("LP_PUSH_DIV")) g->push_div = std::max(1, atoi(ev));
     if (const char* ev = getenv("LP_ID_SINGLE_RANDOM")) g->id_single_random = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_ID_SINGLE_W")) g->id_single_w = atoi(ev) != 0;
     if (const char* ev = getenv("LP_REG_EST")) g->reg_est = std::max(0, std::min(32, atoi(ev)));
     if (const char* ev = getenv("LP_MID_MAX")) g->mid_max = std::max(0, std::min(kMidMax, atoi(ev)));
     if (const char* ev = getenv("LP_MID_HASH")) g->mid_hash = atoi(ev) != 0;
@@ -1773,6 +1775,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.seed = o->seed;
     a.cap_route = g->cap_route;
     a.id_single = 0;
+    a.two_team = 0;
     a.mbits = g->mbits;
     a.first_est_min = g->first_est_min;
     a.first_est_div = g->first_est_div;
@@ -1840,8 +1843,11 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         const bool first_random = it == 1 && !labels_init && g->wmode == kUnit && g->rows_sorted &&
                                   o->tie == kRandom && g->first_round_shortcut;
         // first sweep from labels = ids: unevaluated neighbours carry singleton labels
-        a.id_single = (it == 1 && !labels_init && g->wmode == kUnit && g->rows_sorted && n < (1 << 30) &&
-                       (o->tie != kRandom || g->id_single_random) && g->id_single) ? 1 : 0;
+        a.id_single = (it == 1 && !labels_init && (g->wmode == kUnit || (g->wmode == kFixed && g->id_single_w)) &&
+                       g->rows_sorted && n < (1 << 30) && (o->tie != kRandom || g->id_single_random) && g->id_single)
+                          ? 1
+                          : 0;
+        a.two_team = a.id_single && g->wmode == kUnit;
         if (int rc = solve_sweep(g, a, cross, run_round, kGatherRak, &prof, &rounds, &gathered, first_ids || first_random,
                                  carry, first_random))
             return rc;
@@ -1992,6 +1998,7 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     a.T = T;
     a.cap_route = g->cap_route;
     a.id_single = 0;
+    a.two_team = 0;
     a.mbits = g->mbits;
     a.first_est_min = g->first_est_min;
     a.first_est_div = g->first_est_div;

@@ -144,7 +144,8 @@ struct EvalArgs {
     int32_t T;
     int32_t cap_route;  // route a row to the smallest table that holds d entries even when its
                         // estimate is larger (such a row can never overflow that table)
-    int32_t id_single;  // first sweep from labels = ids, unit weights, duplicate-free rows: see kSingle
+    int32_t id_single;  // first sweep from labels = ids, duplicate-free rows: see kSingle
+    int32_t two_team;   // ... and unit weights: the team / hub kernels take the two passes too
     int32_t warp_maxd[2];  // longest row routed to warp class 0 / 1 (longer rows go to the teams)
     int32_t reg_est;       // rows estimated to hold more labels skip the warp register table
     int32_t mid_max;       // rows of kSmallMax < d <= mid_max go to k_mid (0 = off)
@@ -807,7 +808,7 @@ __device__ __forceinline__ void route_append(const EvalArgs& a, int cls, int32_t
         int gt = -1;
         // slices when the labels are few (a small L2 table); with many labels the
         // smem label partitions are faster than global-table atomics (measured)
-        if (d > kSliceArcs * 2 && est <= kSliceEst && !a.id_single) {
+        if (d > kSliceArcs * 2 && est <= kSliceEst && !a.two_team) {
             gt = atomicAdd(a.r.len + kGtabCursor, 1 << gbits);
             if ((int64_t)gt + (1 << gbits) > a.r.gcap) gt = -1;  // pool exhausted: partitions
         }
@@ -984,7 +985,9 @@ __device__ __forceinline__ bool first_w_commit(const EvalArgs& a, int32_t s, int
     arcs += d;
     ++verts;
     const bool maj = 2ull * t.w1 > total;
-    a.ndist[s] = d | (maj ? kMajBit : 0);
+    // (weighted singleton sweep: warp-sized rows table a fraction of their labels)
+    a.ndist[s] = (a.id_single && d > a.first_est_min && d <= WarpClass<0>::kMaxDeg ? d / a.first_est_div : d) |
+                 (maj ? kMajBit : 0);
     store_lead<unsigned long long>(a, s, (unsigned long long)t.w1, (unsigned long long)t.w2);
     return commit_label_known(a, p, lab, p, p, dchg, writes);
 }
@@ -2058,6 +2061,10 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
             int ntouched = 0;
             bool overflow = false;
             int singles = 0;  // (two passes) flagged labels absent from the table, this lane
+            // (weighted two passes: the best absent flagged label of this lane, and the two
+            // largest absent weights -- a singleton's weight is its arc's)
+            Cand<A> sbest = none_cand<A>();
+            A s1w = A(0), s2w = A(0);
             constexpr int npass = TWO ? 2 : 1;
             uint32_t mysig = 0;  // (two passes, hashed) lane's word of the table keys' 1024-bit signature
             for (int pass = 0; pass < npass && !overflow; ++pass) {
@@ -2097,8 +2104,13 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                                 const int32_t key = __shfl_sync(0xffffffffu, tkey, t);
                                 const uint32_t m = __ballot_sync(0xffffffffu, flag && lab == key);
                                 if (m) {
+                                    A add;
+                                    if constexpr (WM == kUnit)
+                                        add = (A)__popc(m);
+                                    else
+                                        add = masked_sum<A>(m, wv[c]);
                                     if (lane == t) {
-                                        tacc += (A)__popc(m);
+                                        tacc += add;
                                         // (scan-first: a flagged arc may precede the entry's first one)
                                         tfirst = min(tfirst, (uint32_t)(k0 + __ffs(m) - 1));
                                     }
@@ -2111,12 +2123,23 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                             if (flag && ((word >> (h2 & 31u)) & 1u)) {
                                 const int h = tab->t.find(lab);
                                 if (h >= 0) {
-                                    tab->t.add_at(h, A(1));
+                                    tab->t.add_at(h, WM == kUnit ? A(1) : wv[c]);
                                     hit = true;
                                 }
                             }
                         }
                         singles += (flag && !hit) ? 1 : 0;
+                        if (WM != kUnit && flag && !hit) {
+                            const A w = wv[c];
+                            const Cand<A> sc = make_cand<TIE, A>(w, lab, (uint32_t)(k0 + lane), a.seed, a.sweep, vtx);
+                            if (better(sc, sbest)) sbest = sc;
+                            if (w > s1w) {
+                                s2w = s1w;
+                                s1w = w;
+                            } else if (w > s2w) {
+                                s2w = w;
+                            }
+                        }
                         continue;
                     }
                     if (flag) lab = kEmpty;  // pass 0 of two: evaluated labels only
@@ -2259,7 +2282,43 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k
                 for (int t = lane; t < ntouched; t += 32) tab->t.init(tab->touched[t]);
                 __syncwarp();
             }
-            if (TWO) {
+            if (TWO && WM != kUnit) {
+                const int nsingle = (int)__reduce_add_sync(0xffffffffu, (unsigned)singles);
+                wbest = shfl_idx_any(wbest, 0);
+                if (nsingle > 0) {
+                    // the best absent flagged label against the table's winner
+                    const Cand<A> sb = warp_best(sbest);
+#pragma unroll
+                    for (int o = 16; o >= 1; o >>= 1) {
+                        const A o1 = shfl_xor_any(s1w, o), o2 = shfl_xor_any(s2w, o);
+                        const A lo = s1w < o1 ? s1w : o1;
+                        s1w = s1w > o1 ? s1w : o1;
+                        const A m2 = s2w > o2 ? s2w : o2;
+                        s2w = lo > m2 ? lo : m2;
+                    }
+                    const bool table = (hashed ? ntouched : K) > 0;
+                    if (!table || sb.w > wbest) {
+                        wsecond = table ? (wbest > s2w ? wbest : s2w) : s2w;
+                        winner = sb.lab;
+                        wbest = sb.w;
+                    } else if (sb.w < wbest) {
+                        wsecond = wsecond > s1w ? wsecond : s1w;
+                    } else {
+                        // equal weights: the tie rule decides (the table winner's first arc)
+                        int first = -1;
+                        for (int base = 0; base < d && first < 0; base += 32) {
+                            const int k = base + lane;
+                            const bool hitw = k < d && lb_strip(a, a.lbuf[beg + k]) == winner;
+                            const uint32_t hm = __ballot_sync(0xffffffffu, hitw);
+                            if (hm) first = base + __ffs(hm) - 1;
+                        }
+                        const Cand<A> tc = make_cand<TIE, A>(wbest, winner, (uint32_t)first, a.seed, a.sweep, vtx);
+                        if (better(sb, tc)) winner = sb.lab;
+                        wsecond = wbest;
+                    }
+                }
+            }
+            if (TWO && WM == kUnit) {
                 const int nsingle = (int)__reduce_add_sync(0xffffffffu, (unsigned)singles);
                 wbest = __shfl_sync(0xffffffffu, wbest, 0);
                 if (nsingle > 0) {
@@ -2365,7 +2424,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
     // kSingle two-pass tally (first sweep from ids; hub rows are then routed as
     // label partitions, never as slices: a slice cannot look labels up after
     // the other slices' inserts)
-    const bool two = a.id_single;
+    const bool two = a.two_team;
     for (int h = tid; h < HB; h += NT) tab->t.init(h);
     const Item* items = which == kLenHub ? a.r.hub : (which == kLenTeam2 ? a.r.team2 : a.r.team);
     const int cursor = which == kLenHub ? kHubCursor : (which == kLenTeam2 ? kTeam2Cursor : kTeamCursor);
