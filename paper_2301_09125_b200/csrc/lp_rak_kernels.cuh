@@ -211,13 +211,13 @@ constexpr int kSmallMax = 16;     // thread-per-vertex bound (degree)
                            // ballot per entry per chunk)
 #endif
 // warp classes: 0 = 512-slot table (est <= 256, d <= 2048, 8 warps/block),
-// 1 = 1024-slot table (est <= 512, d <= 8192, 8 warps/block)
+// 1 = 1024-slot table (est <= 512, d <= 8192, 4 warps/block)
 template <int WC> struct WarpClass;
 template <> struct WarpClass<0> {
     static constexpr int kBits = 9, kEst = 256, kMaxDeg = 2048, kWarps = 8, kList = 3;
 };
 template <> struct WarpClass<1> {
-    static constexpr int kBits = 10, kEst = 512, kMaxDeg = 8192, kWarps = 8, kList = 6;
+    static constexpr int kBits = 10, kEst = 512, kMaxDeg = 8192, kWarps = 4, kList = 6;  // (4: +25% resident warps)
 };
 constexpr int kWarpEst = WarpClass<0>::kEst;
 constexpr int kTeamEst = 2048;    // 8-warp team: 4096-slot table
