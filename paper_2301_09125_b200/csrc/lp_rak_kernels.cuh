@@ -1876,7 +1876,10 @@ __device__ __forceinline__ uint32_t sig_hash(int32_t lab) { return ((uint32_t)la
 // __match_any_sync first (rows with few distinct labels); otherwise every lane
 // inserts its own label (rows whose labels are mostly distinct).
 // Returns this lane's slot when it created a new entry, else -1.
-template <int WM, int BITS>
+// GSUM: fixed-point weights of a match group summed (two redux.sync) before one
+// table atomic -- measured faster in the team kernels (long rows, hot labels),
+// slower in the warp kernel
+template <int WM, int BITS, bool GSUM = false>
 __device__ __forceinline__ int insert_chunk(STable<WM, BITS>& t, int32_t lab, typename Acc<WM>::T w, bool agg,
                                             bool& full) {
     using A = typename Acc<WM>::T;
@@ -1888,10 +1891,7 @@ __device__ __forceinline__ int insert_chunk(STable<WM, BITS>& t, int32_t lab, ty
         const int leader = __ffs(grp) - 1;
         if constexpr (WM == kUnit) {
             if (lab != kEmpty && lane == leader) h = t.add(lab, (A)__popc(grp), isnew);
-        } else if constexpr (WM == kFixed) {
-            // the group's fixed-point weights (u32 each) summed in two 16-bit halves by
-            // redux over the match group: one shared atomic per distinct label, not
-            // one per arc (hot labels serialise on one address)
+        } else if constexpr (WM == kFixed && GSUM) {
             const uint32_t wu = (uint32_t)w;
             const unsigned long long gs = ((unsigned long long)__reduce_add_sync(grp, wu >> 16) << 16) +
                                           (unsigned long long)__reduce_add_sync(grp, wu & 0xffffu);
@@ -2495,7 +2495,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
 #pragma unroll
                 for (int c = 0; c < U; ++c) {
                     bool full = false;
-                    const int h = insert_chunk<WM, TBITS>(tab->t, labv[c], wv[c], agg, full);
+                    const int h = insert_chunk<WM, TBITS, true>(tab->t, labv[c], wv[c], agg, full);
                     const uint32_t nb = __ballot_sync(0xffffffffu, h >= 0);
                     if (nb) {
                         int b0 = 0;
@@ -2789,12 +2789,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                     const int ti = t0 + __popc(nbal & lanemask_lt());
                     if (isnew && ti < gcapv) gtl[ti] = g;
                 }
-                if constexpr (WM == kFixed) {
-                    const uint32_t wu = (uint32_t)w;  // (group sum, as in insert_chunk)
-                    const unsigned long long gs = ((unsigned long long)__reduce_add_sync(grp, wu >> 16) << 16) +
-                                                  (unsigned long long)__reduce_add_sync(grp, wu & 0xffffu);
-                    if (lab != kEmpty && lane == leader && g >= 0) gacc_add<A>(gacc + g, (A)gs);
-                } else if constexpr (WM != kUnit) {
+                if constexpr (WM != kUnit) {
                     const int gb = __shfl_sync(0xffffffffu, g, leader);
                     if (lab != kEmpty && gb >= 0) gacc_add<A>(gacc + gb, w);
                 }
