@@ -1920,7 +1920,7 @@ __device__ __forceinline__ int insert_chunk(STable<WM, BITS>& t, int32_t lab, ty
 // TWO: the kSingle two-pass tally (first sweep from ids; a separate
 // instantiation keeps the other sweeps' code and registers unchanged)
 template <int WM, int TIE, int WC, bool TWO>
-__global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 ? 4 : 3) k_warp(EvalArgs a) {
+__global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 && WM == kUnit ? 4 : 3) k_warp(EvalArgs a) {
     using A = typename Acc<WM>::T;
     using WT = WarpTable<WM, WC>;
     constexpr int kWarpBits = WarpClass<WC>::kBits;
