@@ -170,6 +170,8 @@ struct lp_graph {
     int32_t* mq_len = nullptr;  // their lengths [2]
     uint32_t* mbits = nullptr;  // marked-vertex bitmap (all zero between passes)
     int2* hb_off = nullptr;     // hub partition buckets (per item cb + q)
+    bool mark_bitmap = true;    // LP_MARK_BITMAP=0: always queue marked vertices by scanning the marks
+    int mark_scan_div = 16;     // ... scan when more than n / mark_scan_div rows changed (LP_MARK_SCAN_DIV)
     bool hub_bucket = false;    // LP_HUB_BUCKET=1: bucket hub partitions (measured: no gain once hubs
                                 // use the singleton two-pass tally)
     int first_est_min = 256, first_est_div = 4;  // LP_FIRST_EST_MIN / LP_FIRST_EST_DIV (tuned on R-MAT-22)
@@ -1294,6 +1296,8 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_MID_MAX")) g->mid_max = std::max(0, std::min(kMidMax, atoi(ev)));
     if (const char* ev = getenv("LP_MID_HASH")) g->mid_hash = atoi(ev) != 0;
     if (const char* ev = getenv("LP_HUB_BUCKET")) g->hub_bucket = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_MARK_BITMAP")) g->mark_bitmap = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_MARK_SCAN_DIV")) g->mark_scan_div = std::max(1, atoi(ev));
     if (const char* ev = getenv("LP_FIRST_EST_MIN")) g->first_est_min = std::max(16, atoi(ev));
     if (const char* ev = getenv("LP_FIRST_EST_DIV")) g->first_est_div = std::max(1, atoi(ev));
     if (const char* ev = getenv("LP_WARP0_MAXD")) g->warp_maxd[0] = std::max(17, std::min(WarpClass<0>::kMaxDeg, atoi(ev)));
@@ -1461,7 +1465,20 @@ static int ensure_waves(lp_graph* g, int W) {
 // active row, then frontier rounds over the mark queue until a round marks
 // nothing.  One host sync per frontier round (route sizes).
 // the vertices a marking pass flagged in the bitmap -> a.mq_out (bits cleared)
+// Marking mode of a pass: the bitmap (a second, cheap atomic per marked arc;
+// compaction reads n/32 words) for passes over few changed rows, the flat scan
+// of the marks (compaction reads 8 B per vertex) for big ones.
+static EvalArgs marks_mode(lp_graph* g, const EvalArgs& a, int64_t changed_rows) {
+    EvalArgs b = a;
+    b.mbits = (g->mark_bitmap && changed_rows * g->mark_scan_div <= g->n) ? g->mbits : nullptr;
+    return b;
+}
+
 static void bits_to_queue(lp_graph* g, const EvalArgs& a) {
+    if (!a.mbits) {
+        k_marks_to_queue<<<grid_for(g->n, 256, g->num_sms * 8), 256, 0, g->stream>>>(g->mark, g->n, a.mq_out, a.mq_len);
+        return;
+    }
     const int64_t nwords = g->n / 32 + 1;
     k_bits_to_queue<<<grid_for(nwords, 256, g->num_sms * 8), 256, 0, g->stream>>>(g->mbits, nwords, a.mq_out, a.mq_len);
 }
@@ -1485,9 +1502,10 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
     // the last wave, so that a vertex marked by two waves is queued once)
     auto mark_pass = [&](int64_t changed_rows, bool compact = true) {
         const int64_t pieces = changed_rows + changed_rows / 8 + 32;
+        const EvalArgs b = marks_mode(g, a, changed_rows);
         prof->begin(st, -1);
-        k_mark_pieces<<<grid_for(pieces, 32 * 8, g->num_sms * 16), 256, 0, st>>>(a);
-        if (compact) bits_to_queue(g, a);
+        k_mark_pieces<<<grid_for(pieces, 32 * 8, g->num_sms * 16), 256, 0, st>>>(b);
+        if (compact) bits_to_queue(g, b);
         prof->end(st);
     };
     // writes of the round just run (label changes); one sync
@@ -1533,7 +1551,7 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
             ++*rounds;
         }
         a.horizon = INT32_MAX;
-        if (a.mark) bits_to_queue(g, a);
+        if (a.mark) bits_to_queue(g, marks_mode(g, a, INT64_MAX / 4));  // (the waves' mode)
         next = kNextQueue;
     }
     cudaEvent_t dbg0 = nullptr, dbg1 = nullptr;
@@ -1639,9 +1657,10 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
                 k_flags_from_changed<<<g->num_sms * 8, 256, 0, st>>>(a, g->chg);
                 LP_CK(cudaMemsetAsync(g->routes.len + kGatherCursor, 0, sizeof(int32_t), st));
                 prof->begin(st, -1);
-                k_pull_marks<<<g->num_sms * 16, 256, 0, st>>>(a, g->chg, P.dslot, P.dk0, P.dcount,
+                const EvalArgs b = marks_mode(g, a, w);
+                k_pull_marks<<<g->num_sms * 16, 256, 0, st>>>(b, g->chg, P.dslot, P.dk0, P.dcount,
                                                              g->routes.len + kGatherCursor, 1);
-                bits_to_queue(g, a);
+                bits_to_queue(g, b);
                 prof->end(st);
                 next = kNextQueue;
             } else {
@@ -1776,7 +1795,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.cap_route = g->cap_route;
     a.id_single = 0;
     a.two_team = 0;
-    a.mbits = g->mbits;
+    a.mbits = g->mbits;  // (per marking pass: marks_mode)
     a.first_est_min = g->first_est_min;
     a.first_est_div = g->first_est_div;
     // (unit weights only: with weights the bucketed arcs' weight loads are
@@ -1820,16 +1839,18 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
                 // few changed rows: push from them (one atomic per neighbour)
                 k_sweep_changes<<<g->num_sms * 8, 256, 0, st>>>(a, L0, X, (int32_t)P.S);  // L0 = last result
                 a.mark_all = 1;
-                k_mark_pieces<<<g->num_sms * 16, 256, 0, st>>>(a);
-                bits_to_queue(g, a);
+                const EvalArgs b = marks_mode(g, a, last_changed);
+                k_mark_pieces<<<g->num_sms * 16, 256, 0, st>>>(b);
+                bits_to_queue(g, b);
                 a.mark_all = 0;
             } else {
                 // many: every row pulls the changed flags of its neighbours (one flat
                 // pass, one atomic per row piece with a changed neighbour)
                 k_changed_flags<<<g->num_sms * 8, 256, 0, st>>>(L0, X, g->chg, n);
-                k_pull_marks<<<g->num_sms * 16, 256, 0, st>>>(a, g->chg, P.dslot, P.dk0, P.dcount,
+                const EvalArgs b = marks_mode(g, a, last_changed);
+                k_pull_marks<<<g->num_sms * 16, 256, 0, st>>>(b, g->chg, P.dslot, P.dk0, P.dcount,
                                                              g->routes.len + kGatherCursor, 0);
-                bits_to_queue(g, a);
+                bits_to_queue(g, b);
             }
             prof.end(st);
         }
@@ -2003,7 +2024,7 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     a.cap_route = g->cap_route;
     a.id_single = 0;
     a.two_team = 0;
-    a.mbits = g->mbits;
+    a.mbits = g->mbits;  // (per marking pass: marks_mode)
     a.first_est_min = g->first_est_min;
     a.first_est_div = g->first_est_div;
     // (unit weights only: with weights the bucketed arcs' weight loads are

@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(256) k_pull_marks(EvalArgs a, const uint32_t* 
         if (sm) {
             const int32_t v = __ldg(a.svid + ps);
             atomicAdd(a.mark + v, sm);  // (fire-and-forget; the bitmap queues v)
-            atomicOr(a.mbits + (v >> 5), 1u << (v & 31));
+            if (a.mbits) atomicOr(a.mbits + (v >> 5), 1u << (v & 31));
         }
         __syncwarp();
     }
@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(256) k_mark_pieces(EvalArgs a) {
                 // 0 -> nonzero transition of the mark)
                 if (e[j] != 0xffffffffu && (a.mark_all || (nb[j] & kLater)) && needs_mark(a, u)) {
                     atomicAdd(a.mark + u, mark_weight(a, e[j]));
-                    atomicOr(a.mbits + (u >> 5), 1u << (u & 31));
+                    if (a.mbits) atomicOr(a.mbits + (u >> 5), 1u << (u & 31));
                 }
             }
         }
@@ -710,6 +710,25 @@ __global__ void __launch_bounds__(256) k_mark_pieces(EvalArgs a) {
 
 // Marked-vertex bitmap -> mark queue (appended to mq_out), bits cleared.
 // Whole warps: lane w of a warp takes bitmap word base + w.
+// Without the bitmap (mbits = null): every vertex with a nonzero mark is
+// queued -- one flat read of the marks instead of a second atomic per
+// marked arc (marks are zero again once routed).
+__global__ void k_marks_to_queue(const unsigned long long* __restrict__ mark, int64_t n, int32_t* __restrict__ mq_out,
+                                 int32_t* mq_len) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+        const int64_t v = base + threadIdx.x;
+        const bool nz = v < n && __ldcg(mark + v) != 0ull;
+        const uint32_t bal = __ballot_sync(0xffffffffu, nz);
+        if (!bal) continue;
+        int b0 = 0;
+        if (lane == 0) b0 = atomicAdd(mq_len, __popc(bal));
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (nz) mq_out[b0 + __popc(bal & lanemask_lt())] = (int32_t)v;
+    }
+}
+
 __global__ void k_bits_to_queue(uint32_t* __restrict__ mbits, int64_t nwords, int32_t* __restrict__ mq_out,
                                 int32_t* mq_len) {
     const int lane = threadIdx.x & 31;
