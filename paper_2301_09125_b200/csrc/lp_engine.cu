@@ -227,6 +227,7 @@ struct lp_graph {
     int push_div = 3;
     bool id_single_random = true;  // LP_ID_SINGLE_RANDOM=0: no singleton labels with random ties
     bool id_single_w = true;       // LP_ID_SINGLE_W=0: no singleton labels with fixed-point weights
+    bool two_team_w = true;        // LP_TWO_TEAM_W=0: weighted team / hub rows insert every label
     int reg_est = LP_WARP_REG_EST;  // LP_REG_EST
     int mid_max = kMidMax;          // LP_MID_MAX: thread-per-row k_mid up to this degree (0 = off)
     bool mid_hash = true;           // LP_MID_HASH=0: unit-weight mid rows by O(d^2) compares (k_mid)      // sweep boundary: push marks from the changed rows when <= 1/push_div of the
@@ -1292,6 +1293,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_PUSH_DIV")) g->push_div = std::max(1, atoi(ev));
     if (const char* ev = getenv("LP_ID_SINGLE_RANDOM")) g->id_single_random = atoi(ev) != 0;
     if (const char* ev = getenv("LP_ID_SINGLE_W")) g->id_single_w = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_TWO_TEAM_W")) g->two_team_w = atoi(ev) != 0;
     if (const char* ev = getenv("LP_REG_EST")) g->reg_est = std::max(0, std::min(32, atoi(ev)));
     if (const char* ev = getenv("LP_MID_MAX")) g->mid_max = std::max(0, std::min(kMidMax, atoi(ev)));
     if (const char* ev = getenv("LP_MID_HASH")) g->mid_hash = atoi(ev) != 0;
@@ -1868,7 +1870,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
                        g->rows_sorted && n < (1 << 30) && (o->tie != kRandom || g->id_single_random) && g->id_single)
                           ? 1
                           : 0;
-        a.two_team = a.id_single && g->wmode == kUnit;
+        a.two_team = a.id_single && (g->wmode == kUnit || (g->wmode == kFixed && g->two_team_w));
         // (the first round's low label estimates serve the next round's singleton
         // tallies; a synchronous weighted schedule has none -- its second sweep's
         // diverse weighted labels then overflow the small tables: measured slower)

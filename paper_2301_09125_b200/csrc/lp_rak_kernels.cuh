@@ -1005,7 +1005,8 @@ __device__ __forceinline__ bool first_w_commit(const EvalArgs& a, int32_t s, int
     ++verts;
     const bool maj = 2ull * t.w1 > total;
     // (weighted singleton sweep: warp-sized rows table a fraction of their labels)
-    a.ndist[s] = (a.id_single && d > a.first_est_min && d <= WarpClass<0>::kMaxDeg ? d / a.first_est_div : d) |
+    a.ndist[s] = (a.id_single && d > a.first_est_min && (a.two_team || d <= WarpClass<0>::kMaxDeg) ? d / a.first_est_div
+                                                                                                  : d) |
                  (maj ? kMajBit : 0);
     store_lead<unsigned long long>(a, s, (unsigned long long)t.w1, (unsigned long long)t.w2);
     return commit_label_known(a, p, lab, p, p, dchg, writes);
@@ -2546,6 +2547,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 __syncthreads();
                 continue;
             }
+            Best<A> sb = none_best<A>();  // (weighted) best absent flagged label of this partition
             if (two) {
                 // pass 2: flagged labels of this partition are looked up only
                 int sg = 0;
@@ -2569,11 +2571,24 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                         if (lab & kSingle) {
                             lab = lb_strip(a, lab);
                             if (parts <= 1 || part_of(lab, parts) == want) {
+                                const A w = WM == kUnit ? A(1) : arc_weight<WM>(a, beg + k);
                                 const int h = tab->t.find(lab);
-                                if (h >= 0)
-                                    tab->t.add_at(h, A(1));
-                                else
+                                if (h >= 0) {
+                                    tab->t.add_at(h, w);
+                                } else {
                                     ++sg;
+                                    if constexpr (WM != kUnit) {
+                                        // a weighted singleton competes with its arc's weight
+                                        Best<A> c;
+                                        c.w = w;
+                                        c.w2 = A(0);
+                                        c.sec = sec_of<TIE>(lab, a.seed, a.sweep, vtx);
+                                        c.ter = ~(uint32_t)k;
+                                        c.lab = lab;
+                                        c.mult = 1;
+                                        merge_best(sb, c);
+                                    }
+                                }
                             }
                         }
                     }
@@ -2581,10 +2596,15 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 sg = (int)__reduce_add_sync(0xffffffffu, (unsigned)sg);
                 if (lane == 0 && sg) atomicAdd(&s_single, sg);
                 __syncthreads();
+                if constexpr (WM != kUnit) sb = block_merge(sb);
             }
             Best<A> b = table_argmax<WM, TIE, TBITS, NW>(tab->t, tab->touched, nt, tid, a.seed, a.sweep, vtx, &s_arg);
             const bool last_pass = single && s_sp == 0;
-            if (b.mult > 1 || !last_pass) {
+            // (weighted singletons: a tie in weight with the table's winner needs its
+            // first arc -- resolve it)
+            const bool wsing = WM != kUnit && two && sb.mult > 0;
+            const bool force = wsing && nt > 0 && sb.w == b.w;
+            if (b.mult > 1 || !last_pass || force) {
                 // earliest arc (scan order) whose label carries the pass maximum
                 if (tid == 0) s_first = ~0ull;
                 __syncthreads();
@@ -2625,6 +2645,12 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 b.lab = (int32_t)(uint32_t)f;
                 b.ter = ~(uint32_t)(f >> 32);
                 b.mult = 1;
+            }
+            if (wsing) {
+                if (nt == 0)
+                    b = sb;
+                else
+                    merge_best(b, sb);
             }
             merge_best(overall, b);
             distinct += nt;
@@ -2707,7 +2733,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
             int2 bk = make_int2(0, -1);
             if (item.P > 1 && a.hb_off) bk = a.hb_off[item.cb + item.q];
             best = row_best(beg, d, vtx, item.P == 1, agg, distinct, bk, (uint32_t)item.P);
-            if (item.P == 1 && two && tid == 0 && s_single > 0) {
+            if (WM == kUnit && item.P == 1 && two && tid == 0 && s_single > 0) {
                 if (best.w < A(2))
                     s_fb = 1;
                 else if (best.w2 < A(1))
@@ -2745,7 +2771,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                             msingle += __ldcg(&src->single);
                             merge_best(best, o);
                         }
-                        if (two && msingle > 0) {
+                        if (WM == kUnit && two && msingle > 0) {
                             if (best.w < A(2))
                                 s_fb = 1;
                             else if (best.w2 < A(1))

@@ -281,6 +281,7 @@ def test_malformed_csr_rejected_on_upload(gpu):
     {"LP_MID_MAX": "0"},                          # no thread-per-row mid-degree kernel
     {"LP_MARK_BITMAP": "0"},                      # marks always queued by scanning
     {"LP_ID_SINGLE_W": "0", "LP_ID_SINGLE_RANDOM": "0"},  # singletons for unit weights / scan ties only
+    {"LP_TWO_TEAM_W": "0"},                       # weighted team rows insert every label
     {"LP_MID_HASH": "0"},                         # mid-degree rows by O(d^2) compares
     {"LP_HUB_BUCKET": "1", "LP_FIRST_EST_MIN": "16", "LP_FIRST_EST_DIV": "64"},  # hub buckets, low estimates
 ])
