@@ -1872,9 +1872,9 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
                           : 0;
         a.two_team = a.id_single && (g->wmode == kUnit || (g->wmode == kFixed && g->two_team_w));
         // (the first round's low label estimates serve the next round's singleton
-        // tallies; a synchronous weighted schedule has none -- its second sweep's
-        // diverse weighted labels then overflow the small tables: measured slower)
-        a.first_est_div = (g->wmode == kFixed && !cross) ? 1 : g->first_est_div;
+        // tallies of unit weights; with weights the labels stay diverse and the
+        // small tables overflow: measured slower, so weighted rows estimate d)
+        a.first_est_div = g->wmode == kFixed ? 1 : g->first_est_div;
         if (int rc = solve_sweep(g, a, cross, run_round, kGatherRak, &prof, &rounds, &gathered, first_ids || first_random,
                                  carry, first_random))
             return rc;
