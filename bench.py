@@ -9,11 +9,28 @@ aggregated over all ranks.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config rmat22|rmat22w|planted|grid] [--non-strict]
-                    [--batches B]
+                    [--batches B] [--no-configs] [--no-parity]
 
---impl reference times the reference's CPU path restated in C (the OpenMP
-port of rak._rak_par in oracle/lp_oracle.c; the Python reference cannot
-travel to the GPU box) on all host cores, same graph / metric / unit.
+The line also carries
+  parity      -- the timed run's labels, per-sweep changed counts and
+                 iteration count against the CPU oracle's restatement of the
+                 same schedule (oracle/lp_oracle.c, pinned to the reference's
+                 own outputs), and modularity / community count against it;
+  modes       -- the synchronous schedule and non-strict ties on the same
+                 graph, each with its parity;
+  configs     -- the other BASELINE RAK configs (R-MAT-22 float32 weights,
+                 planted n=100k strict and non-strict, 4096^2 grid): device
+                 time, GTEPS, step roofline fraction and parity;
+  cpu_baseline-- the reference's deterministic mode (rak_detect(strict,
+                 workers=1) = the sequential sweep, restated in C) on one
+                 host core, on the same graph.
+
+--impl reference times the reference's CPU path on all host cores: the
+OpenMP C port of rak._rak_par (oracle/lp_oracle.c; the Python reference
+cannot travel to the GPU box), on a graph built by the oracle's own
+generators (oracle/graphs.py -- the product library is never loaded), with
+the CSR conversion and the visit order prepared outside the timed region as
+the reference does (rak.py:171-172).
 
 Multi-GPU (torchrun): replicas only -- each rank runs the full detection on
 its own copy of the graph, no collective on the data path (DESIGN.md §6);
@@ -23,12 +40,12 @@ value = all ranks' edges / max-over-ranks device time.
 from __future__ import annotations
 
 import argparse
+import concurrent.futures as cf
 import ctypes as C
 import json
 import os
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -47,8 +64,22 @@ CONFIGS = {
                  tolerance=0.05, max_iterations=50),
 }
 
+METRIC = "RAK GTEPS on R-MAT-22 (dense-equivalent: edge_count x sweeps / time)"
 
-def make_graph(name: str):
+# oracle tie codes (oracle/oracle.py)
+OR_SCAN_FIRST, OR_RANDOM, OR_XORSHIFT = 0, 1, 3
+
+
+def make_graph(name: str, host_only: bool = False):
+    """The config's graph: the product generators (GPU / native builders) for
+    our arm, the oracle's independent generators for the reference arm (the
+    same arrays; tests/test_oracle_graphs.py)."""
+    if host_only:
+        from oracle import graphs as OG
+
+        if name not in OG.BENCH_GRAPHS:
+            raise SystemExit(f"unknown config {name}")
+        return OG.BENCH_GRAPHS[name]()
     from paper_2301_09125_b200 import synth
 
     if name == "rmat22":
@@ -60,6 +91,19 @@ def make_graph(name: str):
     if name == "grid":
         return synth.road_grid(4096, seed=1)
     raise SystemExit(f"unknown config {name}")
+
+
+def bench_config(args, g, world: int) -> dict:
+    """The `config` object: identical in both arms."""
+    cfg = CONFIGS[args.config]
+    return {"workload": args.config, "desc": cfg["desc"],
+            "mode": "non-strict" if args.non_strict else "strict",
+            "schedule": "reference visit order (sequential sweep)" if args.batches == 0 else f"{args.batches} batches",
+            "tolerance": cfg["tolerance"], "max_iterations": cfg["max_iterations"], "seed": args.seed,
+            "vertices": int(g.vertex_count), "arcs": int(g.edge_count),
+            "l2": ("inputs larger than L2 (int32 CSR %.0f MB vs 126 MB L2)" if 4 * g.edge_count > 126e6 else
+                   "inputs fit in L2 (int32 CSR %.0f MB vs 126 MB L2); no flush") % (4 * g.edge_count / 1e6),
+            "parallelism": f"replicas x{world}"}
 
 
 def algorithmic_bytes(vertices: int, arcs: int, weighted: bool) -> int:
@@ -106,6 +150,17 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -116,6 +171,7 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.lines = []
 
     def __enter__(self):
         try:
@@ -189,47 +245,178 @@ def whole_job_gteps(arcs_per_rank: int, ms_max: float, world: int) -> float:
     return world * arcs_per_rank / (ms_max / 1e3) / 1e9
 
 
+def ncom(labels) -> int:
+    return int(np.unique(labels).size)
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+def product_library_loaded() -> bool:
+    """Whether this process mapped liblabelprop_cuda.so (the reference arm
+    must not)."""
+    try:
+        with open("/proc/self/maps") as f:
+            return any("liblabelprop_cuda" in line for line in f)
+    except OSError:
+        return False
+
+
 def run_reference(args, world, rank):
-    """CPU arm: OpenMP port of the reference's _rak_par on all host cores."""
+    """The reference's CPU path on all host cores: the OpenMP port of
+    rak._rak_par (chunks of 1024 positions of the seeded order, per-thread
+    tallies; rak.py:119-158), plus one run of its deterministic mode
+    (workers=1, the sequential _rak_seq) on one core.  Rank 0 only."""
     if rank != 0:
         return
     from oracle import oracle as O
 
     cfg = CONFIGS[args.config]
-    g = make_graph(args.config)
+    g = make_graph(args.config, host_only=True)
+    prep = O.prepare(g)  # CSR conversion outside the clock, as rak.py:171-172
+    order = O.shuffled_indices(g.vertex_count, args.seed)
     threads = os.cpu_count() or 1
     strict = not args.non_strict
+    kw = dict(strict=strict, seed=args.seed, tolerance=cfg["tolerance"], max_iterations=cfg["max_iterations"],
+              threads=threads, order=order)
     for _ in range(args.warmup):
-        O.rak_par(g, strict=strict, seed=args.seed, tolerance=cfg["tolerance"], max_iterations=cfg["max_iterations"],
-                  threads=threads)
-    arcs = 0
+        O.rak_par(prep, **kw)
+    arcs, it = 0, 0
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        lab, it = O.rak_par(g, strict=strict, seed=args.seed, tolerance=cfg["tolerance"],
-                            max_iterations=cfg["max_iterations"], threads=threads)
+        lab, it = O.rak_par(prep, **kw)
         arcs += g.edge_count * it
     dt = time.perf_counter() - t0
     gteps = arcs / dt / 1e9
+    q_par = O.modularity(prep, lab)
+    # the deterministic mode (rak_detect(strict=True, workers=1)): one core
+    t1 = time.perf_counter()
+    slab, sit, _ = O.rak(prep, batches=0, tie=OR_SCAN_FIRST if strict else OR_XORSHIFT, seed=args.seed,
+                         tolerance=cfg["tolerance"], max_iterations=cfg["max_iterations"], order=order)
+    st = time.perf_counter() - t1
+    model = cpu_model()
     line = {
         "impl": "reference",
-        "metric": "RAK GTEPS on R-MAT-22 (dense-equivalent: edge_count x sweeps / time)",
-        "value": gteps, "unit": "GTEPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64 tally / int64 labels", "data": "synthetic",
-        "config": {"workload": args.config, "desc": cfg["desc"], "mode": "strict" if strict else "non-strict",
-                   "tolerance": cfg["tolerance"], "max_iterations": cfg["max_iterations"],
-                   "vertices": g.vertex_count, "arcs": g.edge_count},
-        "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} full RAK detections (rak._rak_par restated in C, OpenMP, "
-                                   f"{threads} threads, chunk 1024)"},
+        "metric": METRIC, "value": gteps, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 tally / int64 labels", "data": "synthetic",
+        "config": bench_config(args, g, world),
+        "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": threads, "kind": "port", "cpu": model,
+                         "sample": f"{args.steps} full RAK detections ({it} sweeps each) of rak._rak_par restated in C "
+                                   f"(OpenMP, {threads} threads, 1024-position chunks); CSR and order prepared "
+                                   f"outside the timed region"},
         "e2e": {"value": gteps, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "iterations": int(it),
+        "iterations": int(it), "modularity": q_par, "communities": ncom(lab),
+        "sequential": {"value": g.edge_count * sit / st / 1e9, "unit": "GTEPS", "cores": 1, "cpu": model,
+                       "ms_per_run": st * 1e3, "iterations": int(sit),
+                       "what": "the reference's deterministic mode (rak_detect strict, workers=1 = _rak_seq, "
+                               "rak.py:87-116) restated in C, one core, one detection",
+                       "modularity": O.modularity(prep, slab), "communities": ncom(slab)},
+        "graph": "built by oracle/graphs.py",
+        "product_library_loaded": product_library_loaded(),
     }
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def _oracle_tie(tie_rule: str) -> int:
+    return {"scan-first": OR_SCAN_FIRST, "random": OR_RANDOM, "min-label": 2}[tie_rule]
+
+
+class Detector:
+    """One uploaded graph + a way to run and read back a detection."""
+
+    def __init__(self, g, local):
+        from paper_2301_09125_b200 import _lib
+
+        self.g = g
+        self.L = _lib.lib()
+        self._lib = _lib
+        self.dg = _lib.DeviceGraph(g, device=local)
+
+    def run(self, opts, stats=None, changed=None):
+        """One detection through the C-ABI (lp_rak_run: labels = ids, the
+        seeded order; final labels downloaded after the timed sweeps)."""
+        st = stats if stats is not None else self._lib.RunStats()
+        self.out = np.empty(self.g.vertex_count, dtype=np.int64)
+        self._lib.check(self.L.lp_rak_run(self.dg.handle, C.byref(opts), None, None, self._lib.ptr(self.out),
+                                          self._lib.ptr(changed), C.byref(st)))
+        return st
+
+    def labels(self):
+        return self.out
+
+    def modularity(self):
+        from paper_2301_09125_b200 import quality
+
+        return quality.modularity_gpu(self.g, None, device_graph=self.dg)
+
+    def close(self):
+        self.dg.close()
+
+
+def timed_runs(det, params, runs: int):
+    """Warm once, then `runs` detections; device ms per run from the
+    library's CUDA events (inputs resident).  Returns a result record with
+    the last run's labels and changed counts."""
+    import paper_2301_09125_b200 as lp
+
+    o = lp.rak._opts(params)
+    det.run(o)
+    tms, it = 0.0, 0
+    changed = np.zeros(params.max_iterations, dtype=np.int64)
+    for _ in range(runs):
+        st = det.run(o, changed=changed)
+        tms += st.kernel_ms
+        it = int(st.iterations)
+    return {"ms": tms / runs, "iterations": it, "changed": changed[:it].copy(), "labels": det.labels(),
+            "q": det.modularity(), "rounds": int(st.rounds)}
+
+
+def parity_jobs(pool, prep, order, params, rec):
+    """Oracle runs checking one of our results: the same schedule and tie
+    rule (bit-exact), plus, for non-strict ties, the reference's own
+    xorshift draws (modularity within 1e-3, communities within 1%)."""
+    from oracle import oracle as O
+
+    kw = dict(batches=params.batches, seed=params.seed, tolerance=params.tolerance,
+              max_iterations=params.max_iterations, order=order)
+    jobs = {"same": pool.submit(O.rak, prep, tie=_oracle_tie(params.tie_rule), **kw)}
+    if params.tie_rule == "random":
+        jobs["xorshift"] = pool.submit(O.rak, prep, tie=OR_XORSHIFT, **kw)
+    return jobs
+
+
+def parity_record(prep, rec, jobs):
+    from oracle import oracle as O
+
+    lab, it, ch = jobs["same"].result()
+    q_ref = O.modularity(prep, lab)
+    out = {"labels_equal_oracle": bool(np.array_equal(rec["labels"], lab)),
+           "iterations_equal": int(it) == rec["iterations"],
+           "changed_equal": bool(np.array_equal(np.asarray(ch), rec["changed"])),
+           "q_ours": rec["q"], "q_ref": q_ref, "ncom_ours": ncom(rec["labels"]), "ncom_ref": ncom(lab),
+           "oracle": "oracle/lp_oracle.c or_rak, same schedule and tie rule"}
+    if "xorshift" in jobs:
+        xl, xit, _ = jobs["xorshift"].result()
+        qx, nx = O.modularity(prep, xl), ncom(xl)
+        out["reference_rng"] = {"q_ref": qx, "ncom_ref": nx, "dq": abs(rec["q"] - qx),
+                                "ncom_rel": abs(ncom(rec["labels"]) - nx) / max(nx, 1),
+                                "within_1e-3_and_1pct": abs(rec["q"] - qx) <= 1e-3
+                                and abs(ncom(rec["labels"]) - nx) <= 0.01 * nx,
+                                "what": "the reference's own non-strict draws (xorshift stream in visit order, "
+                                        "rak.py:71-83) restated in C: no parallel schedule can replay them, so "
+                                        "modularity / community count are compared"}
+    return out
+
+
 def run_ours(args, world, rank, local):
     import paper_2301_09125_b200 as lp
+    from oracle import oracle as O
     from paper_2301_09125_b200 import _lib
 
     cfg = CONFIGS[args.config]
@@ -239,7 +426,8 @@ def run_ours(args, world, rank, local):
     t_gen = time.perf_counter() - t_gen
     params = lp.RakParams(strict=not args.non_strict, seed=args.seed, tolerance=cfg["tolerance"],
                           max_iterations=cfg["max_iterations"], batches=args.batches)
-    dg = _lib.DeviceGraph(g, device=local)
+    det = Detector(g, local)
+    dg = det.dg
     opts = lp.rak._opts(params)
     # per-launch CUDA events (the roofline's kernel times) cost ~0.6 ms per
     # detection: the K timed steps run without them, K more steps with them
@@ -303,7 +491,7 @@ def run_ours(args, world, rank, local):
         except Exception:
             traffic = None
     # whole-step roofline: SURVEY §8 d4 bytes of the dense sweeps / device time
-    sweep_bytes = sum(algorithmic_bytes(g.vertex_count, g.edge_count, weighted) * p["iterations"] for p in per)
+    sweep_bytes = sum(algorithmic_bytes(g.vertex_count, g.edge_count, weighted) * p["iterations"] for p in per_t)
     total_kernel_ms = sum(k["ms"] for k in kernels.values())
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -311,62 +499,108 @@ def run_ours(args, world, rank, local):
         "bytes_model": kt["model"], "peak_source": peak_src, "frac_of_8TBs": achieved / 8000.0,
         "step_achieved_gbs": sweep_bytes / (dt_ms / 1e3) / 1e9,
         "step_frac": sweep_bytes / (dt_ms / 1e3) / 1e9 / peak,
+        "step_bytes_model": "SURVEY §8 d4: (12 n + %d m) bytes per sweep x sweeps" % (12 if weighted else 8),
         "kernel_share": {k: v["ms"] / max(total_kernel_ms, 1e-9) for k, v in kernels.items()},
     }
 
-    # modularity of the final labels (untimed, the reference's parity metric), on the device
-    from paper_2301_09125_b200 import quality
-
-    q_ours = quality.modularity_gpu(g, None, device_graph=dg)
+    # the main run's result (untimed): labels + per-sweep changed counts
+    main = timed_runs(det, params, 1)
+    main["ms"] = dt_ms / args.steps
 
     # the other schedules / tie rules on the same graph (device time, inputs resident)
-    modes = {}
+    mode_recs = {}
     if not args.no_modes:
         for name, kw in (("synchronous_strict", dict(batches=1, strict=True)),
                          ("exact_nonstrict", dict(batches=0, strict=False))):
             mp = lp.RakParams(seed=args.seed, tolerance=cfg["tolerance"], max_iterations=cfg["max_iterations"], **kw)
-            mo = lp.rak._opts(mp)
-            st = _lib.RunStats()
-            _lib.check(L.lp_rak_run_resident(dg.handle, C.byref(mo), None, C.byref(st)))  # warm
-            tms, arcs_m = 0.0, 0
-            for _ in range(3):
-                st = _lib.RunStats()
-                _lib.check(L.lp_rak_run_resident(dg.handle, C.byref(mo), None, C.byref(st)))
-                tms += st.kernel_ms
-                arcs_m += g.edge_count * st.iterations
-            modes[name] = {"gteps": arcs_m / (tms * 1e-3) / 1e9, "ms_per_run": tms / 3, "iterations": int(st.iterations),
-                           "modularity": quality.modularity_gpu(g, None, device_graph=dg)}
+            mode_recs[name] = (mp, timed_runs(det, mp, 3))
+    det.close()
 
     line = {
-        "metric": "RAK GTEPS on R-MAT-22 (dense-equivalent: edge_count x sweeps / time)",
-        "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None,
         "dtype": "int32 labels / u32 counts" if not weighted else "int32 labels / u64 fixed-point sums",
         "data": "synthetic",
-        "config": {"workload": args.config, "desc": cfg["desc"],
-                   "mode": "strict (scan-first ties)" if not args.non_strict else "non-strict (counter-RNG ties)",
-                   "schedule": "reference visit order (exact async)" if args.batches == 0 else f"{args.batches} batches",
-                   "tolerance": cfg["tolerance"], "max_iterations": cfg["max_iterations"],
-                   "vertices": g.vertex_count, "arcs": g.edge_count,
-                   "l2": "inputs larger than L2 (int32 CSR %.0f MB vs 126 MB L2)" % (4 * g.edge_count / 1e6),
-                   "parallelism": f"replicas x{world}"},
+        "config": bench_config(args, g, world),
         "iterations": per_t[-1]["iterations"], "rounds": per_t[-1]["rounds"],
         "arcs_scanned_per_step": per[-1]["arcs_scanned"], "arcs_dense_per_step": per_t[-1]["arcs_dense"],
         "gpu_launches": int(sum(p["launches"] for p in per_t)),
         "kernel_events": "kernel times (roofline) from K more steps run with per-launch CUDA events on the "
                           "library's streams right after the timed region (the events cost ~0.6 ms per step)",
         "roofline": roofline,
-        "modularity": q_ours,
-        "modes": modes,
+        "modularity": main["q"],
         "graph_gen_s": t_gen,
+        "clocks": clk.summary(),
     }
+
+    # the other BASELINE configs: device time, roofline fraction, parity
+    extra = []
+    if world == 1 and args.config == "rmat22" and not args.no_configs:
+        for name, strict in (("rmat22w", True), ("planted", True), ("planted", False), ("grid", True)):
+            c = CONFIGS[name]
+            eg = make_graph(name)
+            ep = lp.RakParams(strict=strict, seed=args.seed, tolerance=c["tolerance"],
+                              max_iterations=c["max_iterations"])
+            edet = Detector(eg, local)
+            rec = timed_runs(edet, ep, 3)
+            edet.close()
+            extra.append((name + ("" if strict else "_nonstrict"), eg, ep, rec))
+
+    # CPU side: the reference's deterministic mode on one core (timed alone),
+    # then every parity check in parallel (the oracle releases the GIL)
+    parity_on = rank == 0 and not args.no_parity
+    if parity_on or (rank == 0 and world == 1 and not args.no_cpu_baseline):
+        prep = O.prepare(g)
+        order = O.shuffled_indices(g.vertex_count, args.seed)
+        threads = os.cpu_count() or 1
+        with cf.ThreadPoolExecutor(max_workers=max(1, threads // 2)) as pool:
+            if world == 1 and not args.no_cpu_baseline:
+                t0 = time.perf_counter()
+                slab, sit, sch = O.rak(prep, batches=0, tie=OR_SCAN_FIRST if params.strict else OR_XORSHIFT,
+                                       seed=args.seed, tolerance=cfg["tolerance"],
+                                       max_iterations=cfg["max_iterations"], order=order)
+                sdt = time.perf_counter() - t0
+                line["cpu_baseline"] = {
+                    "value": g.edge_count * sit / sdt / 1e9, "unit": "GTEPS", "cores": 1, "kind": "port",
+                    "cpu": cpu_model(),
+                    "sample": f"1 full detection ({sit} sweeps, {sdt:.2f} s) in the reference's deterministic mode "
+                              f"(rak_detect strict, workers=1 = _rak_seq, rak.py:87-116) restated in C, one core, "
+                              f"same graph and visit order",
+                    "modularity": O.modularity(prep, slab), "communities": ncom(slab)}
+            if parity_on:
+                jobs = parity_jobs(pool, prep, order, params, main)
+                mjobs = {k: parity_jobs(pool, prep, order, mp, rec) for k, (mp, rec) in mode_recs.items()}
+                eprep = {}
+                ejobs = {}
+                for name, eg, ep, rec in extra:
+                    eprep[name] = O.prepare(eg)
+                    eorder = O.shuffled_indices(eg.vertex_count, ep.seed)
+                    ejobs[name] = parity_jobs(pool, eprep[name], eorder, ep, rec)
+                line["parity"] = parity_record(prep, main, jobs)
+                line["modes"] = {}
+                for k, (mp, rec) in mode_recs.items():
+                    line["modes"][k] = {"gteps": g.edge_count * rec["iterations"] / (rec["ms"] * 1e-3) / 1e9,
+                                        "ms_per_run": rec["ms"], "iterations": rec["iterations"],
+                                        "rounds": rec["rounds"], "modularity": rec["q"],
+                                        "step_frac": algorithmic_bytes(g.vertex_count, g.edge_count, weighted)
+                                        * rec["iterations"] / (rec["ms"] * 1e-3) / 1e9 / peak,
+                                        "parity": parity_record(prep, rec, mjobs[k])}
+                line["configs"] = {}
+                for name, eg, ep, rec in extra:
+                    w = name.startswith("rmat22w")
+                    line["configs"][name] = {
+                        "gteps": eg.edge_count * rec["iterations"] / (rec["ms"] * 1e-3) / 1e9,
+                        "ms_per_run": rec["ms"], "iterations": rec["iterations"], "rounds": rec["rounds"],
+                        "vertices": eg.vertex_count, "arcs": eg.edge_count,
+                        "mode": "strict" if ep.strict else "non-strict",
+                        "step_frac": algorithmic_bytes(eg.vertex_count, eg.edge_count, w) * rec["iterations"]
+                        / (rec["ms"] * 1e-3) / 1e9 / peak,
+                        "parity": parity_record(eprep[name], rec, ejobs[name])}
+    extra = None
 
     if not args.no_e2e:
         line["e2e"] = e2e(args, g, params, world, local)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, g, cfg)
-        line["cpu_baseline"]["modularity"] = line["cpu_baseline"].pop("_q")
-    line["clocks"] = clk.summary()
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -411,25 +645,11 @@ def e2e(args, g, params, world, local):
     finally:
         for a in arrays:
             L.lp_host_unregister(_lib.ptr(a))
-    return {"value": whole_job_gteps(arcs, dt * 1e3, world), "unit": "GTEPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": dt / steps * 1e3, "steps": steps,
+    return {"value": whole_job_gteps(arcs, dt * 1e3, world), "unit": "GTEPS", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": dt / steps * 1e3, "steps": steps,
             "what": "rak_labels() on a freshly uploaded graph each step: CSR H2D from pinned host memory "
                     "(int64 offsets/neighbours as the reference's Graph holds them), plan build, sweeps, "
                     "int64 labels D2H"}
-
-
-def cpu_baseline(args, g, cfg):
-    from oracle import oracle as O
-
-    threads = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    lab, it = O.rak_par(g, strict=not args.non_strict, seed=args.seed, tolerance=cfg["tolerance"],
-                        max_iterations=cfg["max_iterations"], threads=threads)
-    dt = time.perf_counter() - t0
-    return {"value": g.edge_count * it / dt / 1e9, "unit": "GTEPS", "cores": threads, "kind": "port",
-            "sample": f"1 full RAK detection ({it} sweeps) on the same graph, rak._rak_par restated in C "
-                      f"(OpenMP, {threads} threads, 1024-vertex chunks), {dt:.2f} s",
-            "_q": O.modularity(g, lab)}
 
 
 def main():
@@ -445,6 +665,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity checks")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other BASELINE configs")
     ap.add_argument("--no-modes", action="store_true", help="skip the secondary schedule / tie-rule timings")
     ap.add_argument("--no-kernel-events", action="store_true",
                     help="time the steps without per-launch events (no kernel roofline)")

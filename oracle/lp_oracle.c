@@ -602,3 +602,125 @@ double or_modularity(int64_t n, const int64_t* off, const int64_t* nbr, const do
     free(dc);
     return q;
 }
+
+/* ------------------------------------------------------------------------
+ * Benchmark graphs, built without the product library (bench.py's reference
+ * arm and the generator cross-checks in tests/test_oracle_graphs.py).  The
+ * reference ships no R-MAT / planted / grid generator;
+ * these restate the seeded recipes of DESIGN.md §5 independently of the
+ * product's native builders, and the canonical CSR form of the reference's
+ * preprocess(from_arcs(...)) (graph.py:58-84,254-306: symmetric, duplicate
+ * pairs merged, generated self-loops dropped, one unit self-loop per vertex,
+ * rows sorted by neighbour id).
+ * ---------------------------------------------------------------------- */
+
+static inline uint64_t or_splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+/* R-MAT pair i: bit level l (high to low) draws a 53-bit uniform from
+ * splitmix64(key ^ 64 i + l) and takes quadrant a | b | c | d. */
+int or_gen_rmat_pairs(int32_t scale, int64_t edges, double a, double b, double c, uint64_t seed, int64_t* src,
+                      int64_t* dst) {
+    if (scale < 1 || scale > 30 || edges < 0) return -1;
+    const double two53 = 9007199254740992.0;
+    const uint64_t t1 = (uint64_t)(a * two53), t2 = (uint64_t)((a + b) * two53), t3 = (uint64_t)((a + b + c) * two53);
+    const uint64_t key = or_splitmix64(seed ^ 0x524D4154ull);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < edges; ++i) {
+        uint64_t row = 0, col = 0;
+        for (int l = scale - 1; l >= 0; --l) {
+            const uint64_t r = or_splitmix64((key ^ ((uint64_t)i << 6)) + (uint64_t)l) >> 11;
+            /* quadrants: [0,a) top-left, [a,a+b) top-right, [a+b,a+b+c) bottom-left, rest bottom-right */
+            const uint64_t down = r >= t2;
+            const uint64_t right = (r >= t1 && r < t2) || r >= t3;
+            row |= down << l;
+            col |= right << l;
+        }
+        src[i] = (int64_t)row;
+        dst[i] = (int64_t)col;
+    }
+    return 0;
+}
+
+/* LSD radix sort of 64-bit keys, 11-bit digits, skipping digits that are
+ * constant over the input. */
+static int radix_sort_u64(uint64_t* keys, int64_t count) {
+    uint64_t* tmp = (uint64_t*)malloc((size_t)(count > 0 ? count : 1) * sizeof(uint64_t));
+    if (!tmp) return -1;
+    uint64_t *src = keys, *dst = tmp;
+    for (int shift = 0; shift < 64; shift += 11) {
+        int64_t hist[2048];
+        memset(hist, 0, sizeof(hist));
+        for (int64_t i = 0; i < count; ++i) ++hist[(src[i] >> shift) & 2047];
+        int constant = 0;
+        for (int d = 0; d < 2048; ++d)
+            if (hist[d] == count) constant = 1;
+        if (constant) continue;
+        int64_t run = 0;
+        for (int d = 0; d < 2048; ++d) {
+            int64_t h = hist[d];
+            hist[d] = run;
+            run += h;
+        }
+        for (int64_t i = 0; i < count; ++i) dst[hist[(src[i] >> shift) & 2047]++] = src[i];
+        uint64_t* t = src;
+        src = dst;
+        dst = t;
+    }
+    if (src != keys) memcpy(keys, src, (size_t)count * sizeof(uint64_t));
+    free(tmp);
+    return 0;
+}
+
+/* Canonical unit-weight CSR of an undirected pair list.  neighbors must
+ * hold 2 * pairs + n entries; returns the arc count, or -1 on bad input /
+ * allocation failure. */
+int64_t or_csr_undirected(int64_t n, int64_t pairs, const int64_t* u, const int64_t* v, int64_t* offsets,
+                          int64_t* neighbors) {
+    if (n < 0 || n >= ((int64_t)1 << 31) || pairs < 0) return -1;
+    uint64_t* keys = (uint64_t*)malloc((size_t)(pairs > 0 ? pairs : 1) * sizeof(uint64_t));
+    if (!keys) return -1;
+    int64_t k = 0;
+    for (int64_t i = 0; i < pairs; ++i) {
+        if (u[i] < 0 || v[i] < 0 || u[i] >= n || v[i] >= n) {
+            free(keys);
+            return -1;
+        }
+        if (u[i] == v[i]) continue; /* generated self-loops dropped */
+        const uint64_t lo = (uint64_t)(u[i] < v[i] ? u[i] : v[i]), hi = (uint64_t)(u[i] < v[i] ? v[i] : u[i]);
+        keys[k++] = (lo << 32) | hi;
+    }
+    if (radix_sort_u64(keys, k)) {
+        free(keys);
+        return -1;
+    }
+    int64_t uniq = 0;
+    for (int64_t i = 0; i < k; ++i)
+        if (uniq == 0 || keys[i] != keys[uniq - 1]) keys[uniq++] = keys[i];
+    for (int64_t r = 0; r <= n; ++r) offsets[r] = 0;
+    for (int64_t i = 0; i < uniq; ++i) {
+        ++offsets[(keys[i] >> 32) + 1];
+        ++offsets[(keys[i] & 0xFFFFFFFFull) + 1];
+    }
+    for (int64_t r = 0; r < n; ++r) offsets[r + 1] += offsets[r] + 1; /* + the self-loop */
+    /* Row r holds its smaller neighbours, itself, then its larger ones.  In
+     * (lo, hi) order the pairs with a given hi arrive by ascending lo and
+     * those with a given lo by ascending hi, so three passes fill every row
+     * in ascending neighbour order. */
+    int64_t* fill = (int64_t*)malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+    if (!fill) {
+        free(keys);
+        return -1;
+    }
+    for (int64_t r = 0; r < n; ++r) fill[r] = offsets[r];
+    for (int64_t i = 0; i < uniq; ++i) neighbors[fill[keys[i] & 0xFFFFFFFFull]++] = (int64_t)(keys[i] >> 32);
+    for (int64_t r = 0; r < n; ++r) neighbors[fill[r]++] = r;
+    for (int64_t i = 0; i < uniq; ++i) neighbors[fill[keys[i] >> 32]++] = (int64_t)(keys[i] & 0xFFFFFFFFull);
+    free(fill);
+    free(keys);
+    return offsets[n];
+}

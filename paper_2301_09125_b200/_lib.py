@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import subprocess
+import weakref
 
 import numpy as np
 
@@ -259,10 +260,37 @@ class DeviceGraph:
             pass
 
 
+# Device copies of immutable ``Graph`` objects, keyed by id() and dropped when
+# the Graph is collected (weakref.finalize) or released explicitly.  Kept
+# outside the Graph so Graph objects stay picklable / deep-copyable like the
+# reference's (graph.py:34-50) and carry no GPU state.
+_DEVICE_CACHE: dict = {}
+
+
+def _drop(key: int) -> None:
+    dg = _DEVICE_CACHE.pop(key, None)
+    if dg is not None:
+        dg.close()
+
+
 def device_graph(graph) -> DeviceGraph:
     """The cached device copy of an immutable ``Graph`` (uploaded once)."""
-    dg = graph.__dict__.get("_lp_device_graph")
-    if dg is None or dg.handle is None:
+    key = id(graph)
+    dg = _DEVICE_CACHE.get(key)
+    if dg is None or dg.handle is None or dg.owner() is not graph:
         dg = DeviceGraph(graph)
-        object.__setattr__(graph, "_lp_device_graph", dg)
+        dg.owner = weakref.ref(graph)
+        _DEVICE_CACHE[key] = dg
+        weakref.finalize(graph, _drop, key)
     return dg
+
+
+def release_device_graph(graph) -> bool:
+    """Free the device copy of ``graph`` (CSR, plans, route buffers) now
+    instead of when the Graph is collected.  Returns whether one existed."""
+    key = id(graph)
+    dg = _DEVICE_CACHE.get(key)
+    if dg is None or dg.owner() is not graph:
+        return False
+    _drop(key)
+    return True

@@ -1024,8 +1024,10 @@ static void cached_shuffle(int64_t n, uint32_t seed, int64_t* out) {
     std::memcpy(out, c_order.data(), (size_t)n * sizeof(int64_t));
 }
 
-// Device copy of the last shuffled order per device (kept for the process).
-static int device_shuffle(lp_graph* g, int64_t n, uint32_t seed, const int64_t** out) {
+// Device copy of the last shuffled order per device (kept for the process),
+// copied into `dst` on the handle's stream and completed while the lock is
+// held (another thread may replace the shared copy right after).
+static int device_shuffle(lp_graph* g, int64_t n, uint32_t seed, int64_t* dst) {
     struct Entry {
         int64_t n = -1;
         uint32_t seed = 0;
@@ -1055,7 +1057,8 @@ static int device_shuffle(lp_graph* g, int64_t n, uint32_t seed, const int64_t**
         e.n = n;
         e.seed = seed;
     }
-    *out = e.d;
+    LP_CK(cudaMemcpyAsync(dst, e.d, (size_t)n * sizeof(int64_t), cudaMemcpyDeviceToDevice, g->stream));
+    LP_CK(cudaStreamSynchronize(g->stream));
     return LP_OK;
 }
 
@@ -1079,12 +1082,6 @@ static int build_plan(lp_graph* g, int kind, const int64_t* order_host, uint32_t
     free_plan(P);
     // the visit order on the device: identity (INDEX), the caller's, or
     // shuffled_indices(n, seed) from the process-wide device cache
-    const int64_t* order_dev = nullptr;
-    if (index) {
-        order_dev = nullptr;  // generated on the device below
-    } else if (!custom) {
-        if (int rc = device_shuffle(g, n, seed, &order_dev)) return rc;
-    }
     cudaStream_t st = g->stream;
     LP_CK(cudaEventRecord(g->ev0, st));
     int64_t bytes = 0;
@@ -1100,12 +1097,13 @@ static int build_plan(lp_graph* g, int kind, const int64_t* order_host, uint32_t
     LP_CK(dalloc(&t.iota, n, &tmpb));
     LP_CK(dalloc(&t.sdeg, n + 1, &tmpb));
     LP_CK(dalloc(&t.deg, n, &tmpb));
-    if (custom)
+    if (custom) {
         LP_CK(cudaMemcpyAsync(t.order, order_host, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    else if (order_dev)
-        LP_CK(cudaMemcpyAsync(t.order, order_dev, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-    else
+    } else if (!index) {
+        if (int rc = device_shuffle(g, n, seed, t.order)) return rc;
+    } else {
         k_iota64<<<g->num_sms * 8, 256, 0, st>>>(t.order, n);
+    }
     LP_CK(cudaMemsetAsync(g->counters, 0, 8 * sizeof(unsigned long long), st));
     LP_CK(cudaMemsetAsync(P.pos, 0xff, n * sizeof(int32_t), st));
     const int G = g->num_sms * 8;
@@ -1402,10 +1400,12 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
             const unsigned long long bad = g->h_counters[4 + 1];
             const int emin = (int)g->h_counters[4 + 2] - 2048, emax = (int)g->h_counters[4 + 3] - 2048;
             // fixed point: w * 2^shift is an integer < 2^32 for every float32 weight when
-            // shift = 24 - emin and (emax - emin + 24) <= 32; row sums stay < 2^64
+            // shift = 24 - emin and (emax - emin + 24) <= 32.  The integer row sums equal
+            // the reference's float64 sums (rak.py:105) only while those are exact, i.e.
+            // every partial sum fits the 53-bit significand: span + ceil(log2(degree)) <= 53
             const int span = emax - emin + 24;
-            const double deg_bits = std::log2((double)std::max<int64_t>(2, g->max_degree));
-            if (bad == 0 && span <= 32 && span + deg_bits < 63.0) {
+            const int deg_bits = (int)std::ceil(std::log2((double)std::max<int64_t>(2, g->max_degree)));
+            if (bad == 0 && span <= 32 && span + deg_bits <= 53) {
                 g->wmode = kFixed;
                 g->fixed_shift = 24 - emin;
             } else {
@@ -1882,6 +1882,8 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
                               st));
         LP_CK(cudaStreamSynchronize(st));
         LP_CK(cudaGetLastError());
+        if (g->h_counters[kCtrError])
+            return lp_fail(LP_ERR_UNSUPPORTED, "a hub row's label partitions overflowed the team table split stack");
         const int64_t changed = (int64_t)g->h_counters[kCtrChanged];
         if (changed_per_iter) changed_per_iter[it - 1] = changed;
         last_changed = changed;
@@ -2335,6 +2337,8 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
         LP_CK(cudaGetLastError());
         if (g->h_counters[kCtrCount + 1])
             return lp_fail(LP_ERR_UNSUPPORTED, "a row has more distinct labels than the team tables hold");
+        if (g->h_counters[kCtrError])
+            return lp_fail(LP_ERR_UNSUPPORTED, "a hub row's label partitions overflowed the team table split stack");
         const int64_t changed = (int64_t)g->h_counters[kCtrChanged];
         if (changed_per_iter) changed_per_iter[it - 1] = changed;
         std::swap(c0, c1);  // c0 = this sweep's state

@@ -183,7 +183,8 @@ constexpr uint32_t kEarlier = 1u, kLater = 2u;
 // counters: [0] changed delta (reset per sweep), [1] label writes (reset per
 // round), [4+k] arcs scanned and [8+k] vertices evaluated by kernel k
 // (k = 0 hub team, 1 8-warp team, 2 warp, 3 small; accumulated over a run)
-enum { kCtrChanged = 0, kCtrWrites = 1, kCtrGathered = 2, kCtrArcs = 4, kCtrVerts = 8, kCtrCount = 12 };
+// [14] kernel-side failures (a team table split stack exhausted): the run fails
+enum { kCtrChanged = 0, kCtrWrites = 1, kCtrGathered = 2, kCtrArcs = 4, kCtrVerts = 8, kCtrError = 14, kCtrCount = 15 };
 
 // ndist[s]: low 30 bits = distinct labels seen at the last evaluation;
 // kMajBit = that evaluation's winner held a strict majority of the row's
@@ -2537,10 +2538,16 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 for (int h = tid; h < HB; h += NT) tab->t.init(h);
                 __syncthreads();
                 if (tid == 0) {
-                    for (int j = 3; j >= 0; --j) {
-                        s_stack[s_sp][0] = parts * 4;
-                        s_stack[s_sp][1] = want * 4 + j;
-                        ++s_sp;
+                    if (s_sp + 4 > STACK || parts >= (1u << 28)) {
+                        // no room for another 4-way split: fail the run loudly
+                        // (the engine checks kCtrError after every sweep)
+                        atomicAdd(a.counters + kCtrError, 1ull);
+                    } else {
+                        for (int j = 3; j >= 0; --j) {
+                            s_stack[s_sp][0] = parts * 4;
+                            s_stack[s_sp][1] = want * 4 + j;
+                            ++s_sp;
+                        }
                     }
                 }
                 single = false;

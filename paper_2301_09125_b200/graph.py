@@ -39,9 +39,9 @@ class Graph:
     weights: np.ndarray
     total_weight: float
 
-    # Device handles keyed by weight flavour live here so a graph is uploaded
-    # once and reused across runs (the dataclass is frozen, so the cache is
-    # attached through object.__setattr__ by the CUDA layer).
+    # The device copy (uploaded once, reused across runs) is cached by the
+    # CUDA layer outside the object (_lib.device_graph), so a Graph stays
+    # picklable and holds no GPU state.
 
 
 def _ro(a: np.ndarray) -> np.ndarray:

@@ -370,3 +370,20 @@ def test_cli_detect_and_sweep(gpu, tmp_path, capsys):
                      "--modes", "strict", "--batches-grid", "0,1", "--extended"]) == 0
     lines = capsys.readouterr().out.splitlines()
     assert lines[0].endswith(",batches,edges_scanned,gteps") and len(lines) == 3
+
+
+def test_graph_stays_picklable_and_device_copy_releasable(gpu):
+    """the device copy is cached outside the Graph (the reference's
+    Graph pickles and deep-copies; so must ours after a detection)."""
+    import copy
+    import pickle
+
+    g = lp.ring_of_cliques(6, 5)
+    first = lp.rak_detect(g, lp.RakParams(strict=True, seed=2))
+    g2 = pickle.loads(pickle.dumps(g))
+    assert lp.graphs_equal(g, g2) and lp.graphs_equal(g, copy.deepcopy(g))
+    assert np.array_equal(lp.rak_detect(g2, lp.RakParams(strict=True, seed=2)).assignment, first.assignment)
+    assert lp.release_device_graph(g) is True
+    assert lp.release_device_graph(g) is False
+    again = lp.rak_detect(g, lp.RakParams(strict=True, seed=2))  # re-uploads
+    assert np.array_equal(again.assignment, first.assignment)
