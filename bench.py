@@ -121,6 +121,10 @@ def kernel_table(per, weighted):
     from paper_2301_09125_b200 import _lib
 
     out = {}
+    fused = all(p.get("flags", 0) & _lib.STATS_FUSED for p in per)
+    # fused rounds: the tally kernels read the neighbour index and gather its
+    # label (SURVEY §8 d4's per-arc bytes); two-phase: they read lbuf
+    per_arc = (8 if fused else 4) + (4 if weighted else 0)
     for b, name in enumerate(_lib.BIN_NAMES):
         ms = sum(p["bin_ms"][b] for p in per)
         if ms <= 0:
@@ -128,8 +132,10 @@ def kernel_table(per, weighted):
         arcs = sum(p["bin_arcs"][b] for p in per)
         verts = sum(p["bin_vertices"][b] for p in per)
         out[f"tally_{name}"] = {"ms": ms, "launches": sum(p["bin_launches"][b] for p in per),
-                                "bytes": (8 if weighted else 4) * arcs + 12 * verts,
-                                "model": "(4 B label%s per arc) + 12 B per vertex" % (" + 4 B weight" if weighted else "")}
+                                "bytes": per_arc * arcs + 12 * verts,
+                                "model": "(%s%s per arc) + 12 B per vertex" % (
+                                    "4 B index + 4 B neighbour-label gather" if fused else "4 B label",
+                                    " + 4 B weight" if weighted else "")}
     gms = sum(p["gather_ms"] for p in per)
     if gms > 0:
         out["k_gather"] = {"ms": gms, "launches": sum(p["gather_launches"] for p in per),

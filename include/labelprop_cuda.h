@@ -140,8 +140,10 @@ typedef struct lp_run_stats {
     double gather_ms;       /* LP_RAK_PROFILE: phase-1 label gather time    */
     int64_t arcs_gathered;  /* arcs whose neighbour label phase 1 gathered  */
     int64_t gather_launches;
-    int64_t reserved[1];
+    int64_t flags;          /* LP_STATS_FUSED: the tally kernels gathered the
+                               neighbour labels themselves (no phase 1)    */
 } lp_run_stats;
+#define LP_STATS_FUSED 1
 
 /* Upload a CSR graph.  offsets[n+1], neighbors[m] (int64, rows sorted by
  * neighbour id -- graph.py:39-41), weights[m] float64 or NULL (= all 1).

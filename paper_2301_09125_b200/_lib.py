@@ -87,6 +87,7 @@ class CopraOpts(C.Structure):
 
 
 RAK_PROFILE = 1
+STATS_FUSED = 1  # lp_run_stats.flags: labels gathered inside the tally kernels
 BIN_NAMES = ("hub", "team", "warp", "small")
 
 
@@ -108,7 +109,7 @@ class RunStats(C.Structure):
         ("gather_ms", C.c_double),
         ("arcs_gathered", C.c_int64),
         ("gather_launches", C.c_int64),
-        ("reserved", C.c_int64 * 1),
+        ("flags", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -26,7 +26,12 @@ enum TieRule : int { kScanFirst = 0, kRandom = 1, kMinLabel = 2 };
 template <int WM> struct Acc;
 template <> struct Acc<kUnit> { using T = uint32_t; };
 template <> struct Acc<kFixed> { using T = unsigned long long; };
-template <> struct Acc<kFloat> { using T = float; };
+// kFloat: weights that are not float32-exact fixed point (stored as float32)
+// are summed in float64 -- exact for any row whose weights span less than
+// 2^(29 - log2(degree)) in magnitude, so the sums (and ties) do not depend
+// on the atomics' order: deterministic, like the reference's float64 tally
+// (rak.py:105)
+template <> struct Acc<kFloat> { using T = double; };
 
 __host__ __device__ __forceinline__ uint32_t fmix32(uint32_t x) {
     x ^= x >> 16;
@@ -109,11 +114,13 @@ __device__ __forceinline__ unsigned long long shfl_u64(unsigned long long v, int
 }
 __device__ __forceinline__ uint32_t shfl_idx_any(uint32_t v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 __device__ __forceinline__ float shfl_idx_any(float v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ double shfl_idx_any(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 __device__ __forceinline__ unsigned long long shfl_idx_any(unsigned long long v, int src) {
     return __shfl_sync(0xffffffffu, v, src);
 }
 __device__ __forceinline__ uint32_t shfl_xor_any(uint32_t v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
 __device__ __forceinline__ float shfl_xor_any(float v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+__device__ __forceinline__ double shfl_xor_any(double v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
 __device__ __forceinline__ unsigned long long shfl_xor_any(unsigned long long v, int m) { return shfl_u64(v, m); }
 
 template <typename A> __device__ __forceinline__ Cand<A> warp_best(Cand<A> c) {

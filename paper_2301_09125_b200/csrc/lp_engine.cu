@@ -127,6 +127,9 @@ struct Plan {
     int64_t flags_bs = -1;           // batch size the snbr flags were computed for
     int32_t bin_beg[kNumBins + 1] = {0, 0, 0, 0, 0, 0};  // slot range of each bin (idle: [.., n))
     int32_t big_end = 0;             // slots [0, big_end) are big rows, [big_end, S) small
+    // arcs of the rows longer than 16 / than mid_max: big rows come first in
+    // storage order, by descending degree, so each is a prefix of the arcs
+    int64_t arcs_gt16 = 0, arcs_gt_mid = 0;
     // visit order (position -> vertex) and the dense-wave lengths
     int32_t* vorder = nullptr;
     int32_t* wave_len = nullptr;     // [kMaxWaves] device
@@ -145,6 +148,7 @@ struct lp_graph {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaStream_t aux[2] = {nullptr, nullptr};  // concurrent tally kernels of a round
     cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+    cudaEvent_t ev_route = nullptr, ev_gather = nullptr;  // dense route / phase-1 gather done (round())
     int64_t n = 0, m = 0;
     int64_t max_degree = 0;
     int64_t sliceable = 0;  // rows long enough to be cut into slices
@@ -160,6 +164,9 @@ struct lp_graph {
     int pk = kPlanRak;  // the plan the current run uses
     Plan& plan() { return plans[pk]; }
     // run state
+    bool l2_persist = true;  // persisting L2 window over the label arrays (set_l2_window)
+    int fuse_maxd = 16;      // RAK rows of degree <= this gather their labels in the tally kernel
+                             // (EvalArgs::fused); >= 2^30: every row (LP_FUSE_MAXD, -1 = all)
     int32_t* labA = nullptr;
     int32_t* labB = nullptr;
     int32_t* cur = nullptr;  // the buffer holding the latest labels
@@ -402,6 +409,15 @@ __global__ void k_plan_keys(const uint32_t* __restrict__ off, const int32_t* __r
     }
     __syncthreads();
     if (threadIdx.x < kNumBins && sc[threadIdx.x]) atomicAdd(counts + threadIdx.x, sc[threadIdx.x]);
+}
+
+// first slot of [0, big_end) (rows by descending degree) whose degree is <= maxd
+__global__ void k_first_short(const uint32_t* __restrict__ soff, int32_t big_end, int maxd, int32_t* first) {
+    for (int32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < big_end; s += gridDim.x * blockDim.x) {
+        const bool shortrow = (int)(soff[s + 1] - soff[s]) <= maxd;
+        const bool prev_long = s == 0 || (int)(soff[s] - soff[s - 1]) > maxd;
+        if (shortrow && prev_long) atomicMin(first, s);
+    }
 }
 
 __global__ void k_plan_vorder(const int32_t* __restrict__ pos, int32_t* __restrict__ vorder, int64_t n) {
@@ -731,32 +747,22 @@ template <int WM, int TIE> struct Launcher {
         const Plan& P = g->plan();
         const int sms = g->num_sms;
         cudaStream_t st = g->stream;
-        // ---- phase 1: gather every evaluated row's neighbour labels ----
-        prof->begin(st, kKGather);
-        if (alg == kGatherSlpa) {
-            if (dense)
-                k_gather_pieces<kGatherSlpa><<<grid_for(P.npieces, 32 * 8, sms * 16), 256, 0, st>>>(
-                    a, P.dslot, P.dk0, P.dcount, a.r.len + kGatherCursor);
-            else
-                k_gather_pieces<kGatherSlpa><<<grid_for(h_len[kLenGather], 32 * 8, sms * 16), 256, 0, st>>>(
-                    a, a.r.gslot, a.r.gk0, a.r.len + kLenGather, a.r.len + kGatherCursor);
-        } else if (dense) {
-            k_gather_dense<<<grid_for(P.m_active, 256 * 8, sms * 16), 256, 0, st>>>(a, P.m_active);
-        } else {
-            k_gather_pieces<kGatherRak><<<grid_for(h_len[kLenGather], 32 * 8, sms * 16), 256, 0, st>>>(
-                a, a.r.gslot, a.r.gk0, a.r.len + kLenGather, a.r.len + kGatherCursor);
-        }
-        prof->end(st);
-        // ---- phase 2: route and tally ----
-        if (dense && P.big_end > 0) {
-            prof->begin(st, -1);
-            k_route_dense<<<grid_for(P.big_end, 256, sms * 8), 256, 0, st>>>(a, 0, P.big_end);
-            prof->end(st);
-        }
+        // Fused gathers (RAK): rows of degree <= fuse_maxd gather their
+        // neighbour labels inside the tally kernel (arc_label); the phase-1 pass
+        // covers only the longer rows, which come first in storage order.
+        const bool rak = alg == kGatherRak;
+        const bool fuse_all = rak && g->fuse_maxd >= (1 << 30);
+        const bool fuse_small = rak && g->fuse_maxd >= kSmallMax;
+        const bool fuse_mid = rak && a.mid_max > 0 && g->fuse_maxd >= a.mid_max;
+        const int64_t gather_arcs = fuse_all ? 0 : fuse_mid ? P.arcs_gt_mid : fuse_small ? P.arcs_gt16 : P.m_active;
+        EvalArgs af = a, ag = a;  // fused / two-phase launches
+        af.fused = 1;
+        ag.fused = fuse_all ? 1 : 0;
         // The tally kernels of a round are independent except for the spill chain
         // warp<0> -> warp<1> -> team (overflowing rows move up a class), so they
         // run on three streams: the chain on the handle's stream, the small and
         // mid rows and team2 on aux[0], the hubs on aux[1]; their tails overlap.
+        // Fused small rows start at once, beside the phase-1 gather.
         // (Running the routed lists of the chain concurrently and the spills
         // afterwards, on a fourth stream, measured slower: the kernels share the
         // SMs' shared memory, the round is throughput-bound.)
@@ -764,68 +770,115 @@ template <int WM, int TIE> struct Launcher {
         cudaEventRecord(g->ev_fork, st);
         cudaStreamWaitEvent(sB, g->ev_fork, 0);
         cudaStreamWaitEvent(sC, g->ev_fork, 0);
-        // small rows, one launch per degree class (MAXD 16, 8, 4)
-        for (int c = 0; c < 3; ++c) {
-            const int bin = kBinS16 + c;
-            const int list = kLenS16 - c;
-            const int64_t cnt = dense ? (P.bin_beg[bin + 1] - P.bin_beg[bin]) : h_len[list];
-            if (cnt <= 0) continue;
-            const int32_t sb = dense ? P.bin_beg[bin] : -1, se = dense ? P.bin_beg[bin + 1] : -1;
-            a.bin = kKSmall;
-            prof->begin(sB, kKSmall);
-            const int grid = grid_for(cnt, 256, sms * 8);
-            if (c == 0)
-                k_small<WM, TIE, 16><<<grid, 256, 0, sB>>>(a, sb, se);
-            else if (c == 1)
-                k_small<WM, TIE, 8><<<grid, 256, 0, sB>>>(a, sb, se);
+        auto small_rows = [&](const EvalArgs& sa) {
+            // small rows, one launch per degree class (MAXD 16, 8, 4)
+            for (int c = 0; c < 3; ++c) {
+                const int bin = kBinS16 + c;
+                const int list = kLenS16 - c;
+                const int64_t cnt = dense ? (P.bin_beg[bin + 1] - P.bin_beg[bin]) : h_len[list];
+                if (cnt <= 0) continue;
+                const int32_t sb = dense ? P.bin_beg[bin] : -1, se = dense ? P.bin_beg[bin + 1] : -1;
+                EvalArgs b = sa;
+                b.bin = kKSmall;
+                prof->begin(sB, kKSmall);
+                const int grid = grid_for(cnt, 256, sms * 8);
+                if (c == 0)
+                    k_small<WM, TIE, 16><<<grid, 256, 0, sB>>>(b, sb, se);
+                else if (c == 1)
+                    k_small<WM, TIE, 8><<<grid, 256, 0, sB>>>(b, sb, se);
+                else
+                    k_small<WM, TIE, 4><<<grid, 256, 0, sB>>>(b, sb, se);
+                prof->end(sB);
+            }
+        };
+        if (fuse_small) small_rows(af);
+        // ---- route the big rows (dense rounds) ----
+        if (dense && P.big_end > 0) {
+            prof->begin(st, -1);
+            k_route_dense<<<grid_for(P.big_end, 256, sms * 8), 256, 0, st>>>(a, 0, P.big_end);
+            prof->end(st);
+        }
+        cudaEventRecord(g->ev_route, st);
+        // ---- phase 1: gather the neighbour labels of the two-phase rows ----
+        if (alg == kGatherSlpa) {
+            prof->begin(st, kKGather);
+            if (dense)
+                k_gather_pieces<kGatherSlpa><<<grid_for(P.npieces, 32 * 8, sms * 16), 256, 0, st>>>(
+                    a, P.dslot, P.dk0, P.dcount, a.r.len + kGatherCursor);
             else
-                k_small<WM, TIE, 4><<<grid, 256, 0, sB>>>(a, sb, se);
-            prof->end(sB);
+                k_gather_pieces<kGatherSlpa><<<grid_for(h_len[kLenGather], 32 * 8, sms * 16), 256, 0, st>>>(
+                    a, a.r.gslot, a.r.gk0, a.r.len + kLenGather, a.r.len + kGatherCursor);
+            prof->end(st);
+        } else if (fuse_all) {
+        } else if (dense) {
+            if (gather_arcs > 0) {
+                prof->begin(st, kKGather);
+                k_gather_dense<<<grid_for(gather_arcs, 256 * 8, sms * 16), 256, 0, st>>>(a, gather_arcs);
+                prof->end(st);
+            }
+        } else if (h_len[kLenGather] > 0) {
+            prof->begin(st, kKGather);
+            k_gather_pieces<kGatherRak><<<grid_for(h_len[kLenGather], 32 * 8, sms * 16), 256, 0, st>>>(
+                a, a.r.gslot, a.r.gk0, a.r.len + kLenGather, a.r.len + kGatherCursor);
+            prof->end(st);
+        }
+        cudaEventRecord(g->ev_gather, st);
+        // ---- phase 2: tally ----
+        if (!fuse_small) {
+            cudaStreamWaitEvent(sB, g->ev_gather, 0);
+            small_rows(ag);
         }
         const bool big = dense && P.big_end > 0;
         if (a.mid_max > 0 && (big || h_len[kLenMid] > 0)) {
-            a.bin = kKSmall;
+            cudaStreamWaitEvent(sB, fuse_mid ? g->ev_route : g->ev_gather, 0);
+            EvalArgs b = fuse_mid ? af : ag;
+            b.bin = kKSmall;
             prof->begin(sB, kKSmall);
             bool hashed = false;
             if constexpr (WM == kUnit) {
                 if (g->mid_hash) {
                     const int grid = dense ? sms * occ_midh : grid_for(h_len[kLenMid], kMidHThreads, sms * occ_midh);
-                    k_midh<TIE><<<grid, kMidHThreads, mid_hash_smem_bytes(), sB>>>(a);
+                    k_midh<TIE><<<grid, kMidHThreads, mid_hash_smem_bytes(), sB>>>(b);
                     hashed = true;
                 }
             }
             if (!hashed) {
                 const int grid = dense ? sms * occ_mid : grid_for(h_len[kLenMid], kMidThreads, sms * occ_mid);
-                k_mid<WM, TIE><<<grid, kMidThreads, mid_smem_bytes<WM>(), sB>>>(a);
+                k_mid<WM, TIE><<<grid, kMidThreads, mid_smem_bytes<WM>(), sB>>>(b);
             }
             prof->end(sB);
         }
-        if (big || h_len[kLenWarp] > 0) launch_warp<0>(g, a, h_len[kLenWarp], dense, prof, st);
+        if (big || h_len[kLenWarp] > 0) launch_warp<0>(g, ag, h_len[kLenWarp], dense, prof, st);
         // each class may spill into the next one: launch on any upstream work
         if (big || h_len[kLenWarp] + h_len[kLenWarpBig] > 0)
-            launch_warp<1>(g, a, h_len[kLenWarp] + h_len[kLenWarpBig], dense, prof, st);
+            launch_warp<1>(g, ag, h_len[kLenWarp] + h_len[kLenWarpBig], dense, prof, st);
         if (big || (h_len[kLenWarp] + h_len[kLenWarpBig] + h_len[kLenTeam]) > 0) {
-            a.bin = kKTeam;
+            EvalArgs b = ag;
+            b.bin = kKTeam;
             prof->begin(st, kKTeam);
             k_team<WM, TIE, kTeamThreads, kTeamBits, false>
-                <<<sms * occ_team, kTeamThreads, team_smem_bytes<WM, kTeamBits>(), st>>>(a, kLenTeam);
+                <<<sms * occ_team, kTeamThreads, team_smem_bytes<WM, kTeamBits>(), st>>>(b, kLenTeam);
             prof->end(st);
         }
         if (big || h_len[kLenTeam2] > 0) {
-            a.bin = kKTeam;
+            cudaStreamWaitEvent(sB, g->ev_gather, 0);
+            EvalArgs b = ag;
+            b.bin = kKTeam;
             prof->begin(sB, kKTeam);
             const int grid = dense ? sms * occ_team2 : grid_for(h_len[kLenTeam2], 1, sms * occ_team2);
             k_team<WM, TIE, kTeam2Threads, kTeam2Bits, true>
-                <<<grid, kTeam2Threads, team_smem_bytes<WM, kTeam2Bits>(), sB>>>(a, kLenTeam2);
+                <<<grid, kTeam2Threads, team_smem_bytes<WM, kTeam2Bits>(), sB>>>(b, kLenTeam2);
             prof->end(sB);
         }
         if (big || h_len[kLenHub] > 0) {
-            a.bin = kKHub;
+            cudaStreamWaitEvent(sC, g->ev_gather, 0);
+            EvalArgs b = ag;
+            b.bin = kKHub;
             prof->begin(sC, kKHub);
-            if (a.hb_off) k_hub_bucket<<<sms * 2, 1024, 0, sC>>>(a);
+            if (b.hb_off) k_hub_bucket<<<sms * 2, 1024, 0, sC>>>(b);
             const int grid = dense ? sms * occ_hub : grid_for(h_len[kLenHub], 1, sms * occ_hub);
             k_team<WM, TIE, kHubThreads, kHubBits, true>
-                <<<grid, kHubThreads, team_smem_bytes<WM, kHubBits>(), sC>>>(a, kLenHub);
+                <<<grid, kHubThreads, team_smem_bytes<WM, kHubBits>(), sC>>>(b, kLenHub);
             prof->end(sC);
         }
         cudaEventRecord(g->ev_join[0], sB);
@@ -945,8 +998,7 @@ static void destroy_graph(lp_graph* g) {
     dfree(g->off);
     dfree(g->nbr);
     dfree(g->w);
-    dfree(g->labA);
-    dfree(g->labB);
+    dfree(g->labA);  // (labB lives in the same allocation)
     dfree(g->mark);
     dfree(g->gap);
     dfree(g->chg);
@@ -967,6 +1019,8 @@ static void destroy_graph(lp_graph* g) {
         if (g->ev_join[i]) cudaEventDestroy(g->ev_join[i]);
     }
     if (g->ev_fork) cudaEventDestroy(g->ev_fork);
+    if (g->ev_route) cudaEventDestroy(g->ev_route);
+    if (g->ev_gather) cudaEventDestroy(g->ev_gather);
     delete g;
 }
 
@@ -1141,7 +1195,23 @@ static int build_plan(lp_graph* g, int kind, const int64_t* order_host, uint32_t
     LP_CK(cub::DeviceScan::ExclusiveSum(g->cub_tmp, need2, t.sdeg, P.soff, (int)(P.S + 1), st));
     uint32_t m_active = 0;
     LP_CK(cudaMemcpyAsync(&m_active, P.soff + P.S, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    LP_CK(cudaStreamSynchronize(st));
+    {
+        // arcs of the rows longer than 16 / than mid_max (prefixes of the storage order)
+        int32_t* first = reinterpret_cast<int32_t*>(g->counters + 8);
+        const int32_t init = P.big_end;
+        LP_CK(cudaMemcpyAsync(first, &init, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        k_first_short<<<grid_for(P.big_end, 256, g->num_sms * 8), 256, 0, st>>>(P.soff, P.big_end,
+                                                                                 std::max(g->mid_max, kSmallMax), first);
+        uint32_t off2[2] = {0, 0};
+        int32_t fs = 0;
+        LP_CK(cudaMemcpyAsync(&fs, first, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        LP_CK(cudaMemcpyAsync(&off2[0], P.soff + P.big_end, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        LP_CK(cudaStreamSynchronize(st));
+        LP_CK(cudaMemcpyAsync(&off2[1], P.soff + fs, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        LP_CK(cudaStreamSynchronize(st));
+        P.arcs_gt16 = off2[0];
+        P.arcs_gt_mid = off2[1];
+    }
     P.m_active = m_active;
     LP_CK(dalloc(&P.snbr, P.m_active, &bytes));
     LP_CK(dalloc(&P.lbuf, P.m_active, &bytes));
@@ -1277,6 +1347,8 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     };
     if (cudaGetDevice(&g->device) != cudaSuccess) return fail(lp_fail(LP_ERR_CUDA, "cudaGetDevice failed"));
     cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device);
+    if (const char* ev = getenv("LP_L2_PERSIST")) g->l2_persist = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_FUSE_MAXD")) g->fuse_maxd = atoi(ev) < 0 ? (1 << 30) : atoi(ev);
     if (const char* ev = getenv("LP_WAVES")) g->waves = std::max(1, std::min(1024, atoi(ev)));
     if (const char* ev = getenv("LP_MARGIN")) g->margin_skip = atoi(ev) != 0;
     if (const char* ev = getenv("LP_DEBUG_ROUNDS")) g->debug_rounds = atoi(ev) != 0;
@@ -1330,6 +1402,8 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
         }
     }
     G_CK(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
+    G_CK(cudaEventCreateWithFlags(&g->ev_route, cudaEventDisableTiming));
+    G_CK(cudaEventCreateWithFlags(&g->ev_gather, cudaEventDisableTiming));
     StreamScope ss(g->stream);
     pool_keep(g->device);
     G_CK(cudaEventCreate(&g->ev0));
@@ -1337,8 +1411,9 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     cudaStream_t st = g->stream;
     G_CK(dalloc(&g->off, n + 1, &g->bytes));
     G_CK(dalloc(&g->nbr, m, &g->bytes));
-    G_CK(dalloc(&g->labA, n, &g->bytes));
-    G_CK(dalloc(&g->labB, n, &g->bytes));
+    // L0 / x side by side: one persisting L2 window covers both (set_l2_window)
+    G_CK(dalloc(&g->labA, 2 * n + 32, &g->bytes));
+    g->labB = g->labA + ((n + 31) & ~(int64_t)31);
     G_CK(dalloc(&g->mark, n + 4, &g->bytes));
     G_CK(dalloc(&g->gap, n + 4, &g->bytes));
     G_CK(dalloc(&g->chg, n / 32 + 2, &g->bytes));
@@ -1546,7 +1621,7 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
             LP_CK(cudaMemcpyAsync(g->h_len, g->routes.len, kLenCount * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
             LP_CK(cudaStreamSynchronize(st));
             a.horizon = (int32_t)std::min<int64_t>(g->n, (w + 1) * ws);
-            if (g->h_len[kLenGather] > 0) {
+            if (g->h_len[kLenRouted] > 0) {
                 run_round(g, a, false, g->h_len, prof, alg);
                 if (a.mark) mark_pass(INT64_MAX / 4, false);
             }
@@ -1582,12 +1657,12 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
                         g->h_len[kLenWarp], g->h_len[kLenWarpBig], g->h_len[kLenTeam], g->h_len[kLenTeam2],
                         g->h_len[kLenHub], g->h_len[kLenGather]);
             }
-            if (g->h_len[kLenGather] == 0) break;  // everything queued passed the margin test
+            if (g->h_len[kLenRouted] == 0) break;  // everything queued passed the margin test
             q ^= 1;
             a.mq_out = g->mq[q];
             a.mq_len = g->mq_len + q;
             LP_CK(cudaMemsetAsync(g->counters + kCtrWrites, 0, sizeof(unsigned long long), st));
-            if ((double)g->h_len[kLenGather] >= g->dense_frac * (double)P.npieces) {
+            if ((double)g->h_len[kLenRouted] >= g->dense_frac * (double)P.npieces) {
                 // most rows survived the margin test: a full round is cheaper than the
                 // routed frontier (the routes are dropped; every margin is refreshed)
                 LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
@@ -1711,6 +1786,44 @@ static int finish_stats(lp_graph* g, const Prof& prof, lp_run_stats* S, int it, 
     return LP_OK;
 }
 
+// Keep the two label arrays (L0 and x, 8 bytes per vertex: 33.6 MB for
+// R-MAT-22) resident in L2 while the round's index stream and label buffer
+// (1 GB per dense round) stream past them: a persisting access-policy window
+// on every stream the round's kernels run on, with the device's persisting
+// carve-out sized to the window.  The random neighbour-label gathers then hit
+// L2 instead of HBM.
+static void set_l2_window(lp_graph* g) {
+    if (!g->l2_persist || g->n == 0) return;
+    static std::mutex mu;
+    static int64_t limit_set[64] = {};
+    int max_window = 0, max_persist = 0;
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, g->device);
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, g->device);
+    if (max_window <= 0 || max_persist <= 0) return;
+    const size_t want = (size_t)(g->labB - g->labA + g->n) * sizeof(int32_t);
+    const size_t bytes = std::min(want, (size_t)max_window);
+    const size_t carve = std::min(bytes, (size_t)max_persist);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (limit_set[g->device & 63] < (int64_t)carve) {
+            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) != cudaSuccess) {
+                cudaGetLastError();
+                return;
+            }
+            limit_set[g->device & 63] = (int64_t)carve;
+        }
+    }
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.base_ptr = g->labA;
+    v.accessPolicyWindow.num_bytes = bytes;
+    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)carve / (double)bytes);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaStream_t sts[3] = {g->stream, g->aux[0], g->aux[1]};
+    for (cudaStream_t s : sts)
+        if (s && cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // RAK driver
 // ---------------------------------------------------------------------------
@@ -1739,6 +1852,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     const bool cross = bs < n;  // some vertex depends on an earlier batch
     if (int rc = ensure_flags(g, bs, &plan_ms)) return rc;
     S->plan_ms = plan_ms;
+    set_l2_window(g);
     Plan& P = g->plan();
     cudaStream_t st = g->stream;
     round_fn run_round = nullptr;
@@ -1781,7 +1895,11 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     // neighbour that changed since their last evaluation
     // (not with random ties: tie_hash is keyed by the sweep, so an unchanged
     // neighbourhood can still produce a different winner)
-    const bool track = g->sweep_frontier && o->tie != kRandom;
+    // (random ties: tie_hash is keyed by the sweep, so a vertex whose last
+    // evaluation tied may move with an unchanged neighbourhood; the margin
+    // array tells which ones tied, k_mark_ties queues them at the boundary)
+    const bool gap_ok = g->wmode != kFloat && g->margin_skip;
+    const bool track = g->sweep_frontier && (o->tie != kRandom || gap_ok);
     a.mark = (cross || track) ? g->mark : nullptr;
     a.gap = ((cross || track) && g->wmode != kFloat && g->margin_skip) ? g->gap : nullptr;
     a.mark_all = 0;
@@ -1810,6 +1928,11 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.warp_maxd[1] = g->warp_maxd[1];
     a.reg_est = g->reg_est;
     a.mid_max = g->mid_max > kSmallMax ? g->mid_max : 0;
+    a.fused = 0;  // (per launch: Launcher::round)
+    // fused row classes: k_small rows (d <= 16), k_mid rows (d <= mid_max), or all
+    a.fuse_maxd = g->fuse_maxd >= (1 << 30) ? INT32_MAX
+                  : (a.mid_max > 0 && g->fuse_maxd >= a.mid_max) ? a.mid_max
+                  : g->fuse_maxd >= kSmallMax ? kSmallMax : 0;
 
     LP_CK(cudaMemsetAsync(g->counters, 0, kCtrCount * sizeof(unsigned long long), st));
     Prof prof;
@@ -1841,8 +1964,9 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
                 // few changed rows: push from them (one atomic per neighbour)
                 k_sweep_changes<<<g->num_sms * 8, 256, 0, st>>>(a, L0, X, (int32_t)P.S);  // L0 = last result
                 a.mark_all = 1;
-                const EvalArgs b = marks_mode(g, a, last_changed);
+                const EvalArgs b = marks_mode(g, a, o->tie == kRandom ? g->n : last_changed);
                 k_mark_pieces<<<g->num_sms * 16, 256, 0, st>>>(b);
+                if (o->tie == kRandom) k_mark_ties<<<g->num_sms * 8, 256, 0, st>>>(b, (int32_t)P.S);
                 bits_to_queue(g, b);
                 a.mark_all = 0;
             } else {
@@ -1852,6 +1976,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
                 const EvalArgs b = marks_mode(g, a, last_changed);
                 k_pull_marks<<<g->num_sms * 16, 256, 0, st>>>(b, g->chg, P.dslot, P.dk0, P.dcount,
                                                              g->routes.len + kGatherCursor, 0);
+                if (o->tie == kRandom) k_mark_ties<<<g->num_sms * 8, 256, 0, st>>>(b, (int32_t)P.S);
                 bits_to_queue(g, b);
             }
             prof.end(st);
@@ -1898,13 +2023,14 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     g->labels_valid = true;
     if (int rc = finish_stats(g, prof, S, it, rounds, gathered, ms)) return rc;
     S->arcs_dense = g->m * it;
+    if (g->fuse_maxd >= (1 << 30)) S->flags |= LP_STATS_FUSED;
 #ifdef LP_PATH_STATS
     {
         unsigned long long h[8];
-        cudaMemcpy(h, g->counters + 16, sizeof(h), cudaMemcpyDeviceToHost);
+        cudaMemcpy(h, g->counters + 20, sizeof(h), cudaMemcpyDeviceToHost);
         fprintf(stderr, "[lp] k_warp paths: majority %llu, majority-miss %llu, register %llu, hashed %llu, "
                 "hashed-tied %llu, overflow %llu\n", h[0], h[5], h[1], h[2], h[3], h[4]);
-        cudaMemset(g->counters + 16, 0, sizeof(h));
+        cudaMemset(g->counters + 20, 0, sizeof(h));
     }
 #endif
     return LP_OK;
@@ -1982,6 +2108,7 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     const bool cross = bs < n;
     if (int rc = ensure_flags(g, bs, &plan_ms)) return rc;
     S->plan_ms = plan_ms;
+    set_l2_window(g);
     Plan& P = g->plan();
     cudaStream_t st = g->stream;
     round_fn run_round = nullptr;
@@ -2207,6 +2334,7 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
     const bool cross = bs < n;
     if (int rc = ensure_flags(g, bs, &plan_ms)) return rc;
     S->plan_ms = plan_ms;
+    set_l2_window(g);
     if (int rc = copra_buffers(g, K)) return rc;
     Plan& P = g->plan();
     cudaStream_t st = g->stream;

@@ -87,7 +87,8 @@ enum {
     kLenTeam2 = 17,    // 16-warp team, 8192-slot table (est <= kTeam2Est, d <= kTeamMaxDeg)
     kTeam2Cursor = 18,
     kLenMid = 19,      // thread per row, kSmallMax < d <= kMidMax (k_mid)
-    kLenCount = 20
+    kLenRouted = 20,   // pieces of every routed row, fused or not (the round-size decisions)
+    kLenCount = 21
 };
 
 struct Routes {
@@ -157,6 +158,11 @@ struct EvalArgs {
     int32_t* hb_lab;
     uint32_t* hb_pos;
     int2* hb_off;  // per partition item (cb + q): (bucket start, length); length -1 = not bucketed
+    // fused gather (RAK): the tally kernels read each arc's neighbour index and
+    // gather its label themselves (arc_label) instead of a phase-1 pass through
+    // lbuf -- 8 bytes per arc less DRAM traffic and no separate gather launch
+    int32_t fused = 0;
+    int32_t fuse_maxd = 0;  // rows of degree <= fuse_maxd are fused: routing adds no phase-1 pieces for them
 };
 
 // First sweep from labels = vertex ids (rak.py:168): a neighbour that has not
@@ -195,7 +201,7 @@ constexpr int32_t kMajBit = 1 << 30;
 __host__ __device__ __forceinline__ int32_t nd_count(int32_t v) { return v & (kMajBit - 1); }
 
 #ifdef LP_PATH_STATS
-#define LP_STAT(a, k) atomicAdd((a).counters + 16 + (k), 1ull)
+#define LP_STAT(a, k) atomicAdd((a).counters + 20 + (k), 1ull)  // (past COPRA's kCtrCount + 1)
 #else
 #define LP_STAT(a, k) \
     do {              \
@@ -239,7 +245,7 @@ template <int WM> __device__ __forceinline__ typename Acc<WM>::T arc_weight(cons
     } else if constexpr (WM == kFixed) {
         return (unsigned long long)__ldg(a.sw + e);
     } else {
-        return __uint_as_float(__ldg(a.sw + e));
+        return (double)__uint_as_float(__ldg(a.sw + e));
     }
 }
 
@@ -248,6 +254,16 @@ __device__ __forceinline__ int32_t gather_label(const EvalArgs& a, uint32_t nb) 
     const int32_t u = (int32_t)(nb >> 2);
     if (nb & kEarlier) return a.x[u];
     return a.id_single ? (u | kSingle) : __ldg(a.L0 + u);  // (first sweep: L0[u] == u)
+}
+
+// Label of arc e as the tally sees it: fused rounds gather it here (a read of x
+// may race with another row's write this round; the writer marks this row, so
+// the next round repeats the evaluation -- the fixed point is unchanged, and
+// the synchronous schedule reads only the immutable L0); two-phase rounds read
+// the phase-1 buffer.
+__device__ __forceinline__ int32_t arc_label(const EvalArgs& a, uint32_t e) {
+    if (a.fused) return gather_label(a, __ldg(a.snbr + e));
+    return a.lbuf[e];
 }
 
 __device__ __forceinline__ void flush_counters(const EvalArgs& a, long long dchg, long long arcs, long long writes,
@@ -272,7 +288,7 @@ __device__ __forceinline__ void flush_counters(const EvalArgs& a, long long dchg
 // 2 * winner - total, useful when the winner holds a strict majority).
 template <typename A> __device__ __forceinline__ void store_gap(const EvalArgs& a, int32_t s, A win, A total) {
     if (a.gap) {
-        if constexpr (std::is_same<A, float>::value) {
+        if constexpr (std::is_floating_point<A>::value) {
             a.gap[s] = 0ull;
         } else {
             a.gap[s] = (win + win > total) ? (unsigned long long)(win + win - total) : 0ull;
@@ -284,7 +300,7 @@ template <typename A> __device__ __forceinline__ void store_gap(const EvalArgs& 
 // runner-up (w2).
 template <typename A> __device__ __forceinline__ void store_lead(const EvalArgs& a, int32_t s, A w1, A w2) {
     if (a.gap) {
-        if constexpr (std::is_same<A, float>::value)
+        if constexpr (std::is_floating_point<A>::value)
             a.gap[s] = 0ull;
         else
             a.gap[s] = (unsigned long long)(w1 - w2);
@@ -549,6 +565,20 @@ __global__ void k_flags_from_changed(EvalArgs a, uint32_t* __restrict__ chg) {
 }
 
 // (whole warps: 32 consecutive vertices -> one bitmap word)
+// Random ties (non-strict): the winner among tied labels is drawn from a hash
+// keyed by the sweep, so a vertex whose last evaluation ended in a tie (lead 0)
+// may move although no neighbour changed.  At a sweep boundary those vertices
+// join the frontier next to the neighbours of the changed ones (a lead > 0
+// with an unchanged neighbourhood keeps its label: the draw is not consulted).
+__global__ void k_mark_ties(EvalArgs a, int32_t S) {
+    for (int32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
+        if (a.gap[s] != 0ull) continue;
+        const int32_t v = __ldg(a.svid + s);
+        atomicOr(a.mark + v, 1ull);  // (nonzero: queued by either compaction; +1 only widens the margin test)
+        if (a.mbits) atomicOr(a.mbits + (v >> 5), 1u << (v & 31));
+    }
+}
+
 __global__ void k_changed_flags(const int32_t* __restrict__ lnew, const int32_t* __restrict__ lold,
                                 uint32_t* __restrict__ chg, int64_t n) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -895,9 +925,14 @@ __global__ void k_route_queue(EvalArgs a, const int32_t* __restrict__ mq_in, con
             if (s >= 0) cls = route_class(a, s, est, d);
         }
         route_append(a, cls, s, est, d);
-        // phase-1 pieces of the routed row
-        const int np = cls >= 0 ? (d + kPieceArcs - 1) / kPieceArcs : 0;
+        // phase-1 pieces of the routed row (none for fused rows)
+        const int np_all = cls >= 0 ? (d + kPieceArcs - 1) / kPieceArcs : 0;
+        const int np = d > a.fuse_maxd ? np_all : 0;
         const uint32_t act = __activemask();
+        {
+            const unsigned routed = __reduce_add_sync(act, (unsigned)np_all);
+            if (routed && lane == __ffs(act) - 1) atomicAdd(a.r.len + kLenRouted, (int32_t)routed);
+        }
         int incl = np;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1207,7 +1242,7 @@ __global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, i
 #pragma unroll
         for (int k = 0; k < MAXD; ++k) {
             if (k < d) {
-                lab[k] = lb_strip(a, a.lbuf[beg + k]);
+                lab[k] = lb_strip(a, arc_label(a, beg + k));
                 w[k] = arc_weight<WM>(a, beg + k);
             } else {
                 lab[k] = kEmpty;
@@ -1301,7 +1336,7 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(EvalArgs a) {
             const int32_t nd = __ldg(a.ndist + s);
             A total = A(0);
             for (int k = 0; k < d; ++k) {
-                lab[k * kMidThreads] = lb_strip(a, __ldg(a.lbuf + beg + k));
+                lab[k * kMidThreads] = lb_strip(a, arc_label(a, beg + k));
                 const A w = arc_weight<WM>(a, beg + k);
                 if (WM != kUnit) wv[k * kMidThreads] = w;
                 total += w;
@@ -1396,7 +1431,7 @@ __global__ void __launch_bounds__(kMidHThreads) k_midh(EvalArgs a) {
             bool done = false;
             if (nd & kMajBit) {
                 int cw = 0;
-                for (int k = 0; k < d; ++k) cw += lb_strip(a, __ldg(a.lbuf + beg + k)) == xv;
+                for (int k = 0; k < d; ++k) cw += lb_strip(a, arc_label(a, beg + k)) == xv;
                 if (cw + cw > d) {  // strict majority: label unchanged
                     store_gap<A>(a, s, (A)cw, (A)d);
                     done = true;
@@ -1418,7 +1453,7 @@ __global__ void __launch_bounds__(kMidHThreads) k_midh(EvalArgs a) {
                 for (int k = 0; k < d; ++k) {
                     if ((k & (kB - 1)) == 0) {
 #pragma unroll
-                        for (int j = 0; j < kB; ++j) lv[j] = k + j < d ? __ldg(a.lbuf + beg + k + j) : 0;
+                        for (int j = 0; j < kB; ++j) lv[j] = k + j < d ? arc_label(a, beg + k + j) : 0;
                     }
                     int32_t lab = lv[0];
 #pragma unroll
@@ -1493,7 +1528,7 @@ __global__ void __launch_bounds__(1024) k_hub_bucket(EvalArgs a) {
         __syncthreads();
         for (int base = 0; base < d; base += blockDim.x) {
             const int k = base + tid;
-            const uint32_t part = k < d ? part_of(lb_strip(a, a.lbuf[beg + k]), P) : 0xffffffffu;
+            const uint32_t part = k < d ? part_of(lb_strip(a, arc_label(a, beg + k)), P) : 0xffffffffu;
             const uint32_t grp = __match_any_sync(0xffffffffu, part);
             if (part != 0xffffffffu && lane == __ffs(grp) - 1) atomicAdd(&cntp[part], __popc(grp));
         }
@@ -1509,7 +1544,7 @@ __global__ void __launch_bounds__(1024) k_hub_bucket(EvalArgs a) {
         __syncthreads();
         for (int base = 0; base < d; base += blockDim.x) {
             const int k = base + tid;
-            const int32_t lab = k < d ? a.lbuf[beg + k] : 0;  // (kSingle flags kept)
+            const int32_t lab = k < d ? arc_label(a, beg + k) : 0;  // (kSingle flags kept)
             const uint32_t part = k < d ? part_of(lb_strip(a, lab), P) : 0xffffffffu;
             const uint32_t grp = __match_any_sync(0xffffffffu, part);
             const int leader = __ffs(grp) - 1;
@@ -1647,7 +1682,9 @@ template <typename A> struct Best {
 };
 
 template <typename A> __device__ __forceinline__ A from_bits_any(unsigned long long b) {
-    if constexpr (std::is_same<A, float>::value)
+    if constexpr (std::is_same<A, double>::value)
+        return __longlong_as_double((long long)b);
+    else if constexpr (std::is_same<A, float>::value)
         return __uint_as_float((uint32_t)b);
     else
         return (A)b;
@@ -1708,7 +1745,9 @@ template <typename A> __device__ __forceinline__ Best<A> warp_merge(Best<A> b) {
 
 // Order-preserving 64-bit image of a (non-negative) weight, for max-reductions.
 template <typename A> __device__ __forceinline__ unsigned long long wbits(A w) {
-    if constexpr (std::is_same<A, float>::value)
+    if constexpr (std::is_same<A, double>::value)
+        return (unsigned long long)__double_as_longlong(w);  // (non-negative: order-preserving)
+    else if constexpr (std::is_same<A, float>::value)
         return (unsigned long long)__float_as_uint(w);
     else
         return (unsigned long long)w;
@@ -1851,7 +1890,7 @@ __device__ __forceinline__ int32_t all_singles_winner(const EvalArgs& a, uint32_
     unsigned long long bk = 0;
     int32_t bl = -1;
     for (int k = tid; k < d; k += NT) {
-        const int32_t lab = lb_strip(a, a.lbuf[beg + k]);
+        const int32_t lab = lb_strip(a, arc_label(a, beg + k));
         const unsigned long long key =
             ((unsigned long long)sec_of<TIE>(lab, a.seed, a.sweep, vtx) << 32) | (unsigned long long)(~(uint32_t)k);
         if (bl < 0 || key > bk) {
@@ -1994,7 +2033,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 && WM == k
 #pragma unroll
             for (int c = 0; c < U; ++c) {
                 const int k = c * 32 + lane;
-                nbr_next[c] = (k < d0) ? a.lbuf[beg0 + k] : kEmpty;
+                nbr_next[c] = (k < d0) ? arc_label(a, beg0 + k) : kEmpty;
             }
         }
         uint32_t chm = 0;  // batch vertices whose label changed (deferred marks)
@@ -2020,7 +2059,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 && WM == k
         }                                                                                       \
         _Pragma("unroll") for (int c_ = 0; c_ < U; ++c_) {                                      \
             const int k_ = nb_base + c_ * 32 + lane;                                            \
-            nbr_next[c_] = (k_ < nb_d) ? a.lbuf[nb_beg + k_] : kEmpty;                         \
+            nbr_next[c_] = (k_ < nb_d) ? arc_label(a, nb_beg + k_) : kEmpty;                   \
         }                                                                                       \
     } while (0)
             A total;
@@ -2066,7 +2105,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 && WM == k
 #pragma unroll
                 for (int c = 0; c < U; ++c) {
                     const int k = c * 32 + lane;
-                    nbr_next[c] = (k < d) ? a.lbuf[beg + k] : kEmpty;
+                    nbr_next[c] = (k < d) ? arc_label(a, beg + k) : kEmpty;
                 }
             }
             const int est = min(d, nd_count(nd) + (nd_count(nd) >> 2) + 16);
@@ -2290,7 +2329,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 && WM == k
                         bool ok = false;
                         int32_t lab = kEmpty;
                         if (k < d) {
-                            lab = a.lbuf[beg + k];
+                            lab = arc_label(a, beg + k);
                             if (TWO) lab = lb_strip(a, lab);
                             const int h = tab->t.find(lab);
                             ok = h >= 0 && tab->t.weight(h) == b.w && sec_of<TIE>(lab, a.seed, a.sweep, vtx) == b.sec;
@@ -2329,7 +2368,7 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 && WM == k
                         int first = -1;
                         for (int base = 0; base < d && first < 0; base += 32) {
                             const int k = base + lane;
-                            const bool hitw = k < d && lb_strip(a, a.lbuf[beg + k]) == winner;
+                            const bool hitw = k < d && lb_strip(a, arc_label(a, beg + k)) == winner;
                             const uint32_t hm = __ballot_sync(0xffffffffu, hitw);
                             if (hm) first = base + __ffs(hm) - 1;
                         }
@@ -2386,26 +2425,34 @@ template <int WM, int TBITS> struct TeamTable {
 };
 
 template <typename A> __device__ __forceinline__ unsigned long long to_bits(A w) {
-    if constexpr (std::is_same<A, float>::value)
+    if constexpr (std::is_same<A, double>::value)
+        return (unsigned long long)__double_as_longlong(w);  // (non-negative: order-preserving)
+    else if constexpr (std::is_same<A, float>::value)
         return (unsigned long long)__float_as_uint(w);
     else
         return (unsigned long long)w;
 }
 template <typename A> __device__ __forceinline__ A from_bits(unsigned long long b) {
-    if constexpr (std::is_same<A, float>::value)
+    if constexpr (std::is_same<A, double>::value)
+        return __longlong_as_double((long long)b);
+    else if constexpr (std::is_same<A, float>::value)
         return __uint_as_float((uint32_t)b);
     else
         return (A)b;
 }
 
 template <typename A> __device__ __forceinline__ void gacc_add(unsigned long long* acc, A w) {
-    if constexpr (std::is_same<A, float>::value)
+    if constexpr (std::is_same<A, double>::value)
+        atomicAdd(reinterpret_cast<double*>(acc), w);
+    else if constexpr (std::is_same<A, float>::value)
         atomicAdd(reinterpret_cast<float*>(acc), w);
     else
         atomicAdd(acc, (unsigned long long)w);
 }
 template <typename A> __device__ __forceinline__ A gacc_read(const unsigned long long* acc) {
-    if constexpr (std::is_same<A, float>::value)
+    if constexpr (std::is_same<A, double>::value)
+        return __ldcg(reinterpret_cast<const double*>(acc));
+    else if constexpr (std::is_same<A, float>::value)
         return __ldcg(reinterpret_cast<const float*>(acc));
     else
         return (A)__ldcg(acc);
@@ -2504,7 +2551,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                             }
                         }
                     } else if (k < d) {
-                        lab = a.lbuf[beg + k];
+                        lab = arc_label(a, beg + k);
                         w = arc_weight<WM>(a, beg + k);
                         if (two && (lab & kSingle)) lab = kEmpty;  // (two passes: looked up below)
                         else if (parts > 1 && part_of(lb_strip(a, lab), parts) != want) lab = kEmpty;
@@ -2574,7 +2621,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 for (int base = warp * 32; base < d && !bucketed; base += NT) {
                     const int k = base + lane;
                     if (k < d) {
-                        int32_t lab = a.lbuf[beg + k];
+                        int32_t lab = arc_label(a, beg + k);
                         if (lab & kSingle) {
                             lab = lb_strip(a, lab);
                             if (parts <= 1 || part_of(lab, parts) == want) {
@@ -2633,7 +2680,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                     bool ok = false;
                     int32_t lab = kEmpty;
                     if (k < d) {
-                        lab = lb_strip(a, a.lbuf[beg + k]);
+                        lab = lb_strip(a, arc_label(a, beg + k));
                         if (parts <= 1 || part_of(lab, parts) == want) {
                             const int h = tab->t.find(lab);
                             ok = h >= 0 && tab->t.weight(h) == b.w &&
@@ -2697,7 +2744,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
 #pragma unroll
                 for (int c = 0; c < U; ++c) {
                     const int k = base + c * 32 + lane;
-                    labv[c] = (k < d) ? lb_strip(a, a.lbuf[beg + k]) : kEmpty;
+                    labv[c] = (k < d) ? lb_strip(a, arc_label(a, beg + k)) : kEmpty;
                 }
 #pragma unroll
                 for (int c = 0; c < U; ++c) {
@@ -2816,7 +2863,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 int32_t lab = kEmpty;
                 A w = A(0);
                 if (k < k_hi) {
-                    lab = lb_strip(a, a.lbuf[beg + k]);
+                    lab = lb_strip(a, arc_label(a, beg + k));
                     w = arc_weight<WM>(a, beg + k);
                 }
                 const uint32_t grp = __match_any_sync(0xffffffffu, lab);

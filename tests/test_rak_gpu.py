@@ -387,3 +387,37 @@ def test_graph_stays_picklable_and_device_copy_releasable(gpu):
     assert lp.release_device_graph(g) is False
     again = lp.rak_detect(g, lp.RakParams(strict=True, seed=2))  # re-uploads
     assert np.array_equal(again.assignment, first.assignment)
+
+
+def _float_weighted(g, seed=3):
+    """Same graph with float64 weights in [1, 2) that are not float32-exact
+    (both arc directions equal): the device's kFloat path."""
+    from paper_2301_09125_b200 import synth
+
+    gw = synth.with_edge_weights(g, seed=seed)
+    rows = np.repeat(np.arange(g.vertex_count), np.diff(g.offsets))
+    cols = np.asarray(g.neighbors)
+    lo, hi = np.minimum(rows, cols), np.maximum(rows, cols)
+    jitter = ((lo * 2654435761 + hi * 40503) % 1000003) / 1000003.0 * 2.0**-30
+    w = np.where(rows == cols, 1.0, gw.weights + jitter)
+    total = float(w.sum() + w[rows == cols].sum())
+    return lp.Graph(g.vertex_count, g.edge_count, g.offsets, g.neighbors, w, total)
+
+
+@pytest.mark.parametrize("batches", [0, 1])
+def test_float_weights_deterministic_and_close_to_reference(gpu, oracle, batches):
+    """Weights that are not float32-exact: tallied in float64 on the
+    device, so strict runs are deterministic; the reference sums the exact
+    float64 weights (rak.py:105) while the device rounds each weight to
+    float32 first, so parity is statistical: |dQ| <= 1e-3, communities
+    within 1% (the north star's bar for float weights)."""
+    g = _float_weighted(lp.rmat(15, seed=4))
+    assert lp._lib.device_graph(g).info()["weight_mode"] == "float"
+    p = lp.RakParams(strict=True, seed=1, tolerance=0.05, max_iterations=20, batches=batches)
+    a, b = lp.rak_detect(g, p), lp.rak_detect(g, p)
+    assert np.array_equal(a.assignment, b.assignment) and a.iterations == b.iterations
+    want, it, _ = oracle.rak(g, batches=batches, tie=0, seed=1, tolerance=0.05, max_iterations=20)
+    q_ref = oracle.modularity(g, want)
+    n_ref, n = len(np.unique(want)), len(np.unique(a.assignment))
+    assert abs(a.modularity - q_ref) <= 1e-3, (a.modularity, q_ref)
+    assert abs(n - n_ref) <= 0.01 * n_ref, (n, n_ref)
