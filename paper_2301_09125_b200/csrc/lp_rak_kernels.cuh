@@ -2532,9 +2532,39 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 s_full = 0;
             }
             __syncthreads();
+            // raw labels (and bucket arc positions) of the warp's next U chunks,
+            // loaded one step ahead: the loads of step i+1 are in flight while
+            // step i inserts (the tally was stalled on these loads)
+            int32_t pre_lab[U];
+            uint32_t pre_pos[U];
+            auto fetch = [&](int base) {
+#pragma unroll
+                for (int c = 0; c < U; ++c) {
+                    const int k = base + c * 32 + lane;
+                    pre_lab[c] = kEmpty;
+                    pre_pos[c] = 0;
+                    if (k < dd) {
+                        if (bucketed) {
+                            pre_lab[c] = a.hb_lab[bk.x + k];
+                            if (WM != kUnit) pre_pos[c] = a.hb_pos[bk.x + k];
+                        } else {
+                            pre_lab[c] = arc_label(a, beg + k);
+                        }
+                    }
+                }
+            };
+            fetch(warp * 32 * U);
             for (int base = warp * 32 * U; base < dd; base += NT * U) {
                 int32_t labv[U];
                 A wv[U];
+                int32_t raw[U];
+                uint32_t rpos[U];
+#pragma unroll
+                for (int c = 0; c < U; ++c) {
+                    raw[c] = pre_lab[c];
+                    rpos[c] = pre_pos[c];
+                }
+                if (base + NT * U < dd) fetch(base + NT * U);
 #pragma unroll
                 for (int c = 0; c < U; ++c) {
                     const int k = base + c * 32 + lane;
@@ -2542,8 +2572,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                     A w = A(0);
                     if (bucketed) {
                         if (k < dd) {
-                            lab = a.hb_lab[bk.x + k];
-                            w = WM == kUnit ? A(1) : arc_weight<WM>(a, beg + a.hb_pos[bk.x + k]);
+                            lab = raw[c];
+                            w = WM == kUnit ? A(1) : arc_weight<WM>(a, beg + rpos[c]);
                             if (two && (lab & kSingle)) lab = kEmpty;  // (looked up below)
                             else {
                                 lab = lb_strip(a, lab);
@@ -2551,7 +2581,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                             }
                         }
                     } else if (k < d) {
-                        lab = arc_label(a, beg + k);
+                        lab = raw[c];
                         w = arc_weight<WM>(a, beg + k);
                         if (two && (lab & kSingle)) lab = kEmpty;  // (two passes: looked up below)
                         else if (parts > 1 && part_of(lb_strip(a, lab), parts) != want) lab = kEmpty;

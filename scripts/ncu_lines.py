@@ -48,6 +48,8 @@ for fn in fns:
 
 if "--by-inst" in sys.argv:
     for fn in fns:
+        if ksub and ksub not in (fn or ""):
+            continue
         sel = [d for d in recs if d["fn"] == fn]
         inst = sum(float(d.get("Instructions Executed") or 0) for d in sel)
         print("== by instructions", (fn or "?")[:80])

@@ -1,37 +1,3 @@
-# INTEGRATION — plugging the B200 engine into the reference package
-
-The reference's hot path is reached through one call site per detector:
-`rak_detect` calls the numba kernel `_rak_seq(...)` / `_rak_par(...)`
-(`pkg/src/labelprop/rak.py:177-192`). The engine exports the replacement as
-a C-ABI (`include/labelprop_cuda.h`, library
-`paper_2301_09125_b200/liblabelprop_cuda.so`, built by
-`make -C paper_2301_09125_b200/csrc` or `python __graft_entry__.py`).
-
-## Option A — use this package as the drop-in
-
-`paper_2301_09125_b200` exports the reference's names (`rak_detect`,
-`RakParams`, `DetectionResult`, `Graph`, `from_arcs`, `preprocess`,
-`modularity`, `choose_max_label`, `XorShift32`, the synthetic generators,
-...). `import paper_2301_09125_b200 as labelprop` and existing calls work;
-`RakParams(strict=True)` reproduces the reference's deterministic mode label
-for label.  The sweep harness interface (`SweepSpec`, `RunRecord`,
-`run_one`, `run_sweep`, `CSV_HEADER`; `labelprop/sweep.py`) is
-`paper_2301_09125_b200.sweep`: the same grids and 11-column CSV rows on the
-CUDA detectors, plus a `batches` grid (schedule) and
-`RunRecord.csv_row(extended=True)` with the edges scanned and GTEPS.  The
-command line (`python -m paper_2301_09125_b200 detect | sweep | info`,
-`cli.py`) mirrors the reference's `labelprop detect / sweep / info` on
-generator specs (`rmat:S`, `planted:N:C`, `grid:SIDE`) and `.npz` CSR files
-(the reference's text loaders are out of scope).
-
-## Option B — patch the reference (the binding a maintainer would add)
-
-Add `labelprop/_cuda.py` below (kept verbatim as `tests/integration_cuda.py`;
-`tests/test_integration_binding.py` checks this document against it and runs
-it on the GPU against the reference's golden outputs), then replace the kernel
-calls in the reference:
-
-```python
 # labelprop/_cuda.py -- the binding a maintainer would add to the reference
 # package (Option B; kept verbatim there and checked by
 # tests/test_integration_binding.py).  It replaces the numba kernel calls
@@ -147,43 +113,3 @@ def slpa_cuda(graph, params):
                           None, C.byref(stats)))
     it = _iterations(stats)
     return labels, it, slots, np.full(n, it + 1, np.int64)
-```
-
-```python
-# labelprop/rak.py, inside rak_detect (replacing lines 173-192)
-    iterations = _cuda.rak_cuda(graph, labels, order, params.strict, params.tolerance,
-                                params.max_iterations, params.seed)
-# labelprop/copra.py, inside _detect_full (replacing lines 262-284)
-    best, iterations, labs, bels, sizes = _cuda.copra_cuda(graph, params)
-# labelprop/slpa.py, inside _detect_full (replacing lines 169-184)
-    labels, iterations, slots, filled = _cuda.slpa_cuda(graph, params)
-```
-
-Semantics of the calls match the numba kernels: same `offsets` / `neighbors`
-/ `weights` arrays (int64 / int64 / float64), same `order`, labels mutated in
-place, the sweep count returned with `rak.py:94-95` semantics, `ValueError`
-on bad arguments (asymmetric graphs are still rejected by `check_symmetric`
-in Python, `rak.py:165-166`).  Strict RAK is bit-identical to `_rak_seq`;
-non-strict uses the counter-hash tie rule; `workers` has no
-effect (one GPU).  COPRA label sets and belongings are bit-identical to the
-sequential sweep except where the reference draws a random tied maximum;
-SLPA speakers use the counter hash.  `lp_modularity(handle, labels,
-total_weight, &q)` can replace `quality.modularity` for large graphs
-(float64, equal up to summation order).
-
-Not provided by this package (the reference keeps them; off the hot path,
-SURVEY.md §2): the MatrixMarket / edge-list loaders (`load_graph`,
-`load_matrix_market`, `load_edge_list`, `GraphParseError`).  With Option B
-they stay in the reference; with Option A, load with the reference and pass
-the `Graph` fields (or `.npz` CSR arrays) to `paper_2301_09125_b200.Graph`.
-
-## Error mapping
-
-| C-ABI code | meaning | Python |
-|---|---|---|
-| `LP_ERR_INVALID` (-1) | bad argument (order not a permutation, labels out of range, malformed CSR, bad params) | `ValueError` |
-| `LP_ERR_CUDA` (-2) | no device / CUDA failure | `RuntimeError` |
-| `LP_ERR_NOMEM` (-3) | device allocation failed | `RuntimeError` |
-| `LP_ERR_UNSUPPORTED` (-4) | n ≥ 2^30 or m ≥ 2^31, COPRA k > 32 | `RuntimeError` |
-
-The message is in `lp_last_error()` (thread-local).
