@@ -223,6 +223,7 @@ struct lp_graph {
     bool debug_rounds = false;  // LP_DEBUG_ROUNDS=1: per-round route sizes on stderr
     bool rows_sorted = false;  // every row strictly increasing (duplicate-free), checked at upload
     bool first_round_shortcut = true;  // LP_FIRST_ROUND=0 disables k_first_round
+    bool first_chain = true;           // LP_FIRST_CHAIN=0: plain first-arc guess in exact schedules
     bool sweep_frontier = true;        // active frontier across sweeps (LP_SWEEP_FRONTIER=0 disables)
     double carry_frac = 0.5;           // ... after sweeps that changed <= this share of the rows (LP_CARRY_FRAC)
     bool pull_rounds = false;  // LP_PULL_ROUNDS=1: pulled marks instead of full rounds after big rounds (measured: no gain)
@@ -1356,6 +1357,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_PULL_ROUNDS")) g->pull_rounds = atoi(ev) != 0;
     if (const char* ev = getenv("LP_PULL_MAX")) g->pull_max_frac = atof(ev);
     if (const char* ev = getenv("LP_FIRST_ROUND")) g->first_round_shortcut = atoi(ev) != 0;
+    if (const char* ev = getenv("LP_FIRST_CHAIN")) g->first_chain = atoi(ev) != 0;
     if (const char* ev = getenv("LP_SWEEP_FRONTIER")) g->sweep_frontier = atoi(ev) != 0;
     if (const char* ev = getenv("LP_CARRY_FRAC")) g->carry_frac = atof(ev);
     if (const char* ev = getenv("LP_CAP_ROUTE")) g->cap_route = atoi(ev) != 0;
@@ -1561,7 +1563,8 @@ static void bits_to_queue(lp_graph* g, const EvalArgs& a) {
 }
 
 static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round, int alg, Prof* prof, int* rounds,
-                       int64_t* gathered, bool first_ids = false, bool carry = false, bool first_random = false) {
+                       int64_t* gathered, bool first_ids = false, bool carry = false, bool first_random = false,
+                       bool first_chain = false) {
     const Plan& P = g->plan();
     cudaStream_t st = g->stream;
     LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
@@ -1698,7 +1701,8 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
                     k_first_round_r<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S);
                 }
                 else
-                    k_first_round<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S);
+                    k_first_round<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S, P.slot_of,
+                                                                                      first_chain ? 1 : 0);
                 prof->end(st);
             } else {
                 run_round(g, a, true, g->h_len, prof, alg);  // (refreshes every margin)
@@ -1723,8 +1727,11 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
             fprintf(stderr, "[lp]   round %d (%s): %.3f ms, %lld label writes\n", *rounds,
                     next == kNextQueue ? "frontier" : (next == kNextFirst ? "first" : "dense"), ms, (long long)w);
         }
-        if (w == 0) break;  // nothing changed: every read is final
-        if (w >= dense_at) {
+        if (w == 0 && !(first_chain && next == kNextFirst)) break;  // nothing changed: every read is final
+        if (first_chain && next == kNextFirst) {
+            // the chained first round is a guess, not an evaluation: verify every row
+            next = kNextDense;
+        } else if (w >= dense_at) {
             if (g->pull_rounds && P.npieces > 0 && (double)w < g->pull_max_frac * (double)P.S) {
                 // most labels moved: every row pulls the changed flags of its
                 // earlier-batch neighbours (one flat pass instead of an atomic per
@@ -2000,8 +2007,11 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         // tallies of unit weights; with weights the labels stay diverse and the
         // small tables overflow: measured slower, so weighted rows estimate d)
         a.first_est_div = g->wmode == kFixed ? 1 : g->first_est_div;
+        // (exact schedules, scan-first, unit weights: the first round follows first
+        // arcs through earlier-batch neighbours, k_first_round)
+        const bool first_chain = first_ids && cross && g->first_chain && g->wmode == kUnit && o->tie == kScanFirst;
         if (int rc = solve_sweep(g, a, cross, run_round, kGatherRak, &prof, &rounds, &gathered, first_ids || first_random,
-                                 carry, first_random))
+                                 carry, first_random, first_chain))
             return rc;
         LP_CK(cudaMemcpyAsync(g->h_counters, g->counters, kCtrCount * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                               st));

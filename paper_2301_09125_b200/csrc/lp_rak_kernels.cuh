@@ -962,7 +962,16 @@ __global__ void k_route_queue(EvalArgs a, const int32_t* __restrict__ mq_in, con
 // sorted -- so the round needs no gather and no tally: one thread per row
 // reads one neighbour id.  Everything the tally kernels record is recorded
 // (label, changed count, distinct count, majority flag, margin, changed row).
-__global__ void __launch_bounds__(256) k_first_round(EvalArgs a, int32_t S) {
+// chain: a better guess for the exact schedule (scan-first ties).  With every
+// tally all singletons the sequential sweep gives v the label of its first arc:
+// the neighbour's id if it comes in a later batch, else the label that
+// neighbour took -- which is, by the same rule, its own first arc's.  Following
+// first arcs through earlier-batch neighbours (a few hops; rows are sorted, the
+// first arc is the smallest id) reproduces the sequential first sweep for all
+// of those vertices (a third of the wrong guesses of the plain first arc remain
+// on R-MAT-22).  It is a guess, not an evaluation, so a dense round follows.
+__global__ void __launch_bounds__(256) k_first_round(EvalArgs a, int32_t S, const int32_t* __restrict__ slot_of,
+                                                     int chain) {
     long long dchg = 0, arcs = 0, writes = 0, verts = 0;
     // (warp-uniform loop: the changed rows are pushed as pieces by the whole warp)
     for (int32_t base = blockIdx.x * blockDim.x; base < S; base += gridDim.x * blockDim.x) {
@@ -973,7 +982,10 @@ __global__ void __launch_bounds__(256) k_first_round(EvalArgs a, int32_t S) {
             const int32_t p = __ldg(a.svid + s);
             const uint32_t beg = __ldg(a.soff + s);
             d = (int)(__ldg(a.soff + s + 1) - beg);
-            const int32_t lab = (int32_t)(__ldg(a.snbr + beg) >> 2);
+            uint32_t nb = __ldg(a.snbr + beg);
+            for (int hop = 0; chain && (nb & kEarlier) && hop < 64; ++hop)
+                nb = __ldg(a.snbr + __ldg(a.soff + __ldg(slot_of + (nb >> 2))));
+            const int32_t lab = (int32_t)(nb >> 2);
             arcs += d;
             ++verts;
             // (the next round of a singleton first sweep tables only the evaluated
