@@ -807,7 +807,7 @@ template <int WM, int TIE> struct Launcher {
                 k_gather_pieces<kGatherSlpa><<<grid_for(P.npieces, 32 * 8, sms * 16), 256, 0, st>>>(
                     a, P.dslot, P.dk0, P.dcount, a.r.len + kGatherCursor);
             else
-                k_gather_pieces<kGatherSlpa><<<grid_for(h_len[kLenGather], 32 * 8, sms * 16), 256, 0, st>>>(
+                k_gather_pieces<kGatherSlpa><<<grid_for(h_len[kLenGather], 4 * 8, sms * 16), 256, 0, st>>>(
                     a, a.r.gslot, a.r.gk0, a.r.len + kLenGather, a.r.len + kGatherCursor);
             prof->end(st);
         } else if (fuse_all) {
@@ -819,7 +819,7 @@ template <int WM, int TIE> struct Launcher {
             }
         } else if (h_len[kLenGather] > 0) {
             prof->begin(st, kKGather);
-            k_gather_pieces<kGatherRak><<<grid_for(h_len[kLenGather], 32 * 8, sms * 16), 256, 0, st>>>(
+            k_gather_pieces<kGatherRak><<<grid_for(h_len[kLenGather], 4 * 8, sms * 16), 256, 0, st>>>(
                 a, a.r.gslot, a.r.gk0, a.r.len + kLenGather, a.r.len + kGatherCursor);
             prof->end(st);
         }
@@ -1584,7 +1584,7 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         const int64_t pieces = changed_rows + changed_rows / 8 + 32;
         const EvalArgs b = marks_mode(g, a, changed_rows);
         prof->begin(st, -1);
-        k_mark_pieces<<<grid_for(pieces, 32 * 8, g->num_sms * 16), 256, 0, st>>>(b);
+        k_mark_pieces<<<grid_for(pieces, 4 * 8, g->num_sms * 16), 256, 0, st>>>(b);
         if (compact) bits_to_queue(g, b);
         prof->end(st);
     };
@@ -1608,16 +1608,15 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         if (ql == 0) return LP_OK;  // no vertex saw a neighbour change: the sweep changes nothing
         next = kNextQueue;  // (the margin test filters the queue; see the switch below)
     }
-    const int W = (cross && !carry && !first_ids) ? g->waves : 1;
-    if (W > 1) {
-        // Dense waves: the visit order in W consecutive position ranges, each
-        // routed and evaluated after the previous one, so a wave reads the
-        // current-sweep labels of all earlier waves; a changed label marks only
-        // the later neighbours in positions already evaluated (its own wave).
+    // Dense waves: the visit order in W consecutive position ranges, each
+    // routed and evaluated after the previous one, so a wave reads the
+    // current-sweep labels of all earlier waves; a changed label marks only
+    // the later neighbours in positions already evaluated (its own wave).
+    auto dense_waves = [&](int W) -> int {
         if (int rc = ensure_waves(g, W)) return rc;
         const int64_t ws = (g->n + W - 1) / W;
         for (int w = 0; w < W; ++w) {
-            if (w > 0) LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
+            LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
             prof->begin(st, -1);
             k_route_queue<<<g->num_sms * 4, 256, 0, st>>>(a, P.vorder + w * ws, P.wave_len + w, P.slot_of, 0);
             prof->end(st);
@@ -1626,14 +1625,18 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
             a.horizon = (int32_t)std::min<int64_t>(g->n, (w + 1) * ws);
             if (g->h_len[kLenRouted] > 0) {
                 run_round(g, a, false, g->h_len, prof, alg);
-                if (a.mark) mark_pass(INT64_MAX / 4, false);
+                if (a.mark) mark_pass(g->n, false);
             }
             ++*rounds;
         }
         a.horizon = INT32_MAX;
-        if (a.mark) bits_to_queue(g, marks_mode(g, a, INT64_MAX / 4));  // (the waves' mode)
+        if (a.mark) bits_to_queue(g, marks_mode(g, a, g->n));  // (the waves' mode)
         next = kNextQueue;
-    }
+        return LP_OK;
+    };
+    const int W = (cross && !carry && !first_ids) ? g->waves : 1;
+    if (W > 1)
+        if (int rc = dense_waves(W)) return rc;
     cudaEvent_t dbg0 = nullptr, dbg1 = nullptr;
     if (g->debug_rounds) {
         cudaEventCreate(&dbg0);
@@ -1730,6 +1733,7 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         if (w == 0 && !(first_chain && next == kNextFirst)) break;  // nothing changed: every read is final
         if (first_chain && next == kNextFirst) {
             // the chained first round is a guess, not an evaluation: verify every row
+            // (in position-ordered waves instead: measured 1.3-7x slower)
             next = kNextDense;
         } else if (w >= dense_at) {
             if (g->pull_rounds && P.npieces > 0 && (double)w < g->pull_max_frac * (double)P.S) {
@@ -2009,6 +2013,8 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         a.first_est_div = g->wmode == kFixed ? 1 : g->first_est_div;
         // (exact schedules, scan-first, unit weights: the first round follows first
         // arcs through earlier-batch neighbours, k_first_round)
+        // (measured with fixed-point weights too: the weighted first sweep's
+        // cascade of frontier rounds is not shortened, no gain)
         const bool first_chain = first_ids && cross && g->first_chain && g->wmode == kUnit && o->tie == kScanFirst;
         if (int rc = solve_sweep(g, a, cross, run_round, kGatherRak, &prof, &rounds, &gathered, first_ids || first_random,
                                  carry, first_random, first_chain))

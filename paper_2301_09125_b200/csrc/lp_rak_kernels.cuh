@@ -397,6 +397,14 @@ __global__ void __launch_bounds__(256) k_gather_dense(EvalArgs a, int64_t m) {
 // finds its piece by a 5-step search over the warp's prefix (shuffles only).
 constexpr int kPieceArcs = 256;
 
+// Pieces a warp takes at a time: 32 (one per lane) when there are plenty, fewer
+// when a short list -- often a few hub rows of a late frontier round -- would
+// otherwise leave most of the grid idle behind a handful of warps.
+__device__ __forceinline__ int pieces_per_warp(int cnt) {
+    const int warps = (int)(gridDim.x * blockDim.x / 32);
+    return max(1, min(32, cnt / max(warps, 1)));
+}
+
 template <int ALG>
 __global__ void __launch_bounds__(256) k_gather_pieces(EvalArgs a, const int32_t* __restrict__ gslot,
                                                        const int32_t* __restrict__ gk0,
@@ -404,14 +412,15 @@ __global__ void __launch_bounds__(256) k_gather_pieces(EvalArgs a, const int32_t
     constexpr int J = 8;
     const int lane = threadIdx.x & 31;
     const int cnt = *count;
+    const int per = pieces_per_warp(cnt);
     while (true) {
         int b0 = 0;
-        if (lane == 0) b0 = atomicAdd(cursor, 32);
+        if (lane == 0) b0 = atomicAdd(cursor, per);
         b0 = __shfl_sync(0xffffffffu, b0, 0);
         if (b0 >= cnt) break;
         uint32_t pbeg = 0, plen = 0, pk0 = 0;
         int32_t pv = 0;
-        if (b0 + lane < cnt) {
+        if (lane < per && b0 + lane < cnt) {
             const int32_t s = gslot[b0 + lane];
             pk0 = (uint32_t)gk0[b0 + lane];
             const uint32_t rb = __ldg(a.soff + s), re = __ldg(a.soff + s + 1);
@@ -687,13 +696,14 @@ __global__ void __launch_bounds__(256) k_mark_pieces(EvalArgs a) {
     constexpr int J = 8;
     const int lane = threadIdx.x & 31;
     const int cnt = a.r.len[kLenChg];
+    const int per = pieces_per_warp(cnt);
     while (true) {
         int b0 = 0;
-        if (lane == 0) b0 = atomicAdd(a.r.len + kChgCursor, 32);
+        if (lane == 0) b0 = atomicAdd(a.r.len + kChgCursor, per);
         b0 = __shfl_sync(0xffffffffu, b0, 0);
         if (b0 >= cnt) break;
         uint32_t pbeg = 0, plen = 0;
-        if (b0 + lane < cnt) {
+        if (lane < per && b0 + lane < cnt) {
             const int32_t s = a.r.cslot[b0 + lane];
             const uint32_t rb = __ldg(a.soff + s), re = __ldg(a.soff + s + 1);
             pbeg = rb + (uint32_t)a.r.ck0[b0 + lane];
