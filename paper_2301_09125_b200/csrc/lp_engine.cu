@@ -730,7 +730,10 @@ template <int WM, int TIE> struct Launcher {
         const int sms = g->num_sms;
         a.bin = kKWarp;
         prof->begin(s, kKWarp);
-        const int per_block = 32 * WarpClass<WC>::kWarps;
+        // (frontier rounds: a warp per listed row up to the resident grid -- a late
+        // round's few long rows each get their own warp instead of queueing
+        // 32 deep behind one block's eight warps)
+        const int per_block = WarpClass<WC>::kWarps;
         const int grid = dense ? sms * occ_warp[WC] : grid_for(cnt, per_block, sms * occ_warp[WC]);
         if constexpr (WM == kUnit || WM == kFixed) {
             if (a.id_single) {

@@ -27,6 +27,17 @@ from paper_2301_09125_b200.copra import copra_run  # noqa: E402
 from paper_2301_09125_b200.slpa import slpa_run  # noqa: E402
 
 
+def _peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+PEAK = _peak()
+
+
 def timed(fn, steps, warmup):
     for _ in range(warmup):
         fn()
@@ -60,13 +71,22 @@ def main():
                     return it, st["kernel_ms"]
 
                 ms, it = timed(run, args.steps, args.warmup)
+                # roofline: per dense sweep 4 B index + (4 B label + 8 B belonging) per entry of
+                # the neighbour's label set per arc, the row's set written (12 B per entry + size)
+                _, _, _, _, sizes, _, _ = copra_run(g, p, want_sets=True, device_graph=dg)
+                sbar = float(np.mean(sizes))
+                sweep_bytes = g.edge_count * (4 + 12 * sbar) + g.vertex_count * (12 * sbar + 8)
+                gbs = sweep_bytes * it / (ms * 1e-3) / 1e9
                 line = {"algo": "copra", "metric": "COPRA GTEPS on R-MAT-20 (edge_count x sweeps / time)",
                         "value": g.edge_count * it / (ms * 1e-3) / 1e9, "unit": "GTEPS", "ms_per_run": ms,
                         "iterations": it, "config": {"workload": "rmat20", "max_labels": K, "batches": batches,
                                                      "tolerance": 0.01, "vertices": g.vertex_count,
                                                      "arcs": g.edge_count},
                         "modularity": O.modularity(g, run.best),
-                        "communities": int(len(np.unique(run.best)))}
+                        "communities": int(len(np.unique(run.best))),
+                        "roofline": {"bound": "hbm", "achieved": gbs, "peak": PEAK, "unit": "GB/s", "frac": gbs / PEAK,
+                                     "bytes_model": "per sweep m (4 + 12 s) + n (12 s + 8), s = mean label-set size "
+                                                    f"{sbar:.3f}"}}
                 if not args.no_cpu and batches == 0 and K in (1, 8):
                     t0 = time.perf_counter()
                     best, cit, _, _, _ = O.copra(g, max_labels=K, batches=0, tie=1, seed=1, tolerance=0.01,
@@ -89,13 +109,17 @@ def main():
                     return it, st["kernel_ms"]
 
                 ms, it = timed(run, args.steps, args.warmup)
+                # roofline: per speaking round 4 B index + 4 B spoken label per arc, 8 B per vertex
+                gbs = (8 * g.edge_count + 8 * g.vertex_count) * it / (ms * 1e-3) / 1e9
                 line = {"algo": "slpa", "metric": "SLPA GTEPS on planted-1M (edge_count x rounds / time)",
                         "value": g.edge_count * it / (ms * 1e-3) / 1e9, "unit": "GTEPS", "ms_per_run": ms,
                         "iterations": it, "config": {"workload": "planted1m", "memory_size": T, "batches": batches,
                                                      "tolerance": 0.05, "vertices": g.vertex_count,
                                                      "arcs": g.edge_count},
                         "modularity": O.modularity(g, run.labels),
-                        "communities": int(len(np.unique(run.labels)))}
+                        "communities": int(len(np.unique(run.labels))),
+                        "roofline": {"bound": "hbm", "achieved": gbs, "peak": PEAK, "unit": "GB/s", "frac": gbs / PEAK,
+                                     "bytes_model": "per round 8 m + 8 n (index + spoken label per arc)"}}
                 if not args.no_cpu and batches == 0 and T == 20:
                     t0 = time.perf_counter()
                     labels, cit, _, _ = O.slpa(g, memory_size=T, batches=0, tie=1, speaker_rng=1, seed=1,

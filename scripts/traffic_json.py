@@ -14,7 +14,7 @@ def group(name):
         return "tally_warp"
     if name.startswith("k_team"):
         return "tally_hub" if "1024" in name else "tally_team"
-    if name.startswith("k_small") or name.startswith("k_first_round"):
+    if name.startswith("k_small") or name.startswith("k_first_round") or name.startswith("k_mid"):
         return "tally_small"
     if name.startswith("k_gather"):
         return "k_gather"

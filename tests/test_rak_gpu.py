@@ -284,6 +284,11 @@ def test_malformed_csr_rejected_on_upload(gpu):
     {"LP_TWO_TEAM_W": "0"},                       # weighted team rows insert every label
     {"LP_MID_HASH": "0"},                         # mid-degree rows by O(d^2) compares
     {"LP_HUB_BUCKET": "1", "LP_FIRST_EST_MIN": "16", "LP_FIRST_EST_DIV": "64"},  # hub buckets, low estimates
+    {"LP_FIRST_CHAIN": "0"},                      # plain first-arc first round in exact schedules
+    {"LP_FUSE_MAXD": "0"},                        # every row through the phase-1 buffer
+    {"LP_FUSE_MAXD": "-1"},                       # every row gathers its own labels (fused)
+    {"LP_FUSE_MAXD": "64", "LP_L2_PERSIST": "0"},  # small and mid rows fused; no L2 window
+    {"LP_SWEEP_FRONTIER": "0"},                   # no frontier across sweeps (random ties too)
 ])
 def test_engine_policies_keep_exactness(gpu, oracle, env, monkeypatch):
     """Every scheduling policy of the engine (chosen per handle from the
