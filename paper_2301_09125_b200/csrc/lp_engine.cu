@@ -288,6 +288,32 @@ __global__ void k_offsets_check(const int64_t* __restrict__ off, int64_t n, unsi
 }
 
 // neighbours -> int32 with range check; bad[0] counts out-of-range ids
+// neighbours [lo, hi) -> int32 with the range check (bad[0]) and the
+// strictly-increasing-rows check (sorted_bad[0]: arcs that are not a row start
+// and not above their predecessor; the arc before lo is already converted)
+__global__ void k_nbr_convert_check(const int64_t* __restrict__ in, int32_t* __restrict__ out,
+                                    const uint8_t* __restrict__ start, int64_t lo, int64_t hi, int64_t n,
+                                    unsigned long long* bad, unsigned long long* sorted_bad) {
+    unsigned long long nbad = 0, nuns = 0;
+    for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = in[i];
+        nbad += (v < 0 || v >= n);
+        out[i] = (int32_t)v;
+        if (i > 0 && !start[i]) {
+            const int64_t prev = i > lo ? in[i - 1] : (int64_t)out[i - 1];
+            nuns += v <= prev;
+        }
+    }
+    for (int o = 16; o >= 1; o >>= 1) {
+        nbad += __shfl_xor_sync(0xffffffffu, nbad, o);
+        nuns += __shfl_xor_sync(0xffffffffu, nuns, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (nbad) atomicAdd(bad, nbad);
+        if (nuns) atomicAdd(sorted_bad, nuns);
+    }
+}
+
 __global__ void k_nbr_convert(const int64_t* __restrict__ in, int32_t* __restrict__ out, int64_t count, int64_t n,
                               unsigned long long* bad) {
     unsigned long long nbad = 0;
@@ -1435,34 +1461,79 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     G_CK(cudaMemsetAsync(g->gap, 0, (n + 4) * sizeof(unsigned long long), st));
     G_CK(cudaMemsetAsync(g->counters, 0, 32 * sizeof(unsigned long long), st));
     {
+        // Upload pipeline: the host arrays go over PCIe on a copy stream (aux[1])
+        // in chunks; the handle's stream converts and checks each chunk as it
+        // lands (int64 -> int32, range, rows strictly increasing), so only the
+        // last chunk's work trails the transfer.  Offsets first: the row-start
+        // flags, degree statistics and route buffers are ready before the
+        // neighbours finish arriving.
         int64_t* tmp = nullptr;
         int64_t tb = 0;
         G_CK(dalloc(&tmp, std::max(n + 1, m), &tb));
-        G_CK(cudaMemcpyAsync(tmp, offsets, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        cudaStream_t cs = g->aux[1];
+        cudaEvent_t ev_copy = nullptr;
+        G_CK(cudaEventCreateWithFlags(&ev_copy, cudaEventDisableTiming));
+        struct EvGuard {
+            cudaEvent_t e;
+            ~EvGuard() { cudaEventDestroy(e); }
+        } ev_guard{ev_copy};
+        G_CK(cudaEventRecord(ev_copy, st));  // (the memsets above precede the copies)
+        G_CK(cudaStreamWaitEvent(cs, ev_copy, 0));
+        G_CK(cudaMemcpyAsync(tmp, offsets, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, cs));
+        G_CK(cudaEventRecord(ev_copy, cs));
+        G_CK(cudaStreamWaitEvent(st, ev_copy, 0));
         k_i64_to_u32<<<g->num_sms * 8, 256, 0, st>>>(tmp, g->off, n + 1);
         k_offsets_check<<<g->num_sms * 8, 256, 0, st>>>(tmp, n, g->counters + 11);
-        if (m > 0) {
-            G_CK(cudaMemcpyAsync(tmp, neighbors, m * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-            k_nbr_convert<<<g->num_sms * 8, 256, 0, st>>>(tmp, g->nbr, m, n, g->counters);
-        }
-        if (weights && m > 0) {
-            G_CK(cudaMemcpyAsync(tmp, weights, m * sizeof(double), cudaMemcpyHostToDevice, st));
-            unsigned long long init[4] = {0, 0, ~0ull, 0};
-            G_CK(cudaMemcpyAsync(g->counters + 4, init, sizeof(init), cudaMemcpyHostToDevice, st));
-            k_weight_scan<<<g->num_sms * 8, 256, 0, st>>>((const double*)tmp, m, g->counters + 4);
-        }
         k_degree_stats<<<g->num_sms * 8, 256, 0, st>>>(g->off, n, g->counters + 8);
+        uint8_t* rs = nullptr;
+        int64_t rb = 0;
         if (m > 0) {
-            uint8_t* rs = nullptr;
-            int64_t rb = 0;
             G_CK(dalloc(&rs, m, &rb));
             G_CK(cudaMemsetAsync(rs, 0, m, st));
             k_row_starts<<<g->num_sms * 8, 256, 0, st>>>(g->off, n, m, rs);
-            k_rows_sorted_flat<<<g->num_sms * 8, 256, 0, st>>>(g->nbr, rs, m, g->counters + 12);
-            dfree(rs);
+        }
+        // (the neighbours may overwrite tmp once the offsets are converted)
+        G_CK(cudaEventRecord(ev_copy, st));
+        G_CK(cudaStreamWaitEvent(cs, ev_copy, 0));
+        constexpr int64_t kChunk = (int64_t)1 << 25;  // 32M arcs = 256 MB per transfer
+        std::vector<cudaEvent_t> evs;
+        struct EvsGuard {
+            std::vector<cudaEvent_t>& v;
+            ~EvsGuard() {
+                for (cudaEvent_t e : v) cudaEventDestroy(e);
+            }
+        } evs_guard{evs};
+        for (int64_t lo = 0; lo < m; lo += kChunk) {
+            const int64_t len = std::min(kChunk, m - lo);
+            cudaEvent_t e = nullptr;
+            G_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            evs.push_back(e);
+            G_CK(cudaMemcpyAsync(tmp + lo, neighbors + lo, len * sizeof(int64_t), cudaMemcpyHostToDevice, cs));
+            G_CK(cudaEventRecord(e, cs));
+            G_CK(cudaStreamWaitEvent(st, e, 0));
+            k_nbr_convert_check<<<g->num_sms * 8, 256, 0, st>>>(tmp, g->nbr, rs, lo, lo + len, n, g->counters,
+                                                                 g->counters + 12);
+        }
+        if (weights && m > 0) {
+            // (after the neighbours' conversions: the weights reuse tmp)
+            G_CK(cudaEventRecord(ev_copy, st));
+            G_CK(cudaStreamWaitEvent(cs, ev_copy, 0));
+            unsigned long long init[4] = {0, 0, ~0ull, 0};
+            G_CK(cudaMemcpyAsync(g->counters + 4, init, sizeof(init), cudaMemcpyHostToDevice, st));
+            for (int64_t lo = 0; lo < m; lo += kChunk) {
+                const int64_t len = std::min(kChunk, m - lo);
+                cudaEvent_t e = nullptr;
+                G_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                evs.push_back(e);
+                G_CK(cudaMemcpyAsync(tmp + lo, weights + lo, len * sizeof(double), cudaMemcpyHostToDevice, cs));
+                G_CK(cudaEventRecord(e, cs));
+                G_CK(cudaStreamWaitEvent(st, e, 0));
+                k_weight_scan<<<g->num_sms * 8, 256, 0, st>>>((const double*)tmp + lo, len, g->counters + 4);
+            }
         }
         G_CK(cudaMemcpyAsync(g->h_counters, g->counters, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         G_CK(cudaStreamSynchronize(st));
+        dfree(rs);
         if (g->h_counters[11]) {
             dfree(tmp);
             return fail(lp_fail(LP_ERR_INVALID, "offsets must be non-decreasing"));
