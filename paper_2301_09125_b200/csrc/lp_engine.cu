@@ -37,6 +37,7 @@
 #include "lp_common.cuh"
 #include "lp_host.h"
 #include "lp_rak_kernels.cuh"
+#include "lp_loop_kernels.cuh"
 #include "lp_slpa_kernels.cuh"
 #include "lp_copra_kernels.cuh"
 
@@ -219,6 +220,16 @@ struct lp_graph {
     size_t cub_tmp_bytes = 0;
     int num_sms = 148;
     int waves = 1;  // dense waves of the cross-batch schedules (LP_WAVES overrides)
+    // frontier loop (lp_loop_kernels.cuh): rounds that evaluate at most loop_rows rows continue on the
+    // device in one cooperative launch (LP_LOOP_ROWS, 0 = off); graphs whose rows all fit the loop's
+    // warp table and hold at most loop_dense_arcs arcs run their dense rounds there too (LP_LOOP_DENSE_ARCS)
+    int64_t loop_rows = 8192;
+    int64_t loop_dense_arcs = 16 << 20;
+    int loop_max_queue = 1 << 16;
+    int loop_blocks_per_sm = 0;  // 0 = the kernel's occupancy (LP_LOOP_BLOCKS)
+    LoopCtl* loop_ctl = nullptr;  // device
+    LoopCtl* h_loop = nullptr;    // pinned
+    cudaError_t (*loop_run)(lp_graph*, const EvalArgs&, const int32_t*, const int32_t*, int, int, int, int) = nullptr;
     bool margin_skip = true;  // frontier margin test (LP_MARGIN=0 disables)
     bool debug_rounds = false;  // LP_DEBUG_ROUNDS=1: per-round route sizes on stderr
     bool rows_sorted = false;  // every row strictly increasing (duplicate-free), checked at upload
@@ -694,7 +705,7 @@ struct Prof {
 
 template <int WM, int TIE> struct Launcher {
     using A = typename Acc<WM>::T;
-    static int occ_warp[2], occ_team, occ_team2, occ_hub, occ_mid, occ_midh, done_device;
+    static int occ_warp[2], occ_team, occ_team2, occ_hub, occ_mid, occ_midh, occ_loop, done_device;
     template <int WC> static cudaError_t setup_warp() {
         cudaError_t e;
         if constexpr (WM == kUnit || WM == kFixed) {
@@ -748,6 +759,13 @@ template <int WM, int TIE> struct Launcher {
         if (e) return e;
         occ_team = std::max(occ_team, 1);
         occ_hub = std::max(occ_hub, 1);
+        e = cudaFuncSetAttribute(k_frontier_loop<WM, TIE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)loop_smem_bytes<WM>());
+        if (e) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_loop, k_frontier_loop<WM, TIE>, kLoopWarps * 32,
+                                                          loop_smem_bytes<WM>());
+        if (e) return e;
+        occ_loop = std::max(occ_loop, 1);
         done_device = device;
         return cudaSuccess;
     }
@@ -770,6 +788,25 @@ template <int WM, int TIE> struct Launcher {
         }
         k_warp<WM, TIE, WC, false><<<grid, WarpClass<WC>::kWarps * 32, warp_smem_bytes<WM, WC>(), s>>>(a);
         prof->end(s);
+    }
+    // The frontier loop (lp_loop_kernels.cuh): rounds on the device until a round queues
+    // nothing or the queue goes back to the class kernels; the caller reads g->loop_ctl.
+    static cudaError_t loop(lp_graph* g, const EvalArgs& a, const int32_t* list0, const int32_t* list0_len,
+                            int list0_cnt, int first_dst, int dense, int max_queue) {
+        const Plan& P = g->plan();
+        EvalArgs b = a;
+        b.bin = kKWarp;
+        int32_t* q0 = g->mq[0];
+        int32_t* q1 = g->mq[1];
+        const int32_t* slot_of = P.slot_of;
+        LoopCtl* ctl = g->loop_ctl;
+        int32_t* mq_len = g->mq_len;
+        int max_rounds = 1 << 20;
+        void* args[] = {&b, &list0, &list0_len, &list0_cnt, &q0, &q1, &first_dst, &slot_of, &ctl, &mq_len, &dense, &max_queue,
+                        &max_rounds};
+        const int per_sm = g->loop_blocks_per_sm > 0 ? std::min(g->loop_blocks_per_sm, occ_loop) : occ_loop;
+        return cudaLaunchCooperativeKernel((const void*)k_frontier_loop<WM, TIE>, dim3(g->num_sms * per_sm),
+                                           dim3(kLoopWarps * 32), args, loop_smem_bytes<WM>(), g->stream);
     }
     // One round.  dense: k_small sweeps the small slot range and the other
     // slots are routed; frontier: everything comes from the marked route.
@@ -925,6 +962,7 @@ template <int WM, int TIE> int Launcher<WM, TIE>::occ_team2 = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_hub = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_mid = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::occ_midh = 1;
+template <int WM, int TIE> int Launcher<WM, TIE>::occ_loop = 1;
 template <int WM, int TIE> int Launcher<WM, TIE>::done_device = -1;
 
 typedef void (*round_fn)(lp_graph*, EvalArgs, bool, const int32_t*, Prof*, int);
@@ -943,6 +981,15 @@ template <int WM> static void pick_fns(int tie, round_fn* r, setup_fn* s) {
         default:
             *r = Launcher<WM, kScanFirst>::round;
             *s = Launcher<WM, kScanFirst>::setup;
+    }
+}
+
+typedef cudaError_t (*loop_fn)(lp_graph*, const EvalArgs&, const int32_t*, const int32_t*, int, int, int, int);
+template <int WM> static loop_fn pick_loop(int tie) {
+    switch (tie) {
+        case kRandom: return Launcher<WM, kRandom>::loop;
+        case kMinLabel: return Launcher<WM, kMinLabel>::loop;
+        default: return Launcher<WM, kScanFirst>::loop;
     }
 }
 
@@ -1036,6 +1083,8 @@ static void destroy_graph(lp_graph* g) {
     dfree(g->out64);
     dfree(g->cub_tmp);
     if (g->h_len) cudaFreeHost(g->h_len);
+    if (g->h_loop) cudaFreeHost(g->h_loop);
+    if (g->loop_ctl) cudaFree(g->loop_ctl);
     if (g->h_counters) cudaFreeHost(g->h_counters);
     for (cudaEvent_t e : g->event_pool) cudaEventDestroy(e);
     if (g->ev0) cudaEventDestroy(g->ev0);
@@ -1380,6 +1429,10 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (const char* ev = getenv("LP_L2_PERSIST")) g->l2_persist = atoi(ev) != 0;
     if (const char* ev = getenv("LP_FUSE_MAXD")) g->fuse_maxd = atoi(ev) < 0 ? (1 << 30) : atoi(ev);
     if (const char* ev = getenv("LP_WAVES")) g->waves = std::max(1, std::min(1024, atoi(ev)));
+    if (const char* ev = getenv("LP_LOOP_ROWS")) g->loop_rows = std::max(0, atoi(ev));
+    if (const char* ev = getenv("LP_LOOP_DENSE_ARCS")) g->loop_dense_arcs = std::max(0, atoi(ev));
+    if (const char* ev = getenv("LP_LOOP_MAX_QUEUE")) g->loop_max_queue = std::max(1, atoi(ev));
+    if (const char* ev = getenv("LP_LOOP_BLOCKS")) g->loop_blocks_per_sm = std::max(0, atoi(ev));
     if (const char* ev = getenv("LP_MARGIN")) g->margin_skip = atoi(ev) != 0;
     if (const char* ev = getenv("LP_DEBUG_ROUNDS")) g->debug_rounds = atoi(ev) != 0;
     if (const char* ev = getenv("LP_DENSE_FRAC")) g->dense_frac = atof(ev);
@@ -1456,6 +1509,8 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     G_CK(dalloc(&g->counters, 32, &g->bytes));
     G_CK(dalloc(&g->out64, n, &g->bytes));
     G_CK(cudaMallocHost((void**)&g->h_len, kLenCount * sizeof(int32_t)));
+    G_CK(cudaMallocHost((void**)&g->h_loop, sizeof(LoopCtl)));
+    G_CK(cudaMalloc((void**)&g->loop_ctl, sizeof(LoopCtl)));
     G_CK(cudaMallocHost((void**)&g->h_counters, 32 * sizeof(unsigned long long)));
     G_CK(cudaMemsetAsync(g->mark, 0, (n + 4) * sizeof(unsigned long long), st));
     G_CK(cudaMemsetAsync(g->gap, 0, (n + 4) * sizeof(unsigned long long), st));
@@ -1673,6 +1728,31 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
     const int64_t dense_at = (int64_t)(g->dense_frac * (double)P.S);
     enum { kNextDense, kNextFirst, kNextQueue };
     int next = first_ids ? kNextFirst : kNextDense;
+    // The frontier loop: the rounds from here on run in one cooperative launch (lp_loop_kernels.cuh)
+    // until a round queues nothing (*done) or the queue comes back (rows longer than the loop's
+    // table, or more than loop_max_queue of them): then the class kernels route mq[q] as usual.
+    const bool loop_ok = g->loop_run && alg == kGatherRak && cross && a.mark && g->loop_rows > 0;
+    const bool loop_dense = loop_ok && g->max_degree <= kLoopMaxDeg && P.m_active <= g->loop_dense_arcs;
+    auto run_loop = [&](const int32_t* list0, const int32_t* list0_len, int list0_cnt, int first_dst, bool dense,
+                        bool* done) -> int {
+        LP_CK(cudaMemsetAsync(g->loop_ctl, 0, sizeof(LoopCtl), st));
+        prof->begin(st, kKWarp);
+        const cudaError_t e = g->loop_run(g, a, list0, list0_len, list0_cnt, first_dst, dense ? 1 : 0, g->loop_max_queue);
+        prof->end(st);
+        LP_CK(e);
+        LP_CK(cudaMemcpyAsync(g->h_loop, g->loop_ctl, sizeof(LoopCtl), cudaMemcpyDeviceToHost, st));
+        LP_CK(cudaStreamSynchronize(st));
+        *rounds += g->h_loop->rounds;
+        if (g->debug_rounds)
+            fprintf(stderr, "[lp] frontier loop: %d rounds, queue left %d (%d rows handed back)\n", g->h_loop->rounds,
+                    g->h_loop->out_len, g->h_loop->leftover[0] + g->h_loop->leftover[1]);
+        *done = g->h_loop->out_len == 0;
+        q = g->h_loop->out_buf;  // (the queue to route next, its length in mq_len[q])
+        a.mq_out = g->mq[q];
+        a.mq_len = g->mq_len + q;
+        next = kNextQueue;
+        return LP_OK;
+    };
     if (carry) {
         int32_t ql = 0;
         LP_CK(cudaMemcpyAsync(g->h_len, g->mq_len, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -1681,6 +1761,11 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         if (g->debug_rounds) fprintf(stderr, "[lp] sweep start: carried queue %d (dense at %lld)\n", ql, (long long)dense_at);
         if (ql == 0) return LP_OK;  // no vertex saw a neighbour change: the sweep changes nothing
         next = kNextQueue;  // (the margin test filters the queue; see the switch below)
+        if (loop_ok && ql <= g->loop_max_queue && (ql <= 4 * g->loop_rows || loop_dense)) {
+            bool done = false;
+            if (int rc = run_loop(g->mq[0], g->mq_len, 0, 1, false, &done)) return rc;
+            if (done) return LP_OK;
+        }
     }
     // Dense waves: the visit order in W consecutive position ranges, each
     // routed and evaluated after the previous one, so a wave reads the
@@ -1720,6 +1805,16 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
     int64_t last_routed = 0;
     while (true) {
         if (dbg0) cudaEventRecord(dbg0, st);
+        if (next == kNextDense && loop_dense) {
+            // every row fits the loop's warp table: the dense round (visit order) and all the
+            // frontier rounds after it in one launch
+            LP_CK(cudaMemsetAsync(g->mq_len, 0, 2 * sizeof(int32_t), st));
+            bool done = false;
+            if (int rc = run_loop(P.vorder, nullptr, (int)g->n, 0, true, &done)) return rc;
+            *gathered += P.m_active;
+            if (done) break;
+            continue;
+        }
         if (next == kNextQueue) {
             // route the queue (margin test); this round's writes queue into the other one
             LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
@@ -1792,6 +1887,11 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
             small_round = false;
             mark_pass(last_routed);  // (an empty change list marks nothing; the next route ends the loop)
             next = kNextQueue;
+            if (loop_ok && last_routed <= g->loop_rows) {
+                bool done = false;
+                if (int rc = run_loop(g->mq[q], g->mq_len + q, 0, q ^ 1, false, &done)) return rc;
+                if (done) break;
+            }
             continue;
         }
         int64_t w = 0;
@@ -1832,6 +1932,11 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         } else {
             mark_pass(w);
             next = kNextQueue;
+            if (loop_ok && w <= g->loop_rows) {
+                bool done = false;
+                if (int rc = run_loop(g->mq[q], g->mq_len + q, 0, q ^ 1, false, &done)) return rc;
+                if (done) break;
+            }
         }
     }
     if (dbg0) {
@@ -1949,6 +2054,9 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     else
         pick_fns<kUnit>(o->tie, &run_round, &setup);
     LP_CK(setup(g->device));
+    g->loop_run = g->wmode == kFixed   ? pick_loop<kFixed>(o->tie)
+                  : g->wmode == kFloat ? pick_loop<kFloat>(o->tie)
+                                       : pick_loop<kUnit>(o->tie);
 
     if (labels_init) {
         int64_t* tmp = g->out64;

@@ -2670,10 +2670,21 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                         }
                     }
                 }
-                for (int base = warp * 32; base < d && !bucketed; base += NT) {
-                    const int k = base + lane;
+                // (four label loads in flight per lane: one block walks the whole row, and a
+                // hub's 100K arcs at one dependent load per step were the round's tail)
+                constexpr int J2 = 4;
+                for (int base0 = warp * 32; base0 < d && !bucketed; base0 += NT * J2) {
+                    int32_t pl[J2];
+#pragma unroll
+                    for (int j = 0; j < J2; ++j) {
+                        const int k = base0 + j * NT + lane;
+                        pl[j] = k < d ? arc_label(a, beg + k) : 0;
+                    }
+#pragma unroll
+                    for (int j = 0; j < J2; ++j) {
+                    const int k = base0 + j * NT + lane;
                     if (k < d) {
-                        int32_t lab = arc_label(a, beg + k);
+                        int32_t lab = pl[j];
                         if (lab & kSingle) {
                             lab = lb_strip(a, lab);
                             if (parts <= 1 || part_of(lab, parts) == want) {
@@ -2697,6 +2708,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                                 }
                             }
                         }
+                    }
                     }
                 }
                 sg = (int)__reduce_add_sync(0xffffffffu, (unsigned)sg);
