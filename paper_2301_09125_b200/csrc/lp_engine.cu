@@ -1737,7 +1737,8 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
                         bool* done) -> int {
         LP_CK(cudaMemsetAsync(g->loop_ctl, 0, sizeof(LoopCtl), st));
         prof->begin(st, kKWarp);
-        const cudaError_t e = g->loop_run(g, a, list0, list0_len, list0_cnt, first_dst, dense ? 1 : 0, g->loop_max_queue);
+        const cudaError_t e = g->loop_run(g, a, list0, list0_len, list0_cnt, first_dst, dense ? 1 : 0,
+                                          loop_dense ? INT32_MAX : g->loop_max_queue);  // (every row is the loop's)
         prof->end(st);
         LP_CK(e);
         LP_CK(cudaMemcpyAsync(g->h_loop, g->loop_ctl, sizeof(LoopCtl), cudaMemcpyDeviceToHost, st));
@@ -1761,7 +1762,7 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         if (g->debug_rounds) fprintf(stderr, "[lp] sweep start: carried queue %d (dense at %lld)\n", ql, (long long)dense_at);
         if (ql == 0) return LP_OK;  // no vertex saw a neighbour change: the sweep changes nothing
         next = kNextQueue;  // (the margin test filters the queue; see the switch below)
-        if (loop_ok && ql <= g->loop_max_queue && (ql <= 4 * g->loop_rows || loop_dense)) {
+        if (loop_ok && (loop_dense || (ql <= g->loop_max_queue && ql <= 4 * g->loop_rows))) {
             bool done = false;
             if (int rc = run_loop(g->mq[0], g->mq_len, 0, 1, false, &done)) return rc;
             if (done) return LP_OK;
@@ -2646,6 +2647,7 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
             LP_CK(cudaMemcpyAsync(g->h_len, g->mq_len + q, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
             LP_CK(cudaStreamSynchronize(st));
             const int32_t work = g->h_len[0];
+            if (g->debug_rounds) fprintf(stderr, "[lp] copra sweep %d round %d: queue %d\n", it, rounds, work);
             if (work == 0) break;
             a.queue = g->mq[q];
             a.queue_len = g->mq_len + q;

@@ -102,13 +102,12 @@ __global__ void __launch_bounds__(kLoopWarps * 32) k_frontier_loop(EvalArgs a, c
             if (s < 0) continue;  // (an isolated vertex of the dense list)
             const uint32_t beg = __ldg(a.soff + s);
             const int d = (int)(__ldg(a.soff + s + 1) - beg);
-            if (d > kLoopMaxDeg) {
-                // not ours: back into the queue, mark kept (frontier) or set (dense: unless a
-                // neighbour's mark already queued it)
+            const bool ours = d <= kLoopMaxDeg;
+            if (first_dense && !ours) {
+                // not this kernel's row, unmarked: mark it so that the class kernels route it
+                // (unless a neighbour's mark has queued it already)
                 if (lane == 0) {
-                    bool push = true;
-                    if (first_dense) push = atomicAdd(a.mark + v, 1ull) == 0ull;
-                    if (push) dst[atomicAdd(dst_len, 1)] = v;
+                    if (atomicAdd(a.mark + v, 1ull) == 0ull) dst[atomicAdd(dst_len, 1)] = v;
                     atomicAdd(&ctl->leftover[r & 1], 1);
                 }
                 continue;
@@ -127,6 +126,16 @@ __global__ void __launch_bounds__(kLoopWarps * 32) k_frontier_loop(EvalArgs a, c
                         if (lane == 0) a.gap[s] = gp - 2ull * delta;
                         continue;
                     }
+                }
+                if (!ours) {
+                    // a long row that needs its evaluation: the mark goes back and the row into the
+                    // next queue for the class kernels (a marker that found the mark cleared has
+                    // queued it already)
+                    if (lane == 0) {
+                        if (atomicAdd(a.mark + v, delta ? delta : 1ull) == 0ull) dst[atomicAdd(dst_len, 1)] = v;
+                        atomicAdd(&ctl->leftover[r & 1], 1);
+                    }
+                    continue;
                 }
             }
             // ---- tally ----

@@ -211,6 +211,9 @@ __host__ __device__ __forceinline__ int32_t nd_count(int32_t v) { return v & (kM
 #ifndef LP_TEAM_U
 #define LP_TEAM_U 2
 #endif
+#ifndef LP_TEAM_J2
+#define LP_TEAM_J2 4  // label loads in flight per lane in the team kernels' flagged-label lookups
+#endif
 constexpr int kSmallMax = 16;     // thread-per-vertex bound (degree)
 #ifndef LP_WARP_REG_EST
 #define LP_WARP_REG_EST 8  // rows estimated to hold more labels skip the warp register table (LP_REG_EST;
@@ -2672,7 +2675,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : (NT == 512 ? 2 : 3)) k_te
                 }
                 // (four label loads in flight per lane: one block walks the whole row, and a
                 // hub's 100K arcs at one dependent load per step were the round's tail)
-                constexpr int J2 = 4;
+                constexpr int J2 = LP_TEAM_J2;
                 for (int base0 = warp * 32; base0 < d && !bucketed; base0 += NT * J2) {
                     int32_t pl[J2];
 #pragma unroll

@@ -289,6 +289,10 @@ def test_malformed_csr_rejected_on_upload(gpu):
     {"LP_FUSE_MAXD": "-1"},                       # every row gathers its own labels (fused)
     {"LP_FUSE_MAXD": "64", "LP_L2_PERSIST": "0"},  # small and mid rows fused; no L2 window
     {"LP_SWEEP_FRONTIER": "0"},                   # no frontier across sweeps (random ties too)
+    {"LP_LOOP_ROWS": "0"},                        # no frontier loop: every round through the class kernels
+    {"LP_LOOP_ROWS": "1000000", "LP_LOOP_MAX_QUEUE": "1000000"},  # the loop takes every frontier it can
+    {"LP_LOOP_DENSE_ARCS": "0"},                  # frontier loop for tails only (no dense rounds in it)
+    {"LP_LOOP_ROWS": "1000000", "LP_LOOP_BLOCKS": "1", "LP_DENSE_FRAC": "1.01"},  # one block per SM, long loops
 ])
 def test_engine_policies_keep_exactness(gpu, oracle, env, monkeypatch):
     """Every scheduling policy of the engine (chosen per handle from the
