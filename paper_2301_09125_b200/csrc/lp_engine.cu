@@ -166,6 +166,8 @@ struct lp_graph {
     Plan& plan() { return plans[pk]; }
     // run state
     bool l2_persist = true;  // persisting L2 window over the label arrays (set_l2_window)
+    bool fuse_forced = false;  // LP_FUSE_MAXD given: no per-run choice
+    int run_fuse = 16;         // the current run's fuse_maxd (rak_core: every row when the sweep cascades)
     int fuse_maxd = 16;      // RAK rows of degree <= this gather their labels in the tally kernel
                              // (EvalArgs::fused); >= 2^30: every row (LP_FUSE_MAXD, -1 = all)
     int32_t* labA = nullptr;
@@ -818,9 +820,9 @@ template <int WM, int TIE> struct Launcher {
         // neighbour labels inside the tally kernel (arc_label); the phase-1 pass
         // covers only the longer rows, which come first in storage order.
         const bool rak = alg == kGatherRak;
-        const bool fuse_all = rak && g->fuse_maxd >= (1 << 30);
-        const bool fuse_small = rak && g->fuse_maxd >= kSmallMax;
-        const bool fuse_mid = rak && a.mid_max > 0 && g->fuse_maxd >= a.mid_max;
+        const bool fuse_all = rak && g->run_fuse >= (1 << 30);
+        const bool fuse_small = rak && g->run_fuse >= kSmallMax;
+        const bool fuse_mid = rak && a.mid_max > 0 && g->run_fuse >= a.mid_max;
         const int64_t gather_arcs = fuse_all ? 0 : fuse_mid ? P.arcs_gt_mid : fuse_small ? P.arcs_gt16 : P.m_active;
         EvalArgs af = a, ag = a;  // fused / two-phase launches
         af.fused = 1;
@@ -858,6 +860,12 @@ template <int WM, int TIE> struct Launcher {
                 prof->end(sB);
             }
         };
+        auto join = [&]() {
+            cudaEventRecord(g->ev_join[0], sB);
+            cudaEventRecord(g->ev_join[1], sC);
+            cudaStreamWaitEvent(st, g->ev_join[0], 0);
+            cudaStreamWaitEvent(st, g->ev_join[1], 0);
+        };
         if (fuse_small) small_rows(af);
         // ---- route the big rows (dense rounds) ----
         if (dense && P.big_end > 0) {
@@ -890,12 +898,24 @@ template <int WM, int TIE> struct Launcher {
             prof->end(st);
         }
         cudaEventRecord(g->ev_gather, st);
+        const bool big = dense && P.big_end > 0;
+        auto hub_rows = [&]() {
+            if (!(big || h_len[kLenHub] > 0)) return;
+            cudaStreamWaitEvent(sC, g->ev_gather, 0);
+            EvalArgs b = ag;
+            b.bin = kKHub;
+            prof->begin(sC, kKHub);
+            if (b.hb_off) k_hub_bucket<<<sms * 2, 1024, 0, sC>>>(b);
+            const int grid = dense ? sms * occ_hub : grid_for(h_len[kLenHub], 1, sms * occ_hub);
+            k_team<WM, TIE, kHubThreads, kHubBits, true>
+                <<<grid, kHubThreads, team_smem_bytes<WM, kHubBits>(), sC>>>(b, kLenHub);
+            prof->end(sC);
+        };
         // ---- phase 2: tally ----
         if (!fuse_small) {
             cudaStreamWaitEvent(sB, g->ev_gather, 0);
             small_rows(ag);
         }
-        const bool big = dense && P.big_end > 0;
         if (a.mid_max > 0 && (big || h_len[kLenMid] > 0)) {
             cudaStreamWaitEvent(sB, fuse_mid ? g->ev_route : g->ev_gather, 0);
             EvalArgs b = fuse_mid ? af : ag;
@@ -937,21 +957,8 @@ template <int WM, int TIE> struct Launcher {
                 <<<grid, kTeam2Threads, team_smem_bytes<WM, kTeam2Bits>(), sB>>>(b, kLenTeam2);
             prof->end(sB);
         }
-        if (big || h_len[kLenHub] > 0) {
-            cudaStreamWaitEvent(sC, g->ev_gather, 0);
-            EvalArgs b = ag;
-            b.bin = kKHub;
-            prof->begin(sC, kKHub);
-            if (b.hb_off) k_hub_bucket<<<sms * 2, 1024, 0, sC>>>(b);
-            const int grid = dense ? sms * occ_hub : grid_for(h_len[kLenHub], 1, sms * occ_hub);
-            k_team<WM, TIE, kHubThreads, kHubBits, true>
-                <<<grid, kHubThreads, team_smem_bytes<WM, kHubBits>(), sC>>>(b, kLenHub);
-            prof->end(sC);
-        }
-        cudaEventRecord(g->ev_join[0], sB);
-        cudaEventRecord(g->ev_join[1], sC);
-        cudaStreamWaitEvent(st, g->ev_join[0], 0);
-        cudaStreamWaitEvent(st, g->ev_join[1], 0);
+        hub_rows();
+        join();
         // (the deferred marks of the rows that changed this round are launched
         // by the sweep driver: mark_pass)
     }
@@ -1427,7 +1434,10 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     if (cudaGetDevice(&g->device) != cudaSuccess) return fail(lp_fail(LP_ERR_CUDA, "cudaGetDevice failed"));
     cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device);
     if (const char* ev = getenv("LP_L2_PERSIST")) g->l2_persist = atoi(ev) != 0;
-    if (const char* ev = getenv("LP_FUSE_MAXD")) g->fuse_maxd = atoi(ev) < 0 ? (1 << 30) : atoi(ev);
+    if (const char* ev = getenv("LP_FUSE_MAXD")) {
+        g->fuse_maxd = atoi(ev) < 0 ? (1 << 30) : atoi(ev);
+        g->fuse_forced = true;
+    }
     if (const char* ev = getenv("LP_WAVES")) g->waves = std::max(1, std::min(1024, atoi(ev)));
     if (const char* ev = getenv("LP_LOOP_ROWS")) g->loop_rows = std::max(0, atoi(ev));
     if (const char* ev = getenv("LP_LOOP_DENSE_ARCS")) g->loop_dense_arcs = std::max(0, atoi(ev));
@@ -2124,9 +2134,19 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.mid_max = g->mid_max > kSmallMax ? g->mid_max : 0;
     a.fused = 0;  // (per launch: Launcher::round)
     // fused row classes: k_small rows (d <= 16), k_mid rows (d <= mid_max), or all
-    a.fuse_maxd = g->fuse_maxd >= (1 << 30) ? INT32_MAX
-                  : (a.mid_max > 0 && g->fuse_maxd >= a.mid_max) ? a.mid_max
-                  : g->fuse_maxd >= kSmallMax ? kSmallMax : 0;
+    // Exact schedules whose first sweep cascades -- weights or random ties: the all-singleton
+    // tallies of a sweep from ids have leads near zero, so nearly every changed neighbour passes
+    // the margin test -- fuse every row: a tally that reads the working labels in place sees what
+    // the round has already written (Gauss-Seidel inside the round), where the phase-1 snapshot
+    // repeats the whole cascade level by level (R-MAT-22 float32 weights 57 -> 32 ms on average --
+    // 23 to 41: how the round's streams interleave decides how many full rounds the first sweep
+    // takes -- random ties 31 -> 25 ms; unit weights with scan-first ties: two-phase long rows
+    // stay 7% faster, 5.87 vs 6.27 ms).
+    g->run_fuse = g->fuse_forced ? g->fuse_maxd
+                  : (cross && (g->wmode != kUnit || o->tie == kRandom)) ? (1 << 30) : g->fuse_maxd;
+    a.fuse_maxd = g->run_fuse >= (1 << 30) ? INT32_MAX
+                  : (a.mid_max > 0 && g->run_fuse >= a.mid_max) ? a.mid_max
+                  : g->run_fuse >= kSmallMax ? kSmallMax : 0;
 
     LP_CK(cudaMemsetAsync(g->counters, 0, kCtrCount * sizeof(unsigned long long), st));
     Prof prof;
@@ -2222,7 +2242,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     g->labels_valid = true;
     if (int rc = finish_stats(g, prof, S, it, rounds, gathered, ms)) return rc;
     S->arcs_dense = g->m * it;
-    if (g->fuse_maxd >= (1 << 30)) S->flags |= LP_STATS_FUSED;
+    if (g->run_fuse >= (1 << 30)) S->flags |= LP_STATS_FUSED;
 #ifdef LP_PATH_STATS
     {
         unsigned long long h[8];

@@ -33,6 +33,6 @@ for b in args.batches:
         labels, it, st, changed = lp.rak_labels(g, p, device_graph=dg)
         if r:
             ms.append(st["kernel_ms"])
-    print(f"{args.tag} {args.config} batches={b} {'non-strict' if args.non_strict else 'strict'}: "
+    print(f"{args.tag} {args.config} batches={b} {'non-strict' if args.non_strict else 'strict'}: mean {np.mean(ms):.3f} "
           f"median {np.median(ms):.3f} ms min {min(ms):.3f} it {it} rounds {st['rounds']} "
           f"changed {changed.tolist()} labels_hash {hash(labels.tobytes()) & 0xffffffff:08x}", flush=True)
