@@ -1694,7 +1694,7 @@ static EvalArgs marks_mode(lp_graph* g, const EvalArgs& a, int64_t changed_rows)
 
 static void bits_to_queue(lp_graph* g, const EvalArgs& a) {
     if (!a.mbits) {
-        k_marks_to_queue<<<grid_for(g->n, 256, g->num_sms * 8), 256, 0, g->stream>>>(g->mark, g->n, a.mq_out, a.mq_len);
+        k_marks_to_queue<<<grid_for(g->n, 256 * 8, g->num_sms * 8), 256, 0, g->stream>>>(g->mark, g->n, a.mq_out, a.mq_len);
         return;
     }
     const int64_t nwords = g->n / 32 + 1;
@@ -1726,6 +1726,14 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         k_mark_pieces<<<grid_for(pieces, 4 * 8, g->num_sms * 16), 256, 0, st>>>(b);
         if (compact) bits_to_queue(g, b);
         prof->end(st);
+    };
+    // the tally kernels' arguments: without cross-batch reads (synchronous schedule) one round is
+    // the sweep and nobody walks the round's changed rows -- no list (the sweep boundary rebuilds
+    // it from the labels); one append per warp on the list's counter is measurable
+    auto targs = [&]() {
+        EvalArgs t = a;
+        if (!cross) t.mark = nullptr;
+        return t;
     };
     // writes of the round just run (label changes); one sync
     auto round_writes = [&](int64_t* w) -> int {
@@ -1794,7 +1802,7 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
             LP_CK(cudaStreamSynchronize(st));
             a.horizon = (int32_t)std::min<int64_t>(g->n, (w + 1) * ws);
             if (g->h_len[kLenRouted] > 0) {
-                run_round(g, a, false, g->h_len, prof, alg);
+                run_round(g, targs(), false, g->h_len, prof, alg);
                 if (a.mark) mark_pass(g->n, false);
             }
             ++*rounds;
@@ -1853,10 +1861,10 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
                 // routed frontier (the routes are dropped; every margin is refreshed)
                 LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
                 LP_CK(cudaMemsetAsync(g->mq_len + q, 0, sizeof(int32_t), st));
-                run_round(g, a, true, g->h_len, prof, alg);
+                run_round(g, targs(), true, g->h_len, prof, alg);
                 if (alg == kGatherRak) *gathered += P.m_active;
             } else {
-                run_round(g, a, false, g->h_len, prof, alg);
+                run_round(g, targs(), false, g->h_len, prof, alg);
                 // a routed frontier smaller than the full-round threshold cannot write
                 // that many labels: no need to read the write count (one sync less)
                 int64_t routed = 0;
@@ -1876,19 +1884,24 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
                 a.bin = kKSmall;
                 prof->begin(st, kKSmall);
                 if (g->wmode == kFixed) {
-                    k_first_round_wbig<<<g->num_sms * 4, 256, 0, st>>>(a, (int32_t)P.S);
-                    k_first_round_w<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S);
+                    k_first_round_wbig<<<g->num_sms * 4, 256, 0, st>>>(targs(), (int32_t)P.S);
+                    k_first_round_w<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(targs(), (int32_t)P.S);
                 }
                 else if (first_random) {
-                    k_first_round_rbig<<<g->num_sms * 4, 256, 0, st>>>(a, (int32_t)P.S);
-                    k_first_round_r<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S);
+                    k_first_round_rbig<<<g->num_sms * 4, 256, 0, st>>>(targs(), (int32_t)P.S);
+                    k_first_round_r<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(targs(), (int32_t)P.S);
                 }
-                else
-                    k_first_round<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(a, (int32_t)P.S, P.slot_of,
+                else {
+                    // (a full round always follows the chained guess: its changed rows need no list --
+                    // one append per warp on the list's single counter was a third of this kernel)
+                    EvalArgs af = targs();
+                    if (first_chain) af.mark = nullptr;
+                    k_first_round<<<grid_for(P.S, 256, g->num_sms * 16), 256, 0, st>>>(af, (int32_t)P.S, P.slot_of,
                                                                                       first_chain ? 1 : 0);
+                }
                 prof->end(st);
             } else {
-                run_round(g, a, true, g->h_len, prof, alg);  // (refreshes every margin)
+                run_round(g, targs(), true, g->h_len, prof, alg);  // (refreshes every margin)
                 if (alg == kGatherRak) *gathered += P.m_active;  // (piece gathers count themselves)
             }
         }

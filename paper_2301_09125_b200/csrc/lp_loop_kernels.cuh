@@ -28,6 +28,8 @@ namespace lp {
 
 constexpr int kLoopBits = 9;                               // 512-slot table per warp
 constexpr int kLoopMaxDeg = (1 << kLoopBits) / 4 * 3;      // rows up to 384 arcs can never overflow it
+constexpr int kLoopLongDeg = 2048;                         // frontier rounds also try rows up to this long: a
+                                                           // late sweep's rows hold few distinct labels
 constexpr int kLoopWarps = 8;
 
 struct LoopCtl {
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(kLoopWarps * 32) k_frontier_loop(EvalArgs a, c
             if (s < 0) continue;  // (an isolated vertex of the dense list)
             const uint32_t beg = __ldg(a.soff + s);
             const int d = (int)(__ldg(a.soff + s + 1) - beg);
-            const bool ours = d <= kLoopMaxDeg;
+            const bool ours = d <= (first_dense ? kLoopMaxDeg : kLoopLongDeg);
             if (first_dense && !ours) {
                 // not this kernel's row, unmarked: mark it so that the class kernels route it
                 // (unless a neighbour's mark has queued it already)
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(kLoopWarps * 32) k_frontier_loop(EvalArgs a, c
                 }
                 continue;
             }
+            unsigned long long delta0 = 0ull;  // (the mark taken from v, should the row go back)
             if (!first_dense) {
                 // margin test on the weight that changed since v's last evaluation (k_route_queue);
                 // fetch-and-clear: a concurrent mark either lands before (counted in delta, its label
@@ -119,6 +122,7 @@ __global__ void __launch_bounds__(kLoopWarps * 32) k_frontier_loop(EvalArgs a, c
                 unsigned long long delta = 0ull;
                 if (lane == 0) delta = atomicExch(a.mark + v, 0ull);
                 delta = __shfl_sync(0xffffffffu, delta, 0);
+                delta0 = delta;
                 __threadfence();
                 if (a.gap) {
                     const unsigned long long gp = __ldcg(a.gap + s);
@@ -140,6 +144,7 @@ __global__ void __launch_bounds__(kLoopWarps * 32) k_frontier_loop(EvalArgs a, c
             }
             // ---- tally ----
             int ntouched = 0;
+            bool overflow = false;
             for (int base = 0; base < d; base += 32) {
                 const int k = base + lane;
                 int32_t lab = kEmpty;
@@ -153,9 +158,27 @@ __global__ void __launch_bounds__(kLoopWarps * 32) k_frontier_loop(EvalArgs a, c
                 bool full = false;
                 const int h = insert_chunk<WM, kLoopBits>(tab->t, lab, w, true, full);
                 const uint32_t nb = __ballot_sync(0xffffffffu, h >= 0);
-                if (h >= 0) tab->touched[ntouched + __popc(nb & lanemask_lt())] = (uint16_t)h;
+                if (h >= 0) {
+                    const int idx = ntouched + __popc(nb & lanemask_lt());
+                    if (idx < kLoopMaxDeg + 32) tab->touched[idx] = (uint16_t)h;
+                }
                 ntouched += __popc(nb);
                 __syncwarp();
+                if (ntouched > kLoopMaxDeg || __any_sync(0xffffffffu, full)) {
+                    overflow = true;
+                    break;
+                }
+            }
+            if (overflow) {
+                // more distinct labels than the warp table takes: wipe it, the class kernels
+                // evaluate the row (mark restored as for a row that is not ours)
+                for (int h = lane; h < (1 << kLoopBits); h += 32) tab->t.init(h);
+                __syncwarp();
+                if (lane == 0) {
+                    if (atomicAdd(a.mark + v, delta0 ? delta0 : 1ull) == 0ull) dst[atomicAdd(dst_len, 1)] = v;
+                    atomicAdd(&ctl->leftover[r & 1], 1);
+                }
+                continue;
             }
             const uint32_t vtx = (uint32_t)v;
             const Best<A> b = table_argmax<WM, TIE, kLoopBits, 1>(tab->t, tab->touched, ntouched, lane, a.seed, a.sweep,

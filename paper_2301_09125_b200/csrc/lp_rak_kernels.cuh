@@ -521,6 +521,37 @@ __device__ __forceinline__ void push_changed_small(const EvalArgs& a, bool ch, i
     }
 }
 
+// every thread of a <= 1024-thread block, rows of <= kPieceArcs arcs: one atomic per block (the
+// changed list's length is one counter for the whole grid; a dense round of small rows appended
+// to it once per warp, ~100K times in ~100 us).  sw: 2 x 34 shared words, `par` alternates.
+__device__ __forceinline__ void push_changed_block(const EvalArgs& a, bool ch, int32_t s, int32_t (*sw)[34], int par) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    const uint32_t bal = __ballot_sync(0xffffffffu, ch);
+    int32_t* w = sw[par & 1];
+    if (lane == 0) w[warp] = __popc(bal);
+    __syncthreads();
+    if (warp == 0) {
+        const int c = lane < nw ? w[lane] : 0;
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        int b0 = 0;
+        if (lane == 0 && tot) b0 = atomicAdd(a.r.len + kLenChg, tot);
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (lane < nw) w[lane] = b0 + incl - c;
+    }
+    __syncthreads();
+    if (ch) {
+        const int idx = w[warp] + __popc(bal & lanemask_lt());
+        a.r.cslot[idx] = s;
+        a.r.ck0[idx] = 0;
+    }
+}
+
 // whole warp: lane v pushes row (s, d) when bit v of `chm` is set
 __device__ __forceinline__ void push_changed_batch(const EvalArgs& a, uint32_t chm, int32_t s, int d) {
     const int lane = threadIdx.x & 31;
@@ -759,17 +790,36 @@ __global__ void __launch_bounds__(256) k_mark_pieces(EvalArgs a) {
 // marked arc (marks are zero again once routed).
 __global__ void k_marks_to_queue(const unsigned long long* __restrict__ mark, int64_t n, int32_t* __restrict__ mq_out,
                                  int32_t* mq_len) {
+    // (eight vertices per lane: one append per 256 vertices -- every append of the grid lands on
+    // the same counter, and at one per 32 vertices that counter was the kernel's time)
+    constexpr int J = 8;
     const int lane = threadIdx.x & 31;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
-        const int64_t v = base + threadIdx.x;
-        const bool nz = v < n && __ldcg(mark + v) != 0ull;
-        const uint32_t bal = __ballot_sync(0xffffffffu, nz);
-        if (!bal) continue;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = warp * 32 * J; base < n; base += warps * 32 * J) {
+        const int64_t v0 = base + lane * J;
+        uint32_t nz = 0;
+#pragma unroll
+        for (int j = 0; j < J; ++j)
+            if (v0 + j < n && __ldcg(mark + v0 + j) != 0ull) nz |= 1u << j;
+        const int c = __popc(nz);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (tot == 0) continue;
         int b0 = 0;
-        if (lane == 0) b0 = atomicAdd(mq_len, __popc(bal));
-        b0 = __shfl_sync(0xffffffffu, b0, 0);
-        if (nz) mq_out[b0 + __popc(bal & lanemask_lt())] = (int32_t)v;
+        if (lane == 31) b0 = atomicAdd(mq_len, tot);
+        b0 = __shfl_sync(0xffffffffu, b0, 31);
+        int o = b0 + incl - c;
+        while (nz) {
+            const int j = __ffs(nz) - 1;
+            mq_out[o++] = (int32_t)(v0 + j);
+            nz &= nz - 1u;
+        }
     }
 }
 
@@ -909,11 +959,19 @@ __global__ void k_route_dense(EvalArgs a, int32_t s_beg, int32_t s_end) {
 
 // Frontier round: the queued (marked) vertices -> route lists + phase-1
 // pieces; marks are cleared so this round's writes can queue them again.
-__global__ void k_route_queue(EvalArgs a, const int32_t* __restrict__ mq_in, const int32_t* __restrict__ mq_in_len,
-                              const int32_t* __restrict__ slot_of, int clear_marks) {
+__global__ void __launch_bounds__(256) k_route_queue(EvalArgs a, const int32_t* __restrict__ mq_in,
+                                                     const int32_t* __restrict__ mq_in_len,
+                                                     const int32_t* __restrict__ slot_of, int clear_marks) {
+    // The appends are aggregated per block: lists 0-8 (hubs apart), the phase-1 pieces and the
+    // routed count take one global atomic per 256 queue entries each -- every warp of the grid
+    // appending to the same few counters was the kernel's time on long queues.
+    enum { kPieces = 9, kRouted = 10, kSlots = 11 };
+    __shared__ int32_t s_cnt[kSlots], s_base[kSlots];
     const int lane = threadIdx.x & 31;
     const int cnt = *mq_in_len;
     for (int base = blockIdx.x * blockDim.x; base < cnt; base += gridDim.x * blockDim.x) {
+        if (threadIdx.x < kSlots) s_cnt[threadIdx.x] = 0;
+        __syncthreads();
         const int i = base + threadIdx.x;
         int cls = -1, est = 0, d = 0;
         int32_t s = -1;
@@ -937,28 +995,65 @@ __global__ void k_route_queue(EvalArgs a, const int32_t* __restrict__ mq_in, con
             }
             if (s >= 0) cls = route_class(a, s, est, d);
         }
-        route_append(a, cls, s, est, d);
+        // ---- block-local positions ----
+        int idx = 0;  // position of this entry in its list, from the block's base
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+            if (c == 5) continue;  // hubs below
+            const uint32_t m = __ballot_sync(0xffffffffu, cls == c);
+            if (!m) continue;
+            const int leader = __ffs(m) - 1;
+            int b = 0;
+            if (lane == leader) b = atomicAdd(&s_cnt[c], __popc(m));
+            b = __shfl_sync(0xffffffffu, b, leader);
+            if (cls == c) idx = b + __popc(m & lanemask_lt());
+        }
         // phase-1 pieces of the routed row (none for fused rows)
         const int np_all = cls >= 0 ? (d + kPieceArcs - 1) / kPieceArcs : 0;
         const int np = d > a.fuse_maxd ? np_all : 0;
-        const uint32_t act = __activemask();
         {
-            const unsigned routed = __reduce_add_sync(act, (unsigned)np_all);
-            if (routed && lane == __ffs(act) - 1) atomicAdd(a.r.len + kLenRouted, (int32_t)routed);
+            const unsigned routed = __reduce_add_sync(0xffffffffu, (unsigned)np_all);
+            if (routed && lane == 0) atomicAdd(&s_cnt[kRouted], (int32_t)routed);
         }
         int incl = np;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(act, incl, o);
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t;
         }
-        const int tot = __shfl_sync(act, incl, 31);
-        int b0 = 0;
-        if (lane == 31 && tot) b0 = atomicAdd(a.r.len + kLenGather, tot);
-        b0 = __shfl_sync(act, b0, 31);
-        for (int q = 0; q < np; ++q) {
-            a.r.gslot[b0 + incl - np + q] = s;
-            a.r.gk0[b0 + incl - np + q] = q * kPieceArcs;
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        int pb = 0;
+        if (lane == 31 && tot) pb = atomicAdd(&s_cnt[kPieces], tot);
+        pb = __shfl_sync(0xffffffffu, pb, 31);
+        __syncthreads();
+        if (threadIdx.x < kSlots && s_cnt[threadIdx.x]) {
+            const int c = threadIdx.x;
+            const int g = c == kPieces ? kLenGather : c == kRouted ? kLenRouted : c == 7 ? kLenTeam2 : c == 8 ? kLenMid : c;
+            s_base[c] = atomicAdd(a.r.len + g, s_cnt[c]);
+        }
+        __syncthreads();
+        if (cls >= 0 && cls != 5) {
+            const int at = s_base[cls] + idx;
+            if (cls == 8) {
+                a.r.mid[at] = s;
+            } else if (cls < 3) {
+                a.r.small[cls][at] = s;
+            } else if (cls == 3) {
+                a.r.warp[0][at] = s;
+            } else if (cls == 6) {
+                a.r.warp[1][at] = s;
+            } else {
+                Item t = {s, 0, 1, 0, 1, -1, 0, 0};
+                (cls == 7 ? a.r.team2 : a.r.team)[at] = t;
+            }
+        }
+        if (cls == 5) route_append(a, cls, s, est, d);  // (hub items: the row's own atomics)
+        if (np) {
+            const int b0 = s_base[kPieces] + pb;
+            for (int q = 0; q < np; ++q) {
+                a.r.gslot[b0 + incl - np + q] = s;
+                a.r.gk0[b0 + incl - np + q] = q * kPieceArcs;
+            }
         }
     }
 }
@@ -1255,8 +1350,15 @@ __global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, i
     const int32_t cnt = listed ? a.r.len[LIST] : (s_end - s_beg);
     const int32_t* list = a.r.small[LIST];
     long long dchg = 0, arcs = 0, writes = 0, verts = 0;
-    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-        const int32_t s = listed ? list[i] : s_beg + i;
+    __shared__ int32_t s_push[2][34];
+    int par = 0;
+    // (block-uniform trip count: the changed rows of an iteration are appended per block)
+    for (int32_t base = blockIdx.x * blockDim.x; base < cnt; base += gridDim.x * blockDim.x, ++par) {
+        const int32_t i = base + threadIdx.x;
+        bool ch = false;
+        int32_t s = 0;
+        if (i < cnt) do {
+        s = listed ? list[i] : s_beg + i;
         const int32_t p = __ldg(a.svid + s);
         const uint32_t beg = __ldg(a.soff + s);
         const int d = (int)(__ldg(a.soff + s + 1) - beg);
@@ -1288,7 +1390,7 @@ __global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, i
                 if (lab[k] == cand) cw += w[k];
             if (cw + cw > total) {  // strict majority: label unchanged
                 store_gap<A>(a, s, cw, total);
-                continue;
+                break;
             }
         }
         const uint32_t vtx = (uint32_t)p;
@@ -1322,8 +1424,9 @@ __global__ void __launch_bounds__(256, MAXD == 16 ? 3 : 4) k_small(EvalArgs a, i
         const int32_t nd_new = (best.w + best.w > total) ? kMajBit : 0;
         if (nd_new != nd) a.ndist[s] = nd_new;
         store_lead<A>(a, s, w1, w2);
-        const bool ch = commit_label_known(a, p, best.lab, xv, l0v, dchg, writes);
-        if (a.mark) push_changed_small(a, ch, s);
+        ch = commit_label_known(a, p, best.lab, xv, l0v, dchg, writes);
+        } while (0);
+        if (a.mark) push_changed_block(a, ch, s, s_push, par);
     }
     flush_counters(a, dchg, arcs, writes, verts);
 }
@@ -2031,12 +2134,28 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 && WM == k
     // ... and adapted to the arcs a batch held: the routed lists put long rows
     // first, and 32 of them in one warp's batch is a tail of the whole kernel
     int bsz = min(bcap, 2);
+#ifdef LP_WARP_CLAIM_AHEAD
+    // the next batch is claimed while this one is evaluated: the cursor is one counter for the
+    // whole grid, and its round trip would otherwise sit between two batches of every warp
+    int32_t nb0 = 0;
+    int nbsz = bsz;
+    if (lane == 0) nb0 = atomicAdd(a.r.len + cursor, nbsz);
+#endif
     while (true) {
+#ifdef LP_WARP_CLAIM_AHEAD
+        const int32_t b0 = __shfl_sync(0xffffffffu, nb0, 0);
+        const int cur = nbsz;
+        if (b0 >= cnt) break;
+        const int nv = min(cur, cnt - b0);
+        nbsz = bsz;
+        if (lane == 0) nb0 = atomicAdd(a.r.len + cursor, nbsz);
+#else
         int32_t b0 = 0;
         if (lane == 0) b0 = atomicAdd(a.r.len + cursor, bsz);
         b0 = __shfl_sync(0xffffffffu, b0, 0);
         if (b0 >= cnt) break;
         const int nv = min(bsz, cnt - b0);
+#endif
         int32_t ms = -1, mp = 0, mnd = 0, mx = 0, ml0 = 0;
         uint32_t mbeg = 0, mend = 0;
         if (lane < nv) {
