@@ -552,6 +552,42 @@ __device__ __forceinline__ void push_changed_block(const EvalArgs& a, bool ch, i
     }
 }
 
+// ... the same for rows of any length (np pieces each; every thread of the block calls)
+__device__ __forceinline__ void push_changed_rows_block(const EvalArgs& a, bool ch, int32_t s, int d, int32_t (*sw)[34],
+                                                        int par) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    const int np = ch ? (d + kPieceArcs - 1) / kPieceArcs : 0;
+    int wi = np;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += t;
+    }
+    int32_t* w = sw[par & 1];
+    if (lane == 31) w[warp] = wi;
+    __syncthreads();
+    if (warp == 0) {
+        const int c = lane < nw ? w[lane] : 0;
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        int b0 = 0;
+        if (lane == 0 && tot) b0 = atomicAdd(a.r.len + kLenChg, tot);
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (lane < nw) w[lane] = b0 + incl - c;
+    }
+    __syncthreads();
+    const int at = w[warp] + wi - np;
+    for (int q = 0; q < np; ++q) {
+        a.r.cslot[at + q] = s;
+        a.r.ck0[at + q] = q * kPieceArcs;
+    }
+}
+
 // whole warp: lane v pushes row (s, d) when bit v of `chm` is set
 __device__ __forceinline__ void push_changed_batch(const EvalArgs& a, uint32_t chm, int32_t s, int d) {
     const int lane = threadIdx.x & 31;
@@ -577,7 +613,9 @@ __device__ __forceinline__ void push_changed_batch(const EvalArgs& a, uint32_t c
 // k_mark_pieces (mark_all) can queue every neighbour for the next sweep.
 __global__ void k_sweep_changes(EvalArgs a, const int32_t* __restrict__ lnew, const int32_t* __restrict__ lold,
                                 int32_t S) {
-    for (int32_t base = blockIdx.x * blockDim.x; base < S; base += gridDim.x * blockDim.x) {
+    __shared__ int32_t s_push[2][34];
+    int par = 0;
+    for (int32_t base = blockIdx.x * blockDim.x; base < S; base += gridDim.x * blockDim.x, ++par) {
         const int32_t s = base + threadIdx.x;
         bool ch = false;
         int d = 0;
@@ -586,7 +624,7 @@ __global__ void k_sweep_changes(EvalArgs a, const int32_t* __restrict__ lnew, co
             ch = lnew[v] != lold[v];
             d = (int)(__ldg(a.soff + s + 1) - __ldg(a.soff + s));
         }
-        push_changed_batch(a, __ballot_sync(0xffffffffu, ch), s, d);
+        push_changed_rows_block(a, ch, s, d, s_push, par);
     }
 }
 
@@ -1081,8 +1119,10 @@ __global__ void __launch_bounds__(256) k_route_queue(EvalArgs a, const int32_t* 
 __global__ void __launch_bounds__(256) k_first_round(EvalArgs a, int32_t S, const int32_t* __restrict__ slot_of,
                                                      int chain) {
     long long dchg = 0, arcs = 0, writes = 0, verts = 0;
-    // (warp-uniform loop: the changed rows are pushed as pieces by the whole warp)
-    for (int32_t base = blockIdx.x * blockDim.x; base < S; base += gridDim.x * blockDim.x) {
+    __shared__ int32_t s_push[2][34];
+    int par = 0;
+    // (block-uniform loop: the changed rows are pushed as pieces by the whole block)
+    for (int32_t base = blockIdx.x * blockDim.x; base < S; base += gridDim.x * blockDim.x, ++par) {
         const int32_t s = base + threadIdx.x;
         bool ch = false;
         int d = 0;
@@ -1102,7 +1142,7 @@ __global__ void __launch_bounds__(256) k_first_round(EvalArgs a, int32_t S, cons
             store_lead<uint32_t>(a, s, 1u, d > 1 ? 1u : 0u);
             ch = commit_label_known(a, p, lab, p, p, dchg, writes);
         }
-        if (a.mark) push_changed_batch(a, __ballot_sync(0xffffffffu, ch), s, d);
+        if (a.mark) push_changed_rows_block(a, ch, s, d, s_push, par);
     }
     flush_counters(a, dchg, arcs, writes, verts);
 }
@@ -2134,28 +2174,12 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 && WM == k
     // ... and adapted to the arcs a batch held: the routed lists put long rows
     // first, and 32 of them in one warp's batch is a tail of the whole kernel
     int bsz = min(bcap, 2);
-#ifdef LP_WARP_CLAIM_AHEAD
-    // the next batch is claimed while this one is evaluated: the cursor is one counter for the
-    // whole grid, and its round trip would otherwise sit between two batches of every warp
-    int32_t nb0 = 0;
-    int nbsz = bsz;
-    if (lane == 0) nb0 = atomicAdd(a.r.len + cursor, nbsz);
-#endif
     while (true) {
-#ifdef LP_WARP_CLAIM_AHEAD
-        const int32_t b0 = __shfl_sync(0xffffffffu, nb0, 0);
-        const int cur = nbsz;
-        if (b0 >= cnt) break;
-        const int nv = min(cur, cnt - b0);
-        nbsz = bsz;
-        if (lane == 0) nb0 = atomicAdd(a.r.len + cursor, nbsz);
-#else
         int32_t b0 = 0;
         if (lane == 0) b0 = atomicAdd(a.r.len + cursor, bsz);
         b0 = __shfl_sync(0xffffffffu, b0, 0);
         if (b0 >= cnt) break;
         const int nv = min(bsz, cnt - b0);
-#endif
         int32_t ms = -1, mp = 0, mnd = 0, mx = 0, ml0 = 0;
         uint32_t mbeg = 0, mend = 0;
         if (lane < nv) {
