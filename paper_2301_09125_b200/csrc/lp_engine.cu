@@ -224,9 +224,10 @@ struct lp_graph {
     int waves = 1;  // dense waves of the cross-batch schedules (LP_WAVES overrides)
     // frontier loop (lp_loop_kernels.cuh): rounds that evaluate at most loop_rows rows continue on the
     // device in one cooperative launch (LP_LOOP_ROWS, 0 = off); graphs whose rows all fit the loop's
-    // warp table and hold at most loop_dense_arcs arcs run their dense rounds there too (LP_LOOP_DENSE_ARCS)
+    // warp table, hold at most loop_dense_arcs arcs and average >= 12 arcs a row run their dense rounds
+    // there too (LP_LOOP_DENSE_ARCS; SLPA planted-1M 21 -> 14 ms)
     int64_t loop_rows = 8192;
-    int64_t loop_dense_arcs = 16 << 20;
+    int64_t loop_dense_arcs = 64 << 20;
     int loop_max_queue = 1 << 16;
     int loop_blocks_per_sm = 0;  // 0 = the kernel's occupancy (LP_LOOP_BLOCKS)
     LoopCtl* loop_ctl = nullptr;  // device
@@ -1090,8 +1091,7 @@ static void destroy_graph(lp_graph* g) {
     dfree(g->out64);
     dfree(g->cub_tmp);
     if (g->h_len) cudaFreeHost(g->h_len);
-    if (g->h_loop) cudaFreeHost(g->h_loop);
-    if (g->loop_ctl) cudaFree(g->loop_ctl);
+    dfree(g->loop_ctl);
     if (g->h_counters) cudaFreeHost(g->h_counters);
     for (cudaEvent_t e : g->event_pool) cudaEventDestroy(e);
     if (g->ev0) cudaEventDestroy(g->ev0);
@@ -1519,9 +1519,10 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
     G_CK(dalloc(&g->counters, 32, &g->bytes));
     G_CK(dalloc(&g->out64, n, &g->bytes));
     G_CK(cudaMallocHost((void**)&g->h_len, kLenCount * sizeof(int32_t)));
-    G_CK(cudaMallocHost((void**)&g->h_loop, sizeof(LoopCtl)));
-    G_CK(cudaMalloc((void**)&g->loop_ctl, sizeof(LoopCtl)));
-    G_CK(cudaMallocHost((void**)&g->h_counters, 32 * sizeof(unsigned long long)));
+    G_CK(pool_alloc(&g->loop_ctl, sizeof(LoopCtl)));
+    // (pinned: 32 counter words, then the frontier loop's control block)
+    G_CK(cudaMallocHost((void**)&g->h_counters, 32 * sizeof(unsigned long long) + sizeof(LoopCtl)));
+    g->h_loop = reinterpret_cast<LoopCtl*>(g->h_counters + 32);
     G_CK(cudaMemsetAsync(g->mark, 0, (n + 4) * sizeof(unsigned long long), st));
     G_CK(cudaMemsetAsync(g->gap, 0, (n + 4) * sizeof(unsigned long long), st));
     G_CK(cudaMemsetAsync(g->counters, 0, 32 * sizeof(unsigned long long), st));
@@ -1749,8 +1750,10 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
     // The frontier loop: the rounds from here on run in one cooperative launch (lp_loop_kernels.cuh)
     // until a round queues nothing (*done) or the queue comes back (rows longer than the loop's
     // table, or more than loop_max_queue of them): then the class kernels route mq[q] as usual.
-    const bool loop_ok = g->loop_run && alg == kGatherRak && cross && a.mark && g->loop_rows > 0;
-    const bool loop_dense = loop_ok && g->max_degree <= kLoopMaxDeg && P.m_active <= g->loop_dense_arcs;
+    const bool loop_ok = g->loop_run && cross && a.mark && g->loop_rows > 0;  // (RAK and SLPA: a.slots)
+    // (warp per row: not for graphs of very short rows -- the grid's 4-arc rows stay thread per row)
+    const bool loop_dense = loop_ok && g->max_degree <= kLoopMaxDeg && P.m_active <= g->loop_dense_arcs &&
+                            P.m_active >= 12 * P.S;
     auto run_loop = [&](const int32_t* list0, const int32_t* list0_len, int list0_cnt, int first_dst, bool dense,
                         bool* done) -> int {
         LP_CK(cudaMemsetAsync(g->loop_ctl, 0, sizeof(LoopCtl), st));
@@ -2121,6 +2124,8 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
     a.gap = ((cross || track) && g->wmode != kFloat && g->margin_skip) ? g->gap : nullptr;
     a.mark_all = 0;
     a.pos = P.pos;
+    a.slots = nullptr;  // (SLPA's memories: lp_slpa_run)
+    a.T = 0;
     a.horizon = INT32_MAX;
     a.mq_out = nullptr;
     a.mq_len = nullptr;
@@ -2352,6 +2357,9 @@ extern "C" int lp_slpa_run(lp_graph* g, const lp_slpa_opts* o, int64_t* labels_o
     else
         pick_fns<kUnit>(o->tie, &run_round, &setup);
     LP_CK(setup(g->device));
+    g->loop_run = g->wmode == kFixed   ? pick_loop<kFixed>(o->tie)
+                  : g->wmode == kFloat ? pick_loop<kFloat>(o->tie)
+                                       : pick_loop<kUnit>(o->tie);
     const size_t cells = (size_t)n * T;
     if (cells > g->slots_cap) {
         dfree(g->slots);

@@ -15,6 +15,8 @@
 // when it holds rows this kernel does not take (longer than the warp table's
 // capacity) or grows past the caller's bound.
 //
+// SLPA's speaking rounds run through the same loop (the spoken label is drawn from the
+// speaker's memory, loop_label).
 // Same evaluation as the class kernels (reference: _rak_seq's tally and
 // _pick_from_tally, rak.py:57-116): every label of the row is tallied
 // (first-sweep singleton flags are not used: a neighbour in a later batch
@@ -40,6 +42,21 @@ struct LoopCtl {
     int32_t rounds;     // rounds run
     int32_t leftover[2];  // rows handed back unevaluated (longer than kLoopMaxDeg), by round parity
 };
+
+// Label that arc k of listener v's row contributes (read through L2: other SMs write x inside the
+// launch).  RAK: the neighbour's working label if it is in an earlier batch, else its sweep-start
+// label (gather_label).  SLPA (a.slots): the speaker's draw from its memory (k_gather_pieces,
+// slpa.py:76-77) -- slot t, the one this round appends, lives in x.
+__device__ __forceinline__ int32_t loop_label(const EvalArgs& a, uint32_t nb, int32_t v, int k) {
+    const int32_t u = (int32_t)(nb >> 2);
+    if (a.slots) {
+        const uint32_t t = a.sweep;
+        const uint32_t filled = t + ((nb & kEarlier) ? 1u : 0u);
+        const uint32_t q = speak_hash(a.seed, t, (uint32_t)v, (uint32_t)k) % filled;
+        return q == t ? __ldcg(a.x + u) : __ldg(a.slots + (size_t)u * a.T + q);
+    }
+    return (nb & kEarlier) ? __ldcg(a.x + u) : __ldg(a.L0 + u);
+}
 
 template <int WM> struct LoopTable {
     STable<WM, kLoopBits> t;
@@ -150,9 +167,7 @@ __global__ void __launch_bounds__(kLoopWarps * 32) k_frontier_loop(EvalArgs a, c
                 int32_t lab = kEmpty;
                 A w = A(0);
                 if (k < d) {
-                    const uint32_t nb = __ldg(a.snbr + beg + k);
-                    const int32_t u = (int32_t)(nb >> 2);
-                    lab = (nb & kEarlier) ? __ldcg(a.x + u) : __ldg(a.L0 + u);
+                    lab = loop_label(a, __ldg(a.snbr + beg + k), v, k);
                     w = arc_weight<WM>(a, beg + k);
                 }
                 bool full = false;
@@ -193,9 +208,7 @@ __global__ void __launch_bounds__(kLoopWarps * 32) k_frontier_loop(EvalArgs a, c
                     bool ok = false;
                     int32_t lab = kEmpty;
                     if (k < d) {
-                        const uint32_t nb = __ldg(a.snbr + beg + k);
-                        const int32_t u = (int32_t)(nb >> 2);
-                        lab = (nb & kEarlier) ? __ldcg(a.x + u) : __ldg(a.L0 + u);
+                        lab = loop_label(a, __ldg(a.snbr + beg + k), v, k);
                         const int h = tab->t.find(lab);
                         ok = h >= 0 && tab->t.weight(h) == b.w && sec_of<TIE>(lab, a.seed, a.sweep, vtx) == b.sec;
                     }

@@ -4,7 +4,7 @@
 #   bytes, L2 hit rate, occupancy per launch), ncu_traffic.json, and --set full captures of
 #   the tally / gather kernels for rmat22, rmat22w, planted and grid.
 #   Usage: bash scripts/round_measure.sh TAG
-TAG=${1:-r2x}
+TAG=${1:-r2c}
 mkdir -p gpurun_out
 O=gpurun_out/${TAG}
 timeout 900 python bench.py --steps 20 --warmup 5 > ${O}_bench_line.json 2> ${O}_bench.err || exit 1
