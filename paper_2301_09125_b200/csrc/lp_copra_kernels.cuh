@@ -74,6 +74,9 @@ struct CopraArgs {
     // work: dense slot range or a vertex queue; spill list for big tables
     const int32_t* __restrict__ queue;  // null: dense over slots [0, S)
     const int32_t* __restrict__ queue_len;
+    int32_t long_row;                   // rows with more contributions (degree x K) skip the warp tiers:
+                                        // one warp walking a hub's 100K contributions is the tail of
+                                        // every round (0 = off)
     int32_t S;
     int32_t* cursor;                    // work cursor (reset per launch)
     int32_t* big;                       // slots whose tables exceed the warp table
@@ -465,8 +468,9 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         if (s < 0) continue;
         const int est = nd_count(__ldg(a.ndist + s));
         int dist = -1;
-        if (est + (est >> 2) <= limit) {
-            const int d = (int)(__ldg(a.soff + s + 1) - __ldg(a.soff + s));
+        const int d = (int)(__ldg(a.soff + s + 1) - __ldg(a.soff + s));
+        const bool long_row = a.long_row > 0 && (long long)d * a.K > a.long_row;
+        if (!long_row && est + (est >> 2) <= limit) {
             int seen = 0;
             bool over = false;
             for_each_contribution(a, s, 0, d, [&](int32_t lab, double val, int c, bool) {

@@ -222,6 +222,8 @@ struct lp_graph {
     size_t cub_tmp_bytes = 0;
     int num_sms = 148;
     int waves = 1;  // dense waves of the cross-batch schedules (LP_WAVES overrides)
+    int copra_long = 32768;  // COPRA rows with more contributions (degree x K) go to the 16-warp team
+                             // (LP_COPRA_LONG, 0 = off; R-MAT-20 k = 8 in place 122 -> 85 ms)
     // frontier loop (lp_loop_kernels.cuh): rounds that evaluate at most loop_rows rows continue on the
     // device in one cooperative launch (LP_LOOP_ROWS, 0 = off); graphs whose rows all fit the loop's
     // warp table, hold at most loop_dense_arcs arcs and average >= 12 arcs a row run their dense rounds
@@ -1438,6 +1440,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
         g->fuse_maxd = atoi(ev) < 0 ? (1 << 30) : atoi(ev);
         g->fuse_forced = true;
     }
+    if (const char* ev = getenv("LP_COPRA_LONG")) g->copra_long = std::max(0, atoi(ev));
     if (const char* ev = getenv("LP_WAVES")) g->waves = std::max(1, std::min(1024, atoi(ev)));
     if (const char* ev = getenv("LP_LOOP_ROWS")) g->loop_rows = std::max(0, atoi(ev));
     if (const char* ev = getenv("LP_LOOP_DENSE_ARCS")) g->loop_dense_arcs = std::max(0, atoi(ev));
@@ -2633,6 +2636,7 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
     a.gcap_contrib = g->gcon;
     a.counters = g->counters;
     a.seed = o->seed;
+    a.long_row = g->copra_long;
     Prof prof;
     prof.on = (o->flags & LP_RAK_PROFILE) != 0;
     prof.pool = &g->event_pool;
@@ -2672,7 +2676,7 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
         LP_CK(cudaMemcpyAsync(g->cbels[c1], g->cbels[c0], cells * sizeof(double), cudaMemcpyDeviceToDevice, st));
         LP_CK(cudaMemcpyAsync(g->csize[c1], g->csize[c0], n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
         LP_CK(cudaMemcpyAsync(g->cbest[c1], g->cbest[c0], n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
-        // dense round over every active slot
+        // dense round over every active slot, then frontier rounds until nothing is marked
         int q = 0;
         a.queue = nullptr;
         a.queue_len = nullptr;

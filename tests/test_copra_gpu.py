@@ -65,6 +65,25 @@ def test_copra_big_rows_use_global_tables(gpu, oracle):
         assert _same_sets(labs, bels, sizes, olabs, obels, osizes), K
 
 
+@pytest.mark.parametrize("long_row", ["0", "64"])
+def test_copra_long_rows_take_the_team_path(gpu, oracle, monkeypatch, long_row):
+    """Rows with more than LP_COPRA_LONG contributions (degree x k) skip the warp tiers for the
+    16-warp team (one warp per hub row was the tail of every round): same sets either way."""
+    from paper_2301_09125_b200 import _lib
+
+    monkeypatch.setenv("LP_COPRA_LONG", long_row)
+    for g in (lp.rmat(12, seed=6), lp.planted_partition(3000, 30, seed=3)):
+        dg = _lib.DeviceGraph(g)  # fresh handle: reads the policy
+        for K, batches in ((4, 0), (8, 16)):
+            best, it, olabs, obels, osizes = oracle.copra(g, max_labels=K, batches=batches, tie=TIE_RANDOM, seed=3,
+                                                          tolerance=0.01, max_iterations=8)
+            p = lp.CopraParams(max_labels=K, seed=3, tolerance=0.01, max_iterations=8, batches=batches)
+            gbest, git, labs, bels, sizes, _, _ = copra_run(g, p, device_graph=dg)
+            assert git == it and np.array_equal(gbest, best), (long_row, K, batches)
+            assert _same_sets(labs, bels, sizes, olabs, obels, osizes), (long_row, K, batches)
+        dg.close()
+
+
 def test_copra_reference_behaviour(gpu):
     """pkg/tests/test_copra.py:9-64."""
     tri = lp.disjoint_cliques(2, 3)

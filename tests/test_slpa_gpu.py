@@ -47,6 +47,32 @@ def test_slpa_matches_oracle(gpu, golden_slpa, golden_rak, oracle, tie, batches)
             assert np.array_equal(labels, want), key
 
 
+@pytest.mark.parametrize("env", [
+    {"LP_LOOP_ROWS": "0"},                       # every round through the class kernels
+    {"LP_LOOP_DENSE_ARCS": "0"},                 # the frontier loop for the tails only
+    {"LP_LOOP_ROWS": "1000000", "LP_LOOP_MAX_QUEUE": "1000000", "LP_LOOP_BLOCKS": "1"},
+])
+def test_slpa_frontier_loop_policies(gpu, golden_slpa, oracle, env, monkeypatch):
+    """SLPA's speaking rounds through the frontier loop (lp_loop_kernels.cuh: the speaker's draw in
+    loop_label) or the class kernels: same memories."""
+    from paper_2301_09125_b200 import _lib
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for name in ("planted_4000", "rmat_12", "gnp_1000"):
+        g = load_graph(golden_slpa, name)
+        dg = _lib.DeviceGraph(g)  # fresh handle: reads the policy
+        for tie, batches in (("scan-first", 0), ("random", 0), ("random", 16)):
+            want, it, slots, filled = _oracle(oracle, g, 12, batches, tie, 2, 0.05)
+            p = lp.SlpaParams(memory_size=12, tolerance=0.05, seed=2, batches=batches, tie=tie)
+            labels, git, gslots, gfilled, _, _ = slpa_run(g, p, device_graph=dg)
+            key = (env, name, tie, batches)
+            assert git == it, key
+            assert np.array_equal(gslots[:, : it + 1], slots[:, : it + 1]), key
+            assert np.array_equal(labels, want), key
+        dg.close()
+
+
 def test_slpa_detect_contract(gpu, golden_slpa, oracle):
     g = load_graph(golden_slpa, "planted_4000")
     p = lp.SlpaParams(memory_size=10, seed=4)
