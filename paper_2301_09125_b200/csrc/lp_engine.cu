@@ -2187,9 +2187,11 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
         // many changed rows costs more than one full round)
         const bool carry = track && it > 1 && last_changed <= (int64_t)(g->carry_frac * (double)P.S);
         if (carry) {
-            // sweep boundary: every neighbour of a vertex whose label changed in the
-            // last sweep is queued (with the changed weight, for the margin test);
-            // only queued vertices can change in this sweep's first round
+            // sweep boundary: a vertex is queued (with the changed weight, for the margin
+            // test) when a neighbour whose sweep-start label it reads -- same or later
+            // batch -- changed in the last sweep; an earlier-batch neighbour's change was
+            // already read through the working labels, and if it moves again this sweep its
+            // marks say so.  Only queued vertices can change in this sweep's first round
             LP_CK(cudaMemsetAsync(g->routes.len, 0, kLenCount * sizeof(int32_t), st));
             LP_CK(cudaMemsetAsync(g->mq_len, 0, sizeof(int32_t), st));
             a.mq_out = g->mq[0];
@@ -2198,7 +2200,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
             if (last_changed * g->push_div <= P.S) {
                 // few changed rows: push from them (one atomic per neighbour)
                 k_sweep_changes<<<g->num_sms * 8, 256, 0, st>>>(a, L0, X, (int32_t)P.S);  // L0 = last result
-                a.mark_all = 1;
+                a.mark_all = 2;
                 const EvalArgs b = marks_mode(g, a, o->tie == kRandom ? g->n : last_changed);
                 k_mark_pieces<<<g->num_sms * 16, 256, 0, st>>>(b);
                 if (o->tie == kRandom) k_mark_ties<<<g->num_sms * 8, 256, 0, st>>>(b, (int32_t)P.S);
@@ -2210,7 +2212,7 @@ static int rak_core(lp_graph* g, const lp_rak_opts* o, const int64_t* order, con
                 k_changed_flags<<<g->num_sms * 8, 256, 0, st>>>(L0, X, g->chg, n);
                 const EvalArgs b = marks_mode(g, a, last_changed);
                 k_pull_marks<<<g->num_sms * 16, 256, 0, st>>>(b, g->chg, P.dslot, P.dk0, P.dcount,
-                                                             g->routes.len + kGatherCursor, 0);
+                                                             g->routes.len + kGatherCursor, 2);
                 if (o->tie == kRandom) k_mark_ties<<<g->num_sms * 8, 256, 0, st>>>(b, (int32_t)P.S);
                 bits_to_queue(g, b);
             }

@@ -128,7 +128,9 @@ struct EvalArgs {
     unsigned long long* gap;            // per slot: lower bound of (winner - runner-up) weight at the
                                         // last evaluation (0 = unknown); null = no margin skipping
     const int32_t* __restrict__ pos;    // vertex -> visit position (wave horizon test)
-    int32_t mark_all;                   // mark every neighbour (sweep boundary), not only later-batch ones
+    int32_t mark_all;                   // 0: mark later-batch neighbours (inside a sweep); 2: the sweep
+                                        // boundary, every neighbour that reads this row's sweep-start
+                                        // label (not the later-batch ones); 1: every neighbour
     int32_t horizon;                    // dense waves: only positions < horizon have been evaluated
                                         // this sweep and need marks; INT32_MAX = all
     int32_t* mq_out;                    // queue of newly marked vertices (this round's writes)
@@ -729,8 +731,11 @@ __global__ void __launch_bounds__(256) k_pull_marks(EvalArgs a, const uint32_t* 
             const bool unit = !(a.gap && a.sw);  // every mark weighs 1
 #pragma unroll
             for (int j = 0; j < J; ++j) {
-                const bool hit = e[j] != 0xffffffffu && (!earlier_only || (nb[j] & kEarlier)) &&
-                                 chg_bit(chg, (int32_t)(nb[j] >> 2));
+                // (earlier_only 1: in-sweep pull from earlier-batch neighbours; 2: the sweep boundary,
+                // every neighbour whose sweep-start label this row reads -- not the earlier-batch ones)
+                const bool from = earlier_only == 1 ? (nb[j] & kEarlier) != 0u
+                                  : earlier_only == 2 ? !(nb[j] & kEarlier) : true;
+                const bool hit = e[j] != 0xffffffffu && from && chg_bit(chg, (int32_t)(nb[j] >> 2));
                 if (!unit) {
                     if (hit) atomicAdd(&sums[wib][rr[j]], mark_weight(a, e[j]));
                     continue;
@@ -812,7 +817,11 @@ __global__ void __launch_bounds__(256) k_mark_pieces(EvalArgs a) {
                 // (no returning atomic: the weight and the bitmap bit are fire-and-forget;
                 // k_bits_to_queue builds the queue -- 2.5x faster than queueing on the
                 // 0 -> nonzero transition of the mark)
-                if (e[j] != 0xffffffffu && (a.mark_all || (nb[j] & kLater)) && needs_mark(a, u)) {
+                // (mark_all 2, the sweep boundary: u reads this row's sweep-start label next sweep unless
+                // it sits in a later batch -- then it reads the working label and this sweep's marks
+                // have already covered the change)
+                const bool want = a.mark_all == 1 || (a.mark_all == 2 ? !(nb[j] & kLater) : (nb[j] & kLater) != 0u);
+                if (e[j] != 0xffffffffu && want && needs_mark(a, u)) {
                     atomicAdd(a.mark + u, mark_weight(a, e[j]));
                     if (a.mbits) atomicOr(a.mbits + (u >> 5), 1u << (u & 31));
                 }
