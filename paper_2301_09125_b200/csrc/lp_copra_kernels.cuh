@@ -74,6 +74,10 @@ struct CopraArgs {
     // work: dense slot range or a vertex queue; spill list for big tables
     const int32_t* __restrict__ queue;  // null: dense over slots [0, S)
     const int32_t* __restrict__ queue_len;
+    int32_t pre_routed;                 // the rows certain to need the team (copra_team_row) were listed
+                                        // by k_copra_route and run beside the warp tiers: those skip them
+    int32_t* route_mark;                // per slot: route_id of the round that listed it (the decision is
+    int32_t route_id;                   // taken once: the estimate it reads moves while the round runs)
     int32_t long_row;                   // rows with more contributions (degree x K) skip the warp tiers:
                                         // one warp walking a hub's 100K contributions is the tail of
                                         // every round (0 = off)
@@ -432,6 +436,27 @@ __device__ void copra_finish(const CopraArgs& a, int32_t s, int cnt, Get get, Co
     copra_commit(a, s, cnt, kk, mylab, myb);
 }
 
+// A row that the warp tiers would only pass on: more contributions than one warp should walk, or
+// an estimate beyond the larger warp table (2048 slots, 3/4 full).
+__device__ __forceinline__ bool copra_team_row(const CopraArgs& a, int32_t s) {
+    const int est = nd_count(__ldg(a.ndist + s));
+    const int d = (int)(__ldg(a.soff + s + 1) - __ldg(a.soff + s));
+    return (a.long_row > 0 && (long long)d * a.K > a.long_row) || est + (est >> 2) > (1 << 11) / 4 * 3;
+}
+
+// The round's team rows, listed up front so that the team kernel starts beside the warp tiers
+// (its largest hub, alone in one block for ~2 ms, is the round's tail) instead of after them.
+__global__ void k_copra_route(CopraArgs a, int32_t* __restrict__ out, int32_t* out_len) {
+    const int items = a.queue ? *a.queue_len : a.S;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < items; idx += gridDim.x * blockDim.x) {
+        const int32_t s = a.queue ? __ldg(a.slot_of + __ldg(a.queue + idx)) : idx;
+        if (s >= 0 && copra_team_row(a, s)) {
+            a.route_mark[s] = a.route_id;
+            out[atomicAdd(out_len, 1)] = s;
+        }
+    }
+}
+
 // Warp per vertex, table of 2^BITS slots in smem.  Input: `in` (slots)
 // when given, else the dense slot range / the vertex queue of the round.
 // Rows whose distinct labels may exceed 3/4 of the table go to `out`.
@@ -466,6 +491,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         if (idx >= items) break;
         const int32_t s = in ? __ldg(in + idx) : (a.queue ? __ldg(a.slot_of + __ldg(a.queue + idx)) : idx);
         if (s < 0) continue;
+        if (a.pre_routed && a.route_mark[s] == a.route_id) continue;  // (on the team's list already)
         const int est = nd_count(__ldg(a.ndist + s));
         int dist = -1;
         const int d = (int)(__ldg(a.soff + s + 1) - __ldg(a.soff + s));

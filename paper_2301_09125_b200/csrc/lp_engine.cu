@@ -222,6 +222,10 @@ struct lp_graph {
     size_t cub_tmp_bytes = 0;
     int num_sms = 148;
     int waves = 1;  // dense waves of the cross-batch schedules (LP_WAVES overrides)
+    bool copra_overlap = true;  // LP_COPRA_OVERLAP=0: the team rows after the warp tiers, on one stream
+    int32_t* croute = nullptr;  // COPRA: the round's pre-routed team rows [n]
+    int32_t* croute_mark = nullptr;  // ... and per slot the id of the round that listed it [n]
+    int32_t copra_rid = 0;           // round ids (never reused by a handle)
     int copra_long = 32768;  // COPRA rows with more contributions (degree x K) go to the 16-warp team
                              // (LP_COPRA_LONG, 0 = off; R-MAT-20 k = 8 in place 122 -> 85 ms)
     // frontier loop (lp_loop_kernels.cuh): rounds that evaluate at most loop_rows rows continue on the
@@ -1069,6 +1073,8 @@ static void destroy_graph(lp_graph* g) {
     dfree(g->ccur);
     dfree(g->cbig);
     dfree(g->cmid);
+    dfree(g->croute);
+    dfree(g->croute_mark);
     dfree(g->gelab);
     dfree(g->geval);
     dfree(g->gefirst);
@@ -1440,6 +1446,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
         g->fuse_maxd = atoi(ev) < 0 ? (1 << 30) : atoi(ev);
         g->fuse_forced = true;
     }
+    if (const char* ev = getenv("LP_COPRA_OVERLAP")) g->copra_overlap = atoi(ev) != 0;
     if (const char* ev = getenv("LP_COPRA_LONG")) g->copra_long = std::max(0, atoi(ev));
     if (const char* ev = getenv("LP_WAVES")) g->waves = std::max(1, std::min(1024, atoi(ev)));
     if (const char* ev = getenv("LP_LOOP_ROWS")) g->loop_rows = std::max(0, atoi(ev));
@@ -2499,6 +2506,9 @@ static int copra_buffers(lp_graph* g, int K) {
         LP_CK(pool_alloc(&g->ccur, 8 * sizeof(int32_t)));
         LP_CK(pool_alloc(&g->cbig, std::max<int64_t>(n, 1) * sizeof(int32_t)));
         LP_CK(pool_alloc(&g->cmid, std::max<int64_t>(n, 1) * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->croute, std::max<int64_t>(n, 1) * sizeof(int32_t)));
+        LP_CK(pool_alloc(&g->croute_mark, std::max<int64_t>(n, 1) * sizeof(int32_t)));
+        LP_CK(cudaMemsetAsync(g->croute_mark, 0, std::max<int64_t>(n, 1) * sizeof(int32_t), g->stream));
     }
     // team scratch: a row sees at most min(n, max_degree * K) distinct labels and
     // max_degree * K contributions; blocks bounded by a 4 GiB budget
@@ -2645,9 +2655,33 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
     LP_CK(cudaMemsetAsync(g->counters, 0, (kCtrCount + 2) * sizeof(unsigned long long), st));
     LP_CK(cudaEventRecord(g->ev0, st));
     int it = 0, rounds = 0;
+    // One round: the team rows known up front (k_copra_route) run on an auxiliary stream beside the
+    // warp tiers; rows the tiers spill (a table that overflowed its estimate) follow in a second,
+    // usually empty, team pass.
+    const bool pre_route = g->copra_overlap && g->aux[1] != nullptr;
+    a.pre_routed = pre_route ? 1 : 0;
     auto launch = [&](int64_t work) -> int {
         LP_CK(cudaMemsetAsync(g->ccur, 0, 8 * sizeof(int32_t), st));
         // ccur: [0] tier-0 cursor [1] big length [2] big cursor [3] mid length [4] mid cursor
+        //       [5] routed team length [6] routed team cursor
+        cudaStream_t sT = g->aux[1];
+        if (pre_route) {
+            a.route_mark = g->croute_mark;
+            a.route_id = ++g->copra_rid;
+            prof.begin(st, -1);
+            k_copra_route<<<grid_for(work, 256, g->num_sms * 8), 256, 0, st>>>(a, g->croute, g->ccur + 5);
+            prof.end(st);
+            cudaEventRecord(g->ev_fork, st);
+            cudaStreamWaitEvent(sT, g->ev_fork, 0);
+            CopraArgs b = a;
+            b.big = g->croute;
+            b.big_len = g->ccur + 5;
+            b.big_cursor = g->ccur + 6;
+            prof.begin(sT, kKHub);
+            k_copra_team<<<g->gblocks, kCopraTeamWarps * 32, copra_team_smem_bytes(), sT>>>(b);
+            prof.end(sT);
+            cudaEventRecord(g->ev_join[1], sT);
+        }
         prof.begin(st, kKWarp);
         k_copra_warp<COPRA_T0><<<grid_for(work, kCopraWarps, g->num_sms * occ), kCopraWarps * 32,
                                  copra_warp_smem_bytes<kCopraBits, kCopraWarps>(), st>>>(
@@ -2657,6 +2691,7 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
         k_copra_warp<COPRA_T1><<<g->num_sms * occ1, 64, copra_warp_smem_bytes<11, 2>(), st>>>(
             a, g->cmid, g->ccur + 3, g->ccur + 4, g->cbig, g->ccur + 1);
         prof.end(st);
+        if (pre_route) cudaStreamWaitEvent(st, g->ev_join[1], 0);  // (the team scratch is per block: one pass at a time)
         prof.begin(st, kKHub);
         k_copra_team<<<g->gblocks, kCopraTeamWarps * 32, copra_team_smem_bytes(), st>>>(a);  // gblocks <= 2 / SM
         prof.end(st);
