@@ -71,6 +71,10 @@ struct CopraArgs {
     unsigned long long* mark;
     int32_t* mq_out;
     int32_t* mq_len;
+    uint32_t* mbits;                    // marked-vertex bitmap: marks are fire-and-forget bit sets and
+                                        // k_bits_to_queue builds the next queue after the round (an append
+                                        // per 32 arcs of every changed row all landed on mq_len); null:
+                                        // queue on the mark's 0 -> nonzero transition (mark_row)
     // work: dense slot range or a vertex queue; spill list for big tables
     const int32_t* __restrict__ queue;  // null: dense over slots [0, S)
     const int32_t* __restrict__ queue_len;
@@ -295,7 +299,17 @@ __device__ void copra_commit(const CopraArgs& a, int32_t s, int cnt, int kk, int
             a.bestX[v] = bl;
         }
         __threadfence();
-        if (a.mark) mark_row(a, beg, d, lane, 32);
+        if (a.mark && a.mbits) {
+            for (int k = lane; k < d; k += 32) {
+                const uint32_t nb = __ldg(a.snbr + beg + k);
+                if (nb & kLater) {
+                    const int32_t u = (int32_t)(nb >> 2);
+                    atomicOr(a.mbits + (u >> 5), 1u << (u & 31));
+                }
+            }
+        } else if (a.mark) {
+            mark_row(a, beg, d, lane, 32);
+        }
     }
     if (lane == 0) a.ndist[s] = cnt;
 }

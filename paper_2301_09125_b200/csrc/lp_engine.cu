@@ -222,6 +222,7 @@ struct lp_graph {
     size_t cub_tmp_bytes = 0;
     int num_sms = 148;
     int waves = 1;  // dense waves of the cross-batch schedules (LP_WAVES overrides)
+    bool copra_bitmap = true;   // LP_COPRA_BITMAP=0: COPRA marks queue on the mark's transition (mark_row)
     bool copra_overlap = true;  // LP_COPRA_OVERLAP=0: the team rows after the warp tiers, on one stream
     int32_t* croute = nullptr;  // COPRA: the round's pre-routed team rows [n]
     int32_t* croute_mark = nullptr;  // ... and per slot the id of the round that listed it [n]
@@ -1446,6 +1447,7 @@ extern "C" int lp_graph_create(int64_t n, int64_t m, const int64_t* offsets, con
         g->fuse_maxd = atoi(ev) < 0 ? (1 << 30) : atoi(ev);
         g->fuse_forced = true;
     }
+    if (const char* ev = getenv("LP_COPRA_BITMAP")) g->copra_bitmap = atoi(ev) != 0;
     if (const char* ev = getenv("LP_COPRA_OVERLAP")) g->copra_overlap = atoi(ev) != 0;
     if (const char* ev = getenv("LP_COPRA_LONG")) g->copra_long = std::max(0, atoi(ev));
     if (const char* ev = getenv("LP_WAVES")) g->waves = std::max(1, std::min(1024, atoi(ev)));
@@ -2649,6 +2651,7 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
     a.counters = g->counters;
     a.seed = o->seed;
     a.long_row = g->copra_long;
+    a.mbits = (cross && g->copra_bitmap) ? g->mbits : nullptr;
     Prof prof;
     prof.on = (o->flags & LP_RAK_PROFILE) != 0;
     prof.pool = &g->event_pool;
@@ -2695,6 +2698,13 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
         prof.begin(st, kKHub);
         k_copra_team<<<g->gblocks, kCopraTeamWarps * 32, copra_team_smem_bytes(), st>>>(a);  // gblocks <= 2 / SM
         prof.end(st);
+        if (a.mbits) {
+            // the vertices this round marked -> the next round's queue (bits cleared)
+            const int64_t nwords = n / 32 + 1;
+            prof.begin(st, -1);
+            k_bits_to_queue<<<grid_for(nwords, 256, g->num_sms * 8), 256, 0, st>>>(g->mbits, nwords, a.mq_out, a.mq_len);
+            prof.end(st);
+        }
         ++rounds;
         return LP_OK;
     };
@@ -2723,9 +2733,11 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
         if (P.S > 0)
             if (int rc = launch(P.S)) return rc;
         while (cross && P.S > 0) {
-            prof.begin(st, -1);
-            k_clear_marks<<<g->num_sms * 4, 256, 0, st>>>(g->mq[q], g->mq_len + q, g->mark);
-            prof.end(st);
+            if (!a.mbits) {
+                prof.begin(st, -1);
+                k_clear_marks<<<g->num_sms * 4, 256, 0, st>>>(g->mq[q], g->mq_len + q, g->mark);
+                prof.end(st);
+            }
             LP_CK(cudaMemcpyAsync(g->h_len, g->mq_len + q, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
             LP_CK(cudaStreamSynchronize(st));
             const int32_t work = g->h_len[0];
