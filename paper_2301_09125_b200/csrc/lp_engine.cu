@@ -814,6 +814,9 @@ template <int WM, int TIE> struct Launcher {
         int max_rounds = 1 << 20;
         void* args[] = {&b, &list0, &list0_len, &list0_cnt, &q0, &q1, &first_dst, &slot_of, &ctl, &mq_len, &dense, &max_queue,
                         &max_rounds};
+#ifdef LP_LOOP_TEST_FAIL
+        return cudaErrorCooperativeLaunchTooLarge;  // (test build: the caller's fallback path)
+#endif
         const int per_sm = g->loop_blocks_per_sm > 0 ? std::min(g->loop_blocks_per_sm, occ_loop) : occ_loop;
         return cudaLaunchCooperativeKernel((const void*)k_frontier_loop<WM, TIE>, dim3(g->num_sms * per_sm),
                                            dim3(kLoopWarps * 32), args, loop_smem_bytes<WM>(), g->stream);
@@ -1762,9 +1765,9 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
     // The frontier loop: the rounds from here on run in one cooperative launch (lp_loop_kernels.cuh)
     // until a round queues nothing (*done) or the queue comes back (rows longer than the loop's
     // table, or more than loop_max_queue of them): then the class kernels route mq[q] as usual.
-    const bool loop_ok = g->loop_run && cross && a.mark && g->loop_rows > 0;  // (RAK and SLPA: a.slots)
+    bool loop_ok = g->loop_run && cross && a.mark && g->loop_rows > 0;  // (RAK and SLPA: a.slots)
     // (warp per row: not for graphs of very short rows -- the grid's 4-arc rows stay thread per row)
-    const bool loop_dense = loop_ok && g->max_degree <= kLoopMaxDeg && P.m_active <= g->loop_dense_arcs &&
+    bool loop_dense = loop_ok && g->max_degree <= kLoopMaxDeg && P.m_active <= g->loop_dense_arcs &&
                             P.m_active >= 12 * P.S;
     auto run_loop = [&](const int32_t* list0, const int32_t* list0_len, int list0_cnt, int first_dst, bool dense,
                         bool* done) -> int {
@@ -1773,7 +1776,15 @@ static int solve_sweep(lp_graph* g, EvalArgs& a, bool cross, round_fn run_round,
         const cudaError_t e = g->loop_run(g, a, list0, list0_len, list0_cnt, first_dst, dense ? 1 : 0,
                                           loop_dense ? INT32_MAX : g->loop_max_queue);  // (every row is the loop's)
         prof->end(st);
-        LP_CK(e);
+        if (e != cudaSuccess) {
+            // no cooperative launch here (the grid must be co-resident: a device shared through MPS,
+            // a debugger ...): nothing ran; this handle keeps to the class kernels from now on
+            cudaGetLastError();
+            g->loop_rows = 0;
+            loop_ok = loop_dense = false;
+            *done = false;
+            return LP_OK;
+        }
         LP_CK(cudaMemcpyAsync(g->h_loop, g->loop_ctl, sizeof(LoopCtl), cudaMemcpyDeviceToHost, st));
         LP_CK(cudaStreamSynchronize(st));
         *rounds += g->h_loop->rounds;
@@ -2661,7 +2672,9 @@ extern "C" int lp_copra_run(lp_graph* g, const lp_copra_opts* o, int64_t* labs_o
     // One round: the team rows known up front (k_copra_route) run on an auxiliary stream beside the
     // warp tiers; rows the tiers spill (a table that overflowed its estimate) follow in a second,
     // usually empty, team pass.
-    const bool pre_route = g->copra_overlap && g->aux[1] != nullptr;
+    // (in-place schedules only: their rounds end in the tail of a few hub rows; a synchronous
+    // sweep's team pass is throughput-bound and runs slower beside the warp tiers -- measured)
+    const bool pre_route = g->copra_overlap && cross && g->aux[1] != nullptr;
     a.pre_routed = pre_route ? 1 : 0;
     auto launch = [&](int64_t work) -> int {
         LP_CK(cudaMemsetAsync(g->ccur, 0, 8 * sizeof(int32_t), st));
