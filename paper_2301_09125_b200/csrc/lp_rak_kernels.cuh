@@ -2164,7 +2164,9 @@ __global__ void __launch_bounds__(WarpClass<WC>::kWarps * 32, WC == 0 && WM == k
     constexpr int kWarpCap = WT::kCap;
     constexpr int kWarpsPerBlock = WarpClass<WC>::kWarps;
     constexpr int HB = 1 << kWarpBits;
-    constexpr int U = 4;  // 32-arc chunks gathered per step
+    // 32-arc chunks gathered per step (the two-pass first-sweep instantiation keeps fewer in flight:
+    // measured 2.7% faster per exact R-MAT-22 detection at 2 than at 4, 1 and 3 in between)
+    constexpr int U = TWO ? 2 : 4;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
